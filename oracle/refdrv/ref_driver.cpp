@@ -1,0 +1,399 @@
+// ref_driver.cpp -- builds the REFERENCE's own matrix-free path into
+// oracle/_ref/libehmg_ref.so (test infrastructure only).
+//
+// Compiled by oracle/Makefile directly against the unmodified headers under
+// /root/reference/proj/include (grid, media, stencils, operator, vanka,
+// transfer, krylov). Eigen is absent from this image, so shim/Eigen holds
+// declaration-only forward declarations: the Eigen-typed templates (sparse
+// assembly, SparseLU, Kaczmarz) are parsed but never instantiated. The
+// multigrid cycle itself (multigrid.hpp:217 cycle_at) cannot be instantiated
+// without Eigen's SparseLU, so it is restated here around the reference's
+// own smoother/operator/transfer calls with an exact dense LU coarsest solve
+// (the reference's CoarseSolverKind::lu semantics, multigrid.hpp:97).
+//
+// Nothing from this file ships in the product; tests/ and bench.py's
+// reference arm load it to pin the oracle and time the reference CPU path.
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+// Expose VankaSmoother's factorization cache for exact cache parity checks.
+#define private public
+#include "ehmg/krylov.hpp"
+#include "ehmg/operator.hpp"
+#include "ehmg/transfer.hpp"
+#include "ehmg/vanka.hpp"
+#undef private
+
+using namespace ehmg;
+using Cd = std::complex<double>;
+
+namespace {
+
+template <int Dim> Idx<Dim> to_idx(const int* d) {
+  Idx<Dim> r{};
+  for (int a = 0; a < Dim; ++a) r[a] = d[a];
+  return r;
+}
+
+template <int Dim>
+MediaModel<Dim> media_of(const StaggeredGrid<Dim>& g, const double* lam, const double* mu,
+                         const double* rho, const double* gam) {
+  MediaModel<Dim> m;
+  size_t n = size_t(g.n_cells());
+  m.lambda.assign(lam, lam + n);
+  m.mu.assign(mu, mu + n);
+  m.rho.assign(rho, rho + n);
+  m.gamma.assign(gam, gam + n);
+  return m;
+}
+
+template <int Dim> void load(FieldVector<double, Dim>& f, const Cd* src) {
+  size_t o = 0;
+  for (auto& c : f.comp)
+    for (auto& z : c) z = src[o++];
+}
+template <int Dim> void store(const FieldVector<double, Dim>& f, Cd* dst) {
+  size_t o = 0;
+  for (auto& c : f.comp)
+    for (auto& z : c) dst[o++] = z;
+}
+
+struct Media {
+  const double *lam, *mu, *rho, *gam;
+};
+
+// ---- exact coarsest solve (dense LU on reference unit-probe rows) -------
+struct DenseLU {
+  std::int64_t n = 0;
+  std::vector<Cd> a;  // column-major
+  std::vector<std::int64_t> piv;
+  void factor() {
+    piv.resize(size_t(n));
+    for (std::int64_t k = 0; k < n; ++k) {
+      std::int64_t p = k;
+      double best = std::abs(a[size_t(k + k * n)]);
+      for (std::int64_t i = k + 1; i < n; ++i)
+        if (std::abs(a[size_t(i + k * n)]) > best) best = std::abs(a[size_t(i + k * n)]), p = i;
+      piv[size_t(k)] = p;
+      if (p != k)
+        for (std::int64_t j = 0; j < n; ++j) std::swap(a[size_t(k + j * n)], a[size_t(p + j * n)]);
+      Cd d = a[size_t(k + k * n)];
+      for (std::int64_t i = k + 1; i < n; ++i) a[size_t(i + k * n)] /= d;
+      for (std::int64_t j = k + 1; j < n; ++j) {
+        Cd akj = a[size_t(k + j * n)];
+        if (akj == Cd(0)) continue;
+        for (std::int64_t i = k + 1; i < n; ++i) a[size_t(i + j * n)] -= a[size_t(i + k * n)] * akj;
+      }
+    }
+  }
+  void solve(std::vector<Cd>& b) const {
+    for (std::int64_t k = 0; k < n; ++k) std::swap(b[size_t(k)], b[size_t(piv[size_t(k)])]);
+    for (std::int64_t j = 0; j < n; ++j)
+      for (std::int64_t i = j + 1; i < n; ++i) b[size_t(i)] -= a[size_t(i + j * n)] * b[size_t(j)];
+    for (std::int64_t j = n - 1; j >= 0; --j) {
+      b[size_t(j)] /= a[size_t(j + j * n)];
+      for (std::int64_t i = 0; i < j; ++i) b[size_t(i)] -= a[size_t(i + j * n)] * b[size_t(j)];
+    }
+  }
+};
+
+template <int Dim> DenseLU dense_lu(const OpData<double, Dim>& D) {
+  std::array<std::int64_t, Dim + 2> off{};
+  for (int c = 0; c <= Dim; ++c)
+    off[size_t(c) + 1] = off[size_t(c)] + (c < Dim ? D.faceb[size_t(c)].size() : D.cellb.size());
+  DenseLU L;
+  L.n = off[Dim + 1];
+  L.a.assign(size_t(L.n * L.n), Cd(0));
+  for (int cc = 0; cc <= Dim; ++cc) {
+    const Box<Dim>& cb = cc < Dim ? D.faceb[size_t(cc)] : D.cellb;
+    for_each(cb, [&](const Idx<Dim>& ci) {
+      std::int64_t col = off[size_t(cc)] + cb.lin(ci);
+      UnitAcc<double, Dim> acc{D, cc, ci};
+      for (int rc = 0; rc <= Dim; ++rc) {
+        const Box<Dim>& rb = rc < Dim ? D.faceb[size_t(rc)] : D.cellb;
+        std::array<int, 3> lo{-2, -2, Dim == 3 ? -2 : 0}, hi{2, 2, Dim == 3 ? 2 : 0};
+        for (int o2 = lo[2]; o2 <= hi[2]; ++o2)
+          for (int o1 = lo[1]; o1 <= hi[1]; ++o1)
+            for (int o0 = lo[0]; o0 <= hi[0]; ++o0) {
+              Idx<Dim> r = ci;
+              r[0] += o0;
+              r[1] += o1;
+              if constexpr (Dim == 3) r[2] += o2;
+              if (!rb.contains(r)) continue;
+              Cd v = rc < Dim ? row_u(D, rc, r, acc) : row_p(D, r, acc);
+              L.a[size_t(off[size_t(rc)] + rb.lin(r) + col * L.n)] = v;
+            }
+      }
+    });
+  }
+  L.factor();
+  return L;
+}
+
+// ---- restated cycle around the reference components --------------------
+template <int Dim> struct RefMG {
+  using F = FieldVector<double, Dim>;
+  struct Lev {
+    StaggeredGrid<Dim> g;
+    OpData<double, Dim> D;
+    VankaSmoother<double, Dim> sm;
+    F r, t, bc, ec;
+  };
+  std::vector<std::unique_ptr<Lev>> L;
+  DenseLU lu;
+  int cycle, nu1, nu2;
+  double w;
+  VankaMode mode;
+  SweepOrder order;
+
+  RefMG(StaggeredGrid<Dim> g, MediaModel<Dim> m, OperatorParams par, int nl, int cyc, int n1,
+        int n2, double w_, int vmode, int sweep)
+      : cycle(cyc), nu1(n1), nu2(n2), w(w_), mode(vmode ? VankaMode::economic : VankaMode::full),
+        order(sweep ? SweepOrder::red_black : SweepOrder::lexicographic) {
+    for (int l = 0; l < nl; ++l) {
+      auto lv = std::make_unique<Lev>(
+          Lev{g, make_opdata<double>(g, m, par), VankaSmoother<double, Dim>(mode), F(g), F(g), F(g), F(g)});
+      L.push_back(std::move(lv));
+      if (l + 1 < nl) {
+        m = coarsen_media(g, m);
+        g = coarsen_grid(g);
+      }
+    }
+    lu = dense_lu(L.back()->D);
+  }
+  void cyc(int l, const F& b, F& x) {
+    const int nl = int(L.size());
+    if (l + 1 == nl) {
+      std::vector<Cd> v;
+      for (auto& c : b.comp) v.insert(v.end(), c.begin(), c.end());
+      lu.solve(v);
+      size_t o = 0;
+      for (auto& c : x.comp)
+        for (auto& z : c) z = v[o++];
+      return;
+    }
+    Lev& lev = *L[size_t(l)];
+    Lev& nx = *L[size_t(l) + 1];
+    for (int s = 0; s < nu1; ++s) lev.sm.sweep(lev.D, b, x, w, order);
+    apply_mixed_operator(lev.D, x, lev.t);
+    lev.r = b;
+    axpy(Cd(-1), lev.t, lev.r);
+    nx.bc = restrict_field(lev.g, nx.g, lev.r, false);
+    nx.ec.set_zero();
+    cyc(l + 1, nx.bc, nx.ec);
+    if (cycle == 2 && l + 2 != nl) cyc(l + 1, nx.bc, nx.ec);
+    F corr = prolong_field(lev.g, nx.g, nx.ec, false);
+    axpy(Cd(1), corr, x);
+    for (int s = 0; s < nu2; ++s) lev.sm.sweep(lev.D, b, x, w, order);
+  }
+};
+
+template <int Dim>
+int apply_t(const int* dims, double h, Media M, double beta, double omega, double alpha,
+            const Cd* x, Cd* y, int schur) {
+  StaggeredGrid<Dim> g(to_idx<Dim>(dims), h);
+  auto D = make_opdata<double, Dim>(g, media_of<Dim>(g, M.lam, M.mu, M.rho, M.gam),
+                                    {beta, omega, alpha, false});
+  FieldVector<double, Dim> X(g), Y(g);
+  load(X, x);
+  if (schur) schur_eliminate_pressure(D, X, Y);
+  else apply_mixed_operator(D, X, Y);
+  store(Y, y);
+  return 0;
+}
+
+template <int Dim>
+int vanka_t(const int* dims, double h, Media M, double beta, double omega, double alpha, int mode,
+            int order, double w, int nsweeps, const Cd* b, Cd* x, Cd* cache_out) {
+  StaggeredGrid<Dim> g(to_idx<Dim>(dims), h);
+  auto D = make_opdata<double, Dim>(g, media_of<Dim>(g, M.lam, M.mu, M.rho, M.gam),
+                                    {beta, omega, alpha, false});
+  VankaSmoother<double, Dim> sm(mode ? VankaMode::economic : VankaMode::full);
+  FieldVector<double, Dim> B(g), X(g);
+  load(B, b);
+  load(X, x);
+  for (int s = 0; s < nsweeps; ++s)
+    sm.sweep(D, B, X, w, order ? SweepOrder::red_black : SweepOrder::lexicographic);
+  sm.ensure_cache(D);
+  store(X, x);
+  if (cache_out) std::copy(sm.cache_.begin(), sm.cache_.end(), cache_out);
+  return 0;
+}
+
+template <int Dim> int transfer_t(const int* dims_f, int restricting, const Cd* in, Cd* out) {
+  StaggeredGrid<Dim> gf(to_idx<Dim>(dims_f), 1.0);
+  StaggeredGrid<Dim> gc = coarsen_grid(gf);
+  FieldVector<double, Dim> xi(restricting ? gf : gc);
+  load(xi, in);
+  FieldVector<double, Dim> xo =
+      restricting ? restrict_field(gf, gc, xi, false) : prolong_field(gf, gc, xi, false);
+  store(xo, out);
+  return 0;
+}
+
+template <int Dim> int coarsen_t(const int* dims_f, const double* in, double* out) {
+  StaggeredGrid<Dim> gf(to_idx<Dim>(dims_f), 1.0);
+  MediaModel<Dim> m = MediaModel<Dim>::homogeneous(gf, 1, 1, 1, 0);
+  m.lambda.assign(in, in + gf.n_cells());
+  auto mc = coarsen_media(gf, m);
+  std::copy(mc.lambda.begin(), mc.lambda.end(), out);
+  return 0;
+}
+
+template <int Dim>
+int mg_t(const int* dims, double h, Media M, double beta, double omega, double alpha, int nl,
+         int cyc, int nu1, int nu2, double w, int vmode, int sweep, int ncycles, const Cd* b, Cd* x,
+         double* seconds) {
+  StaggeredGrid<Dim> g(to_idx<Dim>(dims), h);
+  RefMG<Dim> mg(g, media_of<Dim>(g, M.lam, M.mu, M.rho, M.gam), {beta, omega, alpha, false}, nl,
+                cyc, nu1, nu2, w, vmode, sweep);
+  for (auto& lv : mg.L) lv->sm.ensure_cache(lv->D);
+  FieldVector<double, Dim> B(g), X(g);
+  load(B, b);
+  load(X, x);
+  auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < ncycles; ++i) mg.cyc(0, B, X);
+  if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  store(X, x);
+  return 0;
+}
+
+template <int Dim>
+int solve_t(const int* dims, double h, Media M, double beta, double omega, double alpha, int nl,
+            int cyc, int nu1, int nu2, double w, int vmode, int sweep, int restart, int max_it,
+            double rtol, const Cd* b, Cd* x, int* iters, int* status, double* relres,
+            double* hist, int hist_cap, int* n_hist) {
+  StaggeredGrid<Dim> g(to_idx<Dim>(dims), h);
+  auto media = media_of<Dim>(g, M.lam, M.mu, M.rho, M.gam);
+  RefMG<Dim> mg(g, media, {beta, omega, alpha, false}, nl, cyc, nu1, nu2, w, vmode, sweep);
+  auto D0 = make_opdata<double, Dim>(g, media, {beta, omega, 0.0, false});
+  using F = FieldVector<double, Dim>;
+  F B(g), X(g);
+  load(B, b);
+  load(X, x);
+  KrylovOptions ko;
+  ko.restart = restart;
+  ko.max_iterations = max_it;
+  ko.rtol = rtol;
+  auto A = [&](const F& in, F& out) { apply_mixed_operator(D0, in, out); };
+  auto Mp = [&](const F& r, F& z) {
+    z.set_zero();
+    mg.cyc(0, r, z);
+  };
+  KrylovResult res = fgmres(A, Mp, B, X, ko);
+  store(X, x);
+  *iters = res.iterations;
+  *status = int(res.status);
+  *relres = res.relres;
+  int nh = std::min<int>(hist_cap, int(res.history.size()));
+  for (int i = 0; i < nh; ++i) hist[i] = res.history[size_t(i)];
+  *n_hist = int(res.history.size());
+  return 0;
+}
+
+template <class F> int guard(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_apply(int ndim, const int* dims, double h, const double* lam, const double* mu,
+              const double* rho, const double* gam, double beta, double omega, double alpha,
+              const Cd* x, Cd* y) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    return ndim == 2 ? apply_t<2>(dims, h, M, beta, omega, alpha, x, y, 0)
+                     : apply_t<3>(dims, h, M, beta, omega, alpha, x, y, 0);
+  });
+}
+
+int ref_schur_apply(int ndim, const int* dims, double h, const double* lam, const double* mu,
+                    const double* rho, const double* gam, double beta, double omega, double alpha,
+                    const Cd* x, Cd* y) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    return ndim == 2 ? apply_t<2>(dims, h, M, beta, omega, alpha, x, y, 1)
+                     : apply_t<3>(dims, h, M, beta, omega, alpha, x, y, 1);
+  });
+}
+
+int ref_vanka(int ndim, const int* dims, double h, const double* lam, const double* mu,
+              const double* rho, const double* gam, double beta, double omega, double alpha,
+              int mode, int order, double w, int nsweeps, const Cd* b, Cd* x, Cd* cache_out) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    return ndim == 2 ? vanka_t<2>(dims, h, M, beta, omega, alpha, mode, order, w, nsweeps, b, x, cache_out)
+                     : vanka_t<3>(dims, h, M, beta, omega, alpha, mode, order, w, nsweeps, b, x, cache_out);
+  });
+}
+
+int ref_transfer(int ndim, const int* dims_f, int restricting, const Cd* in, Cd* out) {
+  return guard([&] {
+    return ndim == 2 ? transfer_t<2>(dims_f, restricting, in, out)
+                     : transfer_t<3>(dims_f, restricting, in, out);
+  });
+}
+
+int ref_coarsen(int ndim, const int* dims_f, const double* in, double* out) {
+  return guard([&] { return ndim == 2 ? coarsen_t<2>(dims_f, in, out) : coarsen_t<3>(dims_f, in, out); });
+}
+
+int ref_attenuation(int ndim, const int* dims, double gamma_phys, int L, double gamma_max,
+                    int absorb_top, double* out) {
+  return guard([&] {
+    SpongeConfig s;
+    s.layer_width = L;
+    s.gamma_max = gamma_max;
+    s.absorb_top = absorb_top != 0;
+    std::vector<double> v;
+    if (ndim == 2) v = build_attenuation_profile(StaggeredGrid<2>(to_idx<2>(dims), 1.0), gamma_phys, s);
+    else v = build_attenuation_profile(StaggeredGrid<3>(to_idx<3>(dims), 1.0), gamma_phys, s);
+    std::copy(v.begin(), v.end(), out);
+    return 0;
+  });
+}
+
+int ref_mg_cycles(int ndim, const int* dims, double h, const double* lam, const double* mu,
+                  const double* rho, const double* gam, double beta, double omega, double alpha,
+                  int nl, int cyc, int nu1, int nu2, double w, int vmode, int sweep, int ncycles,
+                  const Cd* b, Cd* x, double* seconds) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    return ndim == 2 ? mg_t<2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, ncycles, b, x, seconds)
+                     : mg_t<3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, ncycles, b, x, seconds);
+  });
+}
+
+int ref_solve(int ndim, const int* dims, double h, const double* lam, const double* mu,
+              const double* rho, const double* gam, double beta, double omega, double alpha, int nl,
+              int cyc, int nu1, int nu2, double w, int vmode, int sweep, int restart, int max_it,
+              double rtol, const Cd* b, Cd* x, int* iters, int* status, double* relres,
+              double* hist, int hist_cap, int* n_hist) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    return ndim == 2 ? solve_t<2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist)
+                     : solve_t<3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist);
+  });
+}
+
+}  // extern "C"
