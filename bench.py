@@ -1,0 +1,438 @@
+"""Headline benchmark: V-cycles/s (complex128) of the shifted-Laplacian
+V(2,2) preconditioner at 257^3 nodes (256^3 cells) 3D elastic Helmholtz,
+plus stencil GDOF/s and FGMRES time-to-1e-6 (BASELINE.json configs[2]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one preconditioner application z = M r (5 levels, 256^3 -> 16^3,
+full red-black Vanka V(2,2), exact coarsest solve). `value` times K steps on
+HBM-resident buffers with CUDA events on the solver stream; `e2e` times the
+same call through the public API with pinned host buffers (H2D of r and D2H
+of z inside the timed region). Fields are 1.08 GB each, far larger than the
+126 MB L2, so no explicit flush is needed between steps.
+N > 1: one process per GPU, each running its own replica of the workload
+(weak scaling; the z-slab decomposed hierarchy is DESIGN.md row (e)).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# workload: BASELINE.json configs[2]
+N_CELLS = 256
+LEVELS = 5
+BETA = 2.0 / 3.0
+ALPHA = 0.5          # shift (the 0.1 default stalls at 5 levels)
+DAMPING = 0.25       # experiments.hpp:221 default for >= 4 levels
+SPONGE = 24
+GAMMA_PHYS = 0.01
+LAM, MU, RHO = 2.0, 1.0, 1.0   # cs = 1, cp = 2
+PPW = 10.0
+
+
+def metric_name():
+    return "V-cycles/s (complex128) at 257^3 3D elastic Helmholtz"
+
+
+def workload_config(n):
+    return {"workload": f"configs[2]: 3D homogeneous {n + 1}^3 nodes ({n}^3 cells), h=1/{n}",
+            "media": "lambda=2 mu=1 rho=1 (cs=1, cp=2)", "omega": f"2*pi/({PPW:g}h)",
+            "sponge_cells": SPONGE, "gamma_phys": GAMMA_PHYS, "beta": BETA, "alpha": ALPHA,
+            "cycle": "V(2,2) full red-black Vanka", "levels": LEVELS,
+            "coarsest": f"{n >> (LEVELS - 1)}^3 exact (LU-derived inverse in HBM)",
+            "damping": DAMPING, "source": "unit point source, x-component, centre",
+            "krylov": "FGMRES(10), rtol 1e-6", "l2": "inputs (1.08 GB/field) larger than L2"}
+
+
+# ------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        cmd = ["nvidia-smi", "-i", str(self.index),
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+               "clocks_event_reasons.sw_power_cap,power.draw", "--format=csv,noheader,nounits",
+               "-lms", "200"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+        except OSError:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.rows.append([s.strip() for s in line.split(",")])
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for nm, v in zip(names, r[2:6]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- dist
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "b200" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------- roofline bytes
+def level_dims(n, l):
+    return (n >> l,) * 3
+
+
+def ndofs(d):
+    c = d[0] * d[1] * d[2]
+    return c + sum(c // d[a] * (d[a] + 1) for a in range(3))
+
+
+def alg_bytes(kernel, n, level):
+    """Algorithmic HBM bytes of one launch at a level."""
+    d = level_dims(n, level)
+    C = d[0] * d[1] * d[2]
+    N = ndofs(d)
+    Nu = N - C
+    if kernel == "residual":
+        return 16 * 3 * N + 32 * C
+    if kernel == "apply":
+        return 16 * 2 * N + 32 * C
+    if kernel == "vanka_corr":     # x neighbourhood, b at owned DOFs, media, cache + delta of half the cells
+        return 16 * N + 16 * (Nu + C // 2) + 32 * C + 16 * 25 * (C // 2) + 16 * 7 * (C // 2)
+    if kernel == "vanka_apply":
+        return 16 * 7 * (C // 2) + 2 * 16 * (Nu + C // 2)
+    if kernel == "restrict":
+        return 16 * N + 16 * ndofs(level_dims(n, level + 1))
+    if kernel == "prolong_add":
+        return 16 * ndofs(level_dims(n, level + 1)) + 2 * 16 * N
+    if kernel == "coarse_solve":
+        return 16 * N * N + 32 * N
+    return 0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------- CPU baseline
+REF_SAMPLE_N = 32
+REF_SAMPLE_LEVELS = 3
+
+
+def level_work(n, levels):
+    """Sum of DOFs over the smoothed levels: V-cycle work scales with it."""
+    return sum(ndofs(level_dims(n, l)) for l in range(levels - 1))
+
+
+def cpu_sample_media(n):
+    from oracle import oracle as O
+    c = n ** 3
+    gam = O.attenuation((n, n, n), GAMMA_PHYS, max(1, SPONGE * n // N_CELLS))
+    return O.Media(np.full(c, LAM), np.full(c, MU), np.full(c, RHO), gam)
+
+
+def run_cpu_sample(steps, threads):
+    """Reference V(2,2) cycles (oracle/_ref = the reference headers) on a
+    REF_SAMPLE_N^3 cube with the same media/omega-per-h recipe, `threads`
+    independent replicas in parallel. Returns (V-cycles/s extrapolated to
+    N_CELLS^3, kind, raw seconds per sample cycle)."""
+    from oracle import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    n = REF_SAMPLE_N
+    dims = (n, n, n)
+    m = cpu_sample_media(n)
+    omega = 2 * math.pi / (PPW / n)
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(O.n_dofs(dims)) + 1j * rng.standard_normal(O.n_dofs(dims))
+    secs = []
+    lock = threading.Lock()
+
+    def work():
+        if kind == "reference":
+            _, s = O.ref_mg_cycles(dims, 1.0 / n, m, BETA, omega, ALPHA, b, np.zeros_like(b),
+                                   ncycles=steps, n_levels=REF_SAMPLE_LEVELS, cycle="v", nu1=2,
+                                   nu2=2, damping=DAMPING)
+        else:
+            mg = O.MG(dims, 1.0 / n, m, BETA, omega, ALPHA, n_levels=REF_SAMPLE_LEVELS, cycle="v",
+                      nu1=2, nu2=2, damping=DAMPING)
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                mg.precondition(b)
+            s = time.perf_counter() - t0
+        with lock:
+            secs.append(s / steps)
+
+    ths = [threading.Thread(target=work) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    per_cycle = max(secs)
+    rate_sample = threads / per_cycle
+    scale = level_work(REF_SAMPLE_N, REF_SAMPLE_LEVELS) / level_work(N_CELLS, LEVELS)
+    return rate_sample * scale, kind, per_cycle, wall
+
+
+# ------------------------------------------------------------ b200 arm
+def build_problem(n, E):
+    g = E.StaggeredGrid((n, n, n), 1.0 / n)
+    med = E.MediaModel.homogeneous(g, LAM, MU, RHO, GAMMA_PHYS)
+    med.gamma = E.build_attenuation_profile(g, GAMMA_PHYS, E.SpongeConfig(SPONGE))
+    omega = 2 * math.pi * 1.0 / (PPW * g.h)
+    return g, med, omega
+
+
+def run_b200(args, ws, rank, local):
+    import torch
+    import paper_2307_03242_b200 as E
+    torch.cuda.set_device(local)
+    E.lib().ehmg_set_device(local)
+    n = args.n
+    g, med, omega = build_problem(n, E)
+    opt = E.MgOptions(n_levels=LEVELS, cycle="v", nu1=2, nu2=2, damping=DAMPING,
+                      vanka_mode="full", sweep="red_black")
+    t0 = time.perf_counter()
+    mg = E.Multigrid(g, med, E.OperatorParams(BETA, omega, ALPHA), opt)
+    D0 = E.make_opdata(g, med, E.OperatorParams(BETA, omega, 0.0))
+    setup_s = time.perf_counter() - t0
+    N = g.n_dofs()
+    b = torch.from_numpy(E.make_point_source(g, 0, (n // 2, n // 2, n // 2))).cuda()
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    r = torch.randn(N, dtype=torch.complex128, device="cuda", generator=gen)
+    z = torch.zeros(N, dtype=torch.complex128, device="cuda")
+    stream = torch.cuda.ExternalStream(mg.stream)
+
+    # warm-up
+    for _ in range(args.warmup):
+        mg.precondition(r, z)
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        mg.precondition(r, z)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    barrier(ws)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ws, ms)
+    value = ws * args.steps / (ms_max / 1e3)
+
+    # profile pass (same steps, per-launch events) -> dominant kernel
+    E.profile_enable(True)
+    for _ in range(args.steps):
+        mg.precondition(r, z)
+    torch.cuda.synchronize()
+    prof = E.profile_report()
+    E.profile_enable(False)
+    launches_per_step = sum(c for (_, _, c, _) in prof) / args.steps
+    top = max(prof, key=lambda t: t[3])
+    peak, peak_src = load_peaks()
+    kname, klev, kcount, kms = top
+    avg_ms = kms / kcount
+    nbytes = alg_bytes(kname, n, klev)
+    achieved = nbytes / (avg_ms / 1e3) / 1e9
+    # level-0 kernels for the record
+    kernels = {f"{k}@L{lv}": {"avg_ms": round(t / c, 4), "count_per_step": c / args.steps,
+                              "share": round(t / sum(p[3] for p in prof), 4),
+                              "alg_GBps": round(alg_bytes(k, n, lv) / (t / c / 1e3) / 1e9, 1)}
+               for (k, lv, c, t) in prof if lv <= 0 or k == "coarse_solve"}
+
+    # stencil throughput: the unshifted operator apply at full size
+    y = torch.empty_like(r)
+    for _ in range(3):
+        E.apply_mixed_operator(D0, r, y)
+    s0 = torch.cuda.ExternalStream(D0.stream)
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    a0.record(s0)
+    for _ in range(reps):
+        E.apply_mixed_operator(D0, r, y)
+    a1.record(s0)
+    torch.cuda.synchronize()
+    apply_ms = a0.elapsed_time(a1) / reps
+    gdofs = N / (apply_ms / 1e3) / 1e9
+
+    # e2e: public API with pinned host buffers (H2D r, D2H z per step)
+    rh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+    zh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+    rh.copy_(r.cpu())
+    rn, zn = rh.numpy(), zh.numpy()
+    mg.precondition(rn, zn)
+    barrier(ws)
+    e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e_steps):
+        mg.precondition(rn, zn)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
+    e2e_ms = max_over_ranks(ws, e2e_ms)
+    e2e = ws * e_steps / (e2e_ms / 1e3)
+
+    # GMRES time-to-1e-6 on the point-source problem (device buffers)
+    solve = None
+    if args.solve:
+        x = torch.zeros(N, dtype=torch.complex128, device="cuda")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+        torch.cuda.synchronize()
+        ts = time.perf_counter() - t0
+        solve = {"status": res.status, "iterations": res.iterations, "relres": res.relres,
+                 "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5)}
+
+    line = {
+        "metric": metric_name(), "value": round(value, 4), "unit": "V-cycles/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
+        "data": "synthetic (BASELINE configs[2] media recipe; seeded residual)",
+        "config": workload_config(n),
+        "e2e": {"value": round(e2e, 4), "unit": "V-cycles/s", "h2d_bytes_per_step": N * 16,
+                "d2h_bytes_per_step": N * 16},
+        "stencil_gdofs": round(gdofs, 3), "stencil_apply_ms": round(apply_ms, 4),
+        "gmres_time_to_1e-6": solve, "setup_s": round(setup_s, 2),
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "roofline": {"bound": "hbm", "kernel": f"{kname}@L{klev}", "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": None, "alg_bytes_per_launch": nbytes,
+                     "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
+        "kernels": kernels, "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        rate, kind, per, wall = run_cpu_sample(1, 1)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": "V-cycles/s", "cores": 1, "kind": kind,
+            "sample": (f"one V(2,2) cycle of the reference on a {REF_SAMPLE_N}^3 cube "
+                       f"({REF_SAMPLE_LEVELS} levels, same media/omega*h/shift/damping), "
+                       f"{per:.2f} s, extrapolated to {N_CELLS}^3 by smoothed-level DOF ratio")}
+    return line
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    threads = max(1, os.cpu_count() or 1)
+    run_cpu_sample(1, threads) if args.warmup > 0 else None
+    rate, kind, per, wall = run_cpu_sample(args.steps, threads)
+    return {
+        "metric": metric_name(), "value": rate, "unit": "V-cycles/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "complex128 (f64)", "data": "synthetic", "config": workload_config(N_CELLS),
+        "impl": "reference",
+        "cpu_baseline": {"value": rate, "unit": "V-cycles/s", "cores": threads, "kind": kind,
+                         "sample": (f"{threads} concurrent replicas x {args.steps} V(2,2) cycles "
+                                    f"of the reference on a {REF_SAMPLE_N}^3 cube "
+                                    f"({REF_SAMPLE_LEVELS} levels), extrapolated to "
+                                    f"{N_CELLS}^3 by smoothed-level DOF ratio")},
+        "e2e": {"value": rate, "unit": "V-cycles/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--n", type=int, default=N_CELLS)
+    ap.add_argument("--solve", type=int, default=1)
+    ap.add_argument("--max-it", type=int, default=600)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        line = run_reference(args, ws, rank)
+    else:
+        line = run_b200(args, ws, rank, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

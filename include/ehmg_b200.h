@@ -1,0 +1,153 @@
+/*
+ * ehmg_b200.h -- C ABI of the B200-native elastic-Helmholtz multigrid path.
+ *
+ * Drop-in boundary for the reference's matrix-free solver API
+ * (/root/reference/proj/include/ehmg/*.hpp). Every entry point below names
+ * the reference interface it replaces (file:line). Plain pointers and sizes
+ * only; no torch or CUDA types cross this boundary.
+ *
+ * Field vectors are complex128 (interleaved re, im) in the reference
+ * flatten() order (assemble.hpp:256): displacement components u_0..u_{d-1}
+ * on their face boxes, then the cell-centred pressure, each block
+ * axis-0-fastest. `where` says whether field pointers are host memory
+ * (EHMG_HOST: copied to/from HBM inside the call) or device memory that the
+ * caller keeps resident in HBM (EHMG_DEVICE).
+ *
+ * Media are cell-sized float64 arrays, axis-0-fastest (media.hpp:13).
+ * Errors: every call returns 0 on success or a negative EHMG_E* code; the
+ * message (mirroring the reference's exception text) is available from
+ * ehmg_last_error().
+ */
+#ifndef EHMG_B200_H
+#define EHMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EHMG_HOST 0
+#define EHMG_DEVICE 1
+
+#define EHMG_OK 0
+#define EHMG_EINVAL -1   /* std::invalid_argument in the reference */
+#define EHMG_ERUNTIME -2 /* std::runtime_error (singular cell / LU failure) */
+#define EHMG_ECUDA -3    /* CUDA / no device */
+#define EHMG_ERANGE -4   /* std::out_of_range / std::length_error */
+
+typedef struct ehmg_op_s* ehmg_op;
+typedef struct ehmg_vanka_s* ehmg_vanka;
+typedef struct ehmg_mg_s* ehmg_mg;
+
+const char* ehmg_last_error(void);
+/* Version string of the built library (sm_100a build id). */
+const char* ehmg_version(void);
+/* Select the CUDA device for subsequent handles (one process per GPU). */
+int ehmg_set_device(int device);
+
+/* ---- operator: operator.hpp:76 make_opdata, :437 apply_mixed_operator,
+ *      :449 apply_shifted_operator (alpha folded into the mass term) ----- */
+int ehmg_op_create(int ndim, const int* dims, double h, const double* lambda, const double* mu,
+                   const double* rho, const double* gamma, double beta, double omega,
+                   double alpha, ehmg_op* out);
+int ehmg_op_destroy(ehmg_op op);
+int64_t ehmg_op_n_dofs(ehmg_op op);
+/* y = H x (operator.hpp:437) */
+int ehmg_apply_mixed_operator(ehmg_op op, const double* x, double* y, int where);
+/* r = b - H x (multigrid.hpp:210 residual) */
+int ehmg_residual(ehmg_op op, const double* b, const double* x, double* r, int where);
+/* CUDA stream the handle's kernels run on (cudaStream_t as an integer). */
+uint64_t ehmg_op_stream(ehmg_op op);
+
+/* ---- Vanka box smoother: vanka.hpp:27 VankaSmoother, :49 sweep -------
+ * mode 0 = full, 1 = economic; order 0 = lexicographic, 1 = red-black.
+ * The factorisation cache (vanka.hpp:76) is built on the device at create. */
+int ehmg_vanka_create(ehmg_op op, int mode, ehmg_vanka* out);
+int ehmg_vanka_destroy(ehmg_vanka v);
+int ehmg_vanka_per_cell_complex_count(ehmg_vanka v); /* vanka.hpp:35 */
+int ehmg_vanka_cache(ehmg_vanka v, double* out);     /* host copy of the cache */
+int ehmg_vanka_sweep(ehmg_vanka v, const double* b, double* x, double w, int order, int nsweeps,
+                     int where);
+
+/* ---- transfers: transfer.hpp:188 restrict_field, :197 prolong_field,
+ *      :40 coarsen_media (one cell field) -------------------------------- */
+int ehmg_restrict_field(int ndim, const int* dims_fine, const double* xf, double* xc, int where);
+int ehmg_prolong_field(int ndim, const int* dims_fine, const double* xc, double* xf, int where);
+int ehmg_coarsen_media(int ndim, const int* dims_fine, const double* fine, double* coarse);
+/* media.hpp:95 build_attenuation_profile (host arrays) */
+int ehmg_attenuation_profile(int ndim, const int* dims, double gamma_phys, int layer_width,
+                             double gamma_max, int absorb_top, double* out);
+
+/* ---- multigrid: multigrid.hpp:34 MgOptions, :75 Multigrid, :133 cycle,
+ *      :136 precondition --------------------------------------------------
+ * cycle: 0 two_grid, 1 v, 2 w, 3 k. coarse: the coarsest level is solved
+ * exactly (CoarseSolverKind::lu, multigrid.hpp:97) by an LU-derived inverse
+ * held in HBM. */
+typedef struct {
+  int n_levels;
+  int cycle;
+  int nu1, nu2;
+  double damping;
+  int vanka_mode;
+  int sweep;
+  int k_inner_iterations;
+  double k_inner_rtol;
+} ehmg_mg_options;
+
+int ehmg_multigrid_create(int ndim, const int* dims, double h, const double* lambda,
+                          const double* mu, const double* rho, const double* gamma, double beta,
+                          double omega, double alpha, const ehmg_mg_options* opt, ehmg_mg* out);
+int ehmg_multigrid_destroy(ehmg_mg mg);
+int ehmg_multigrid_n_levels(ehmg_mg mg);
+int ehmg_multigrid_cycle(ehmg_mg mg, const double* b, double* x, int where);
+int ehmg_multigrid_precondition(ehmg_mg mg, const double* r, double* z, int where);
+uint64_t ehmg_multigrid_stream(ehmg_mg mg);
+/* Replay `count` preconditioner applications on device buffers and return
+ * the CUDA-event time of the whole batch in milliseconds (bench helper). */
+int ehmg_multigrid_time_precondition(ehmg_mg mg, const double* r_dev, double* z_dev, int count,
+                                     double* ms);
+
+/* Per-launch CUDA-event profiling of the cycle kernels (bench roofline).
+ * report: one "kernel level count total_ms" line per (kernel, level). */
+int ehmg_profile_enable(int on);
+int ehmg_profile_report(char* buf, int cap);
+
+/* ---- Krylov: krylov.hpp:45 KrylovOptions, :55 KrylovResult, :65 fgmres,
+ *      driven as in experiments.hpp:313 (A = unshifted operator, M = one
+ *      multigrid cycle on the shifted hierarchy) ---------------------------
+ * status: 0 converged, 1 max_iterations, 2 breakdown, 3 stalled. */
+typedef struct {
+  int restart;
+  int max_iterations;
+  double rtol;
+  double stall_factor;
+  int stall_cycles;
+} ehmg_krylov_options;
+
+typedef struct {
+  int status;
+  int iterations;
+  double relres;
+  int n_history;
+} ehmg_krylov_result;
+
+int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int where,
+                      const ehmg_krylov_options* opt, ehmg_krylov_result* res, double* history,
+                      int history_cap);
+
+/* ---- field BLAS-1 on device buffers (grid.hpp:129 axpy, :135 scal,
+ *      :142 dot, :150 norm) ------------------------------------------------ */
+int ehmg_field_dot(int64_t n, const double* x, const double* y, double* out_re_im);
+int ehmg_field_norm(int64_t n, const double* x, double* out);
+int ehmg_field_axpy(int64_t n, double a_re, double a_im, const double* x, double* y);
+
+/* ---- device memory helpers for callers without their own allocator ---- */
+int ehmg_device_alloc(int64_t bytes, void** out);
+int ehmg_device_free(void* p);
+int ehmg_memcpy(void* dst, const void* src, int64_t bytes, int kind /* 0 H2D, 1 D2H, 2 D2D */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,518 @@
+// ehmg_kernels.cuh -- sm_100a kernels of the multigrid path (all levels):
+// operator/residual, Vanka factorisation + red-black sweep, staggered
+// transfers, media coarsening, coarsest-level assembly and inverse apply,
+// and the deterministic BLAS-1 reductions used by FGMRES.
+#pragma once
+
+#include "ehmg_core.cuh"
+
+namespace ehmg {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t n, int cap = 148 * 16) {
+  int64_t b = (n + kThreads - 1) / kThreads;
+  if (b < 1) b = 1;
+  return (int)(b < cap ? b : cap);
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// --------------------------------------------------------------- operator
+// y = A x (b == nullptr) or y = b - A x. One thread per DOF, generic rows.
+template <int ND>
+__global__ void __launch_bounds__(kThreads) k_apply_generic(Geo g, OpPar P, const Cell* __restrict__ m,
+                                                            const cplx* __restrict__ x,
+                                                            const cplx* __restrict__ b,
+                                                            cplx* __restrict__ y) {
+  FieldAcc A{x};
+  GRID_STRIDE(r, g.ndofs) {
+    int i[3];
+    int comp = g.unlin(r, i);
+    cplx v = row_any<ND>(g, m, P, comp, i, A);
+    y[r] = b ? b[r] - v : v;
+  }
+}
+
+// ------------------------------------------------------------------ Vanka
+// vanka.hpp:85 build_cell: per-cell factorisation from unit-probe rows.
+// Layout per cell (complex): for each component k
+//   full: Uinv00 Uinv01 Uinv10 Uinv11 g0 g1 h0 h1; economic: Uinv0 Uinv1 g0 g1 h0 h1
+// then 1/s.
+template <int ND>
+__global__ void k_vanka_build(Geo g, OpPar P, const Cell* __restrict__ m, int full,
+                              cplx* __restrict__ cache, int* __restrict__ bad) {
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
+  GRID_STRIDE(ci, g.ncells) {
+    int c[3] = {(int)(ci % g.n[0]), (int)((ci / g.n[0]) % g.n[1]), (int)(ci / ((int64_t)g.n[0] * g.n[1]))};
+    cplx* q = cache + ci * stride;
+    cplx sum_cg = mk(0, 0);
+    for (int k = 0; k < ND; ++k) {
+      int f[2][3];
+      f[0][0] = c[0], f[0][1] = c[1], f[0][2] = c[2];
+      sh(c, k, 1, f[1]);
+      cplx U[2][2] = {{mk(0, 0), mk(0, 0)}, {mk(0, 0), mk(0, 0)}}, bk[2], ck[2];
+      for (int i = 0; i < 2; ++i) {
+        for (int j = 0; j < 2; ++j) {
+          if (!full && i != j) continue;
+          UnitAcc A{k, {f[j][0], f[j][1], f[j][2]}};
+          U[i][j] = row_u<ND>(g, m, P, k, f[i], A);
+        }
+        UnitAcc Ap{ND, {c[0], c[1], c[2]}};
+        bk[i] = row_u<ND>(g, m, P, k, f[i], Ap);
+        UnitAcc Au{k, {f[i][0], f[i][1], f[i][2]}};
+        ck[i] = row_p<ND>(g, m, P, c, Au);
+      }
+      cplx Ui[2][2];
+      if (full) {
+        cplx det = U[0][0] * U[1][1] - U[0][1] * U[1][0];
+        if (!(abs2(det) > 0)) *bad = 1;
+        cplx idet = cdiv(mk(1, 0), det);
+        Ui[0][0] = U[1][1] * idet;
+        Ui[0][1] = -U[0][1] * idet;
+        Ui[1][0] = -U[1][0] * idet;
+        Ui[1][1] = U[0][0] * idet;
+      } else {
+        if (!(abs2(U[0][0]) > 0) || !(abs2(U[1][1]) > 0)) *bad = 1;
+        Ui[0][0] = cdiv(mk(1, 0), U[0][0]);
+        Ui[1][1] = cdiv(mk(1, 0), U[1][1]);
+        Ui[0][1] = Ui[1][0] = mk(0, 0);
+      }
+      cplx g0 = Ui[0][0] * bk[0] + Ui[0][1] * bk[1];
+      cplx g1 = Ui[1][0] * bk[0] + Ui[1][1] * bk[1];
+      cplx h0 = ck[0] * Ui[0][0] + ck[1] * Ui[1][0];
+      cplx h1 = ck[0] * Ui[0][1] + ck[1] * Ui[1][1];
+      sum_cg += ck[0] * g0 + ck[1] * g1;
+      if (full) {
+        *q++ = Ui[0][0];
+        *q++ = Ui[0][1];
+        *q++ = Ui[1][0];
+        *q++ = Ui[1][1];
+      } else {
+        *q++ = Ui[0][0];
+        *q++ = Ui[1][1];
+      }
+      *q++ = g0;
+      *q++ = g1;
+      *q++ = h0;
+      *q++ = h1;
+    }
+    UnitAcc Ap{ND, {c[0], c[1], c[2]}};
+    cplx d = row_p<ND>(g, m, P, c, Ap);
+    cplx s = d - sum_cg;
+    if (!(abs2(s) > 0)) *bad = 1;
+    *q = cdiv(mk(1, 0), s);
+  }
+}
+
+// vanka.hpp:157 corrections of one cell from the current state.
+template <int ND>
+__device__ __forceinline__ void vanka_corr(const Geo& g, const OpPar& P, const Cell* m, int full,
+                                           const cplx* q, const cplx* b, const FieldAcc& A,
+                                           const int* c, cplx* du, cplx& dp) {
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
+  const int blk_w = full ? 8 : 6;
+  cplx r[ND][2];
+  cplx dpa = b[g.off[ND] + g.clin(c)] - row_p<ND>(g, m, P, c, A);
+  for (int k = 0; k < ND; ++k) {
+    int f1[3];
+    sh(c, k, 1, f1);
+    r[k][0] = b[g.off[k] + g.flin(k, c)] - row_u<ND>(g, m, P, k, c, A);
+    r[k][1] = b[g.off[k] + g.flin(k, f1)] - row_u<ND>(g, m, P, k, f1, A);
+    const cplx* hk = q + k * blk_w + (full ? 6 : 4);
+    dpa -= hk[0] * r[k][0] + hk[1] * r[k][1];
+  }
+  dp = q[stride - 1] * dpa;
+  for (int k = 0; k < ND; ++k) {
+    const cplx* blk = q + k * blk_w;
+    const cplx* gk = blk + (full ? 4 : 2);
+    if (full) {
+      du[2 * k + 0] = blk[0] * r[k][0] + blk[1] * r[k][1] - gk[0] * dp;
+      du[2 * k + 1] = blk[2] * r[k][0] + blk[3] * r[k][1] - gk[1] * dp;
+    } else {
+      du[2 * k + 0] = blk[0] * r[k][0] - gk[0] * dp;
+      du[2 * k + 1] = blk[1] * r[k][1] - gk[1] * dp;
+    }
+  }
+}
+
+// Cells of one colour (parity of the index sum): with an even axis-0 extent
+// every row holds n0/2 of them and thread `t` maps to one directly; odd
+// extents fall back to one thread per cell with a parity test.
+EH_HD int64_t colour_threads(const Geo& g) {
+  return (g.n[0] % 2 == 0) ? g.ncells / 2 : g.ncells;
+}
+EH_HD bool colour_cell(const Geo& g, int64_t t, int color, int* c) {
+  if (g.n[0] % 2 == 0) {
+    const int half = g.n[0] / 2;
+    const int64_t row = t / half;
+    c[1] = (int)(row % g.n[1]);
+    c[2] = (int)(row / g.n[1]);
+    c[0] = 2 * (int)(t % half) + ((color - c[1] - c[2]) & 1);
+    return true;
+  }
+  c[0] = (int)(t % g.n[0]);
+  c[1] = (int)((t / g.n[0]) % g.n[1]);
+  c[2] = (int)(t / ((int64_t)g.n[0] * g.n[1]));
+  return ((c[0] + c[1] + c[2]) & 1) == color;
+}
+
+// Red-black phase 1: corrections of every cell of `color` from the state at
+// the start of the colour (vanka.hpp:205), deferred into `delta`.
+template <int ND>
+__global__ void __launch_bounds__(kThreads) k_vanka_corr(Geo g, OpPar P, const Cell* __restrict__ m, int full,
+                                                         const cplx* __restrict__ cache,
+                                                         const cplx* __restrict__ b,
+                                                         const cplx* __restrict__ x, int color,
+                                                         cplx* __restrict__ delta) {
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
+  const int nl = 2 * ND + 1;
+  FieldAcc A{x};
+  GRID_STRIDE(t, colour_threads(g)) {
+    int c[3];
+    if (!colour_cell(g, t, color, c)) continue;
+    const int64_t ci = g.clin(c);
+    cplx du[2 * ND], dp;
+    vanka_corr<ND>(g, P, m, full, cache + ci * stride, b, A, c, du, dp);
+    cplx* slot = delta + ci * nl;
+    for (int q = 0; q < 2 * ND; ++q) slot[q] = du[q];
+    slot[2 * ND] = dp;
+  }
+}
+
+// Red-black phase 2: x += w * delta on the DOFs owned by cells of `color`.
+// Cells of one colour share no DOFs, so the writes commute.
+template <int ND>
+__global__ void __launch_bounds__(kThreads) k_vanka_apply(Geo g, int color, const cplx* __restrict__ delta,
+                                                          double w, cplx* __restrict__ x) {
+  const int nl = 2 * ND + 1;
+  GRID_STRIDE(t, colour_threads(g)) {
+    int c[3];
+    if (!colour_cell(g, t, color, c)) continue;
+    const int64_t ci = g.clin(c);
+    const cplx* slot = delta + ci * nl;
+    for (int k = 0; k < ND; ++k) {
+      int f1[3];
+      sh(c, k, 1, f1);
+      x[g.off[k] + g.flin(k, c)] += w * slot[2 * k];
+      x[g.off[k] + g.flin(k, f1)] += w * slot[2 * k + 1];
+    }
+    x[g.off[ND] + ci] += w * slot[2 * ND];
+  }
+}
+
+// Lexicographic sweep (vanka.hpp:192): inherently sequential; one thread.
+template <int ND>
+__global__ void k_vanka_lex(Geo g, OpPar P, const Cell* __restrict__ m, int full,
+                            const cplx* __restrict__ cache, const cplx* __restrict__ b,
+                            cplx* __restrict__ x, double w) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
+  FieldAcc A{x};
+  for (int64_t ci = 0; ci < g.ncells; ++ci) {
+    int c[3] = {(int)(ci % g.n[0]), (int)((ci / g.n[0]) % g.n[1]), (int)(ci / ((int64_t)g.n[0] * g.n[1]))};
+    cplx du[2 * ND], dp;
+    vanka_corr<ND>(g, P, m, full, cache + ci * stride, b, A, c, du, dp);
+    for (int k = 0; k < ND; ++k) {
+      int f1[3];
+      sh(c, k, 1, f1);
+      x[g.off[k] + g.flin(k, c)] += w * du[2 * k];
+      x[g.off[k] + g.flin(k, f1)] += w * du[2 * k + 1];
+    }
+    x[g.off[ND] + ci] += w * dp;
+  }
+}
+
+// -------------------------------------------------------------- transfers
+// transfer.hpp:77 restrict_1d, :109 prolong_1d (non-periodic) as tap rows.
+struct Taps {
+  int cnt;
+  int idx[3];
+  double w[3];
+};
+EH_HD void renorm(Taps& t) {
+  double s = 0;
+  for (int i = 0; i < t.cnt; ++i) s += t.w[i];
+  for (int i = 0; i < t.cnt; ++i) t.w[i] /= s;
+}
+EH_HD Taps restrict_taps(int i, int n_fine, bool face) {
+  Taps t;
+  t.cnt = 0;
+  if (face) {
+    const double ws[3] = {0.25, 0.5, 0.25};
+    for (int q = 0; q < 3; ++q) {
+      int f = 2 * i + q - 1;
+      if (f >= 0 && f < n_fine) {
+        t.idx[t.cnt] = f;
+        t.w[t.cnt++] = ws[q];
+      }
+    }
+    renorm(t);
+  } else {
+    t.cnt = 2;
+    t.idx[0] = 2 * i;
+    t.w[0] = 0.5;
+    t.idx[1] = 2 * i + 1;
+    t.w[1] = 0.5;
+  }
+  return t;
+}
+EH_HD Taps prolong_taps(int f, int n_fine, bool face) {
+  Taps t;
+  if (face) {
+    if (f % 2 == 0) {
+      t.cnt = 1;
+      t.idx[0] = f / 2;
+      t.w[0] = 1.0;
+    } else {
+      t.cnt = 2;
+      t.idx[0] = f / 2;
+      t.w[0] = 0.5;
+      t.idx[1] = f / 2 + 1;
+      t.w[1] = 0.5;
+    }
+  } else {
+    int nc = n_fine / 2, c = f / 2, far = (f % 2 == 0) ? c - 1 : c + 1;
+    t.cnt = 1;
+    t.idx[0] = c;
+    t.w[0] = 0.75;
+    if (far >= 0 && far < nc) {
+      t.idx[1] = far;
+      t.w[1] = 0.25;
+      t.cnt = 2;
+    }
+    renorm(t);
+  }
+  return t;
+}
+
+// One thread per destination DOF; the tensor product is contracted axis 0
+// innermost, the association the reference's axis-by-axis sweep produces
+// (transfer.hpp:164).
+template <int ND>
+__global__ void __launch_bounds__(kThreads) k_transfer(Geo gf, Geo gc, int restricting,
+                                                       const cplx* __restrict__ in,
+                                                       cplx* __restrict__ out, int accumulate) {
+  const Geo& gto = restricting ? gc : gf;
+  const Geo& gfrom = restricting ? gf : gc;
+  GRID_STRIDE(r, gto.ndofs) {
+    int o[3];
+    int comp = gto.unlin(r, o);
+    Taps t[3];
+    for (int a = 0; a < 3; ++a) {
+      if (a >= ND) {
+        t[a].cnt = 1;
+        t[a].idx[0] = 0;
+        t[a].w[0] = 1.0;
+        continue;
+      }
+      bool face = comp == a;
+      int n_fine = face ? gf.n[a] + 1 : gf.n[a];
+      t[a] = restricting ? restrict_taps(o[a], n_fine, face) : prolong_taps(o[a], n_fine, face);
+    }
+    const int64_t base = gfrom.off[comp];
+    int d0 = comp < ND ? gfrom.fdim(comp, 0) : gfrom.n[0];
+    int d1 = comp < ND ? gfrom.fdim(comp, 1) : gfrom.n[1];
+    cplx s2 = mk(0, 0);
+    for (int q2 = 0; q2 < t[2].cnt; ++q2) {
+      cplx s1 = mk(0, 0);
+      for (int q1 = 0; q1 < t[1].cnt; ++q1) {
+        cplx s0 = mk(0, 0);
+        const int64_t rowb = base + (int64_t)d0 * (t[1].idx[q1] + (int64_t)d1 * t[2].idx[q2]);
+        for (int q0 = 0; q0 < t[0].cnt; ++q0) s0 += t[0].w[q0] * in[rowb + t[0].idx[q0]];
+        s1 += t[1].w[q1] * s0;
+      }
+      s2 += t[2].w[q2] * s1;
+    }
+    out[r] = accumulate ? out[r] + s2 : s2;
+  }
+}
+
+// ------------------------------------------------------------------ media
+// transfer.hpp:40 coarsen_media, four fields at once.
+__global__ void k_coarsen_media(int nd, int nf0, int nf1, int nf2, int64_t ncc, const double* __restrict__ f0,
+                                const double* __restrict__ f1, const double* __restrict__ f2,
+                                const double* __restrict__ f3, double* __restrict__ c0, double* __restrict__ c1,
+                                double* __restrict__ c2, double* __restrict__ c3) {
+  const int n0 = nf0 / 2, n1 = nf1 / 2;
+  GRID_STRIDE(ci, ncc) {
+    int c[3] = {(int)(ci % n0), (int)((ci / n0) % n1), (int)(ci / ((int64_t)n0 * n1))};
+    double s[4] = {0, 0, 0, 0};
+    const int nch = 1 << nd;
+    for (int bits = 0; bits < nch; ++bits) {
+      int f[3] = {0, 0, 0};
+      for (int a = 0; a < nd; ++a) f[a] = 2 * c[a] + ((bits >> a) & 1);
+      int64_t fi = f[0] + (int64_t)nf0 * (f[1] + (int64_t)nf1 * f[2]);
+      s[0] += f0[fi];
+      s[1] += f1[fi];
+      s[2] += f2[fi];
+      s[3] += f3[fi];
+    }
+    c0[ci] = s[0] / nch;
+    c1[ci] = s[1] / nch;
+    c2[ci] = s[2] / nch;
+    c3[ci] = s[3] / nch;
+  }
+}
+
+// Pack {mu, rho, gamma, 1/(lambda+mu)} (operator.hpp:99-105).
+__global__ void k_pack_media(int64_t n, const double* __restrict__ lam, const double* __restrict__ mu,
+                             const double* __restrict__ rho, const double* __restrict__ gam,
+                             Cell* __restrict__ out) {
+  GRID_STRIDE(i, n) {
+    double lm = lam[i] + mu[i];
+    out[i] = make_double4(mu[i], rho[i], gam[i], 1.0 / lm);
+  }
+}
+
+// ------------------------------------------------------- coarsest level
+// Row-major dense matrix via unit probes in a +-2 window around each column.
+template <int ND>
+__global__ void k_coarse_matrix(Geo g, OpPar P, const Cell* __restrict__ m, cplx* __restrict__ A) {
+  const int W = 5, nwin = (ND == 3) ? W * W * W : W * W;
+  const int64_t N = g.ndofs;
+  const int64_t total = N * (ND + 1) * nwin;
+  GRID_STRIDE(t, total) {
+    int64_t col = t / ((ND + 1) * nwin);
+    int rem = (int)(t % ((ND + 1) * nwin));
+    int rc = rem / nwin, w = rem % nwin;
+    int ci[3];
+    int cc = g.unlin(col, ci);
+    int o[3] = {w % W - 2, (w / W) % W - 2, ND == 3 ? w / (W * W) - 2 : 0};
+    int r[3] = {ci[0] + o[0], ci[1] + o[1], ci[2] + o[2]};
+    bool ok = rc < ND ? g.face_ok(rc, r) : g.cell_ok(r);
+    if (!ok) continue;
+    UnitAcc U{cc, {ci[0], ci[1], ci[2]}};
+    cplx v = row_any<ND>(g, m, P, rc, r, U);
+    int64_t row = g.off[rc] + (rc < ND ? g.flin(rc, r) : g.clin(r));
+    A[row * N + col] = v;
+  }
+}
+
+// x = Ainv b with Ainv row-major: one warp per row, coalesced along the row.
+__global__ void __launch_bounds__(kThreads) k_gemv_rows(int64_t N, const cplx* __restrict__ A,
+                                                        const cplx* __restrict__ b, cplx* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; row < N; row += warps) {
+    const cplx* a = A + row * N;
+    double sr = 0, si = 0;
+    for (int64_t j = lane; j < N; j += 32) {
+      cplx av = a[j], bv = __ldg(&b[j]);
+      sr = fma(av.x, bv.x, fma(-av.y, bv.y, sr));
+      si = fma(av.x, bv.y, fma(av.y, bv.x, si));
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, s);
+      si += __shfl_xor_sync(0xffffffffu, si, s);
+    }
+    if (lane == 0) x[row] = mk(sr, si);
+  }
+}
+
+__global__ void k_identity(int64_t N, cplx* __restrict__ B) {
+  GRID_STRIDE(i, N * N) { B[i] = (i / N == i % N) ? mk(1, 0) : mk(0, 0); }
+}
+
+// ------------------------------------------------------------------ BLAS-1
+constexpr int kRedBlocks = 148 * 4;
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v);
+template <>
+__device__ __forceinline__ double warp_sum<double>(double v) {
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  return v;
+}
+
+// Deterministic reduction: fixed grid, per-block partials, the last block
+// to finish sums the partials in block order. mode 0: <x,y> (conj x),
+// mode 1: ||x||^2. Result (re, im) to out[0..1]; optional negated copy to
+// coef (the MGS axpy coefficient) and accumulation into hacc.
+__global__ void __launch_bounds__(kThreads) k_reduce(int mode, int64_t n, const cplx* __restrict__ x,
+                                                     const cplx* __restrict__ y, double2* __restrict__ partial,
+                                                     unsigned* __restrict__ counter, double* __restrict__ out,
+                                                     double* __restrict__ coef, double* __restrict__ hacc) {
+  double sr = 0, si = 0;
+  GRID_STRIDE(i, n) {
+    cplx a = x[i];
+    if (mode == 1) {
+      sr += a.x * a.x + a.y * a.y;
+    } else {
+      cplx bb = y[i];
+      sr += a.x * bb.x + a.y * bb.y;
+      si += a.x * bb.y - a.y * bb.x;
+    }
+  }
+  __shared__ double shr[kThreads / 32], shi[kThreads / 32];
+  __shared__ bool last;
+  sr = warp_sum(sr);
+  si = warp_sum(si);
+  if ((threadIdx.x & 31) == 0) {
+    shr[threadIdx.x / 32] = sr;
+    shi[threadIdx.x / 32] = si;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b2 = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      a += shr[w];
+      b2 += shi[w];
+    }
+    partial[blockIdx.x] = make_double2(a, b2);
+    __threadfence();
+    unsigned done = atomicAdd(counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double a = 0, b2 = 0;
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      const volatile double* pp = (const volatile double*)partial;
+      a += pp[2 * q];
+      b2 += pp[2 * q + 1];
+    }
+    out[0] = a;
+    out[1] = b2;
+    if (coef) {
+      coef[0] = -a;
+      coef[1] = -b2;
+    }
+    if (hacc) {
+      hacc[0] += a;
+      hacc[1] += b2;
+    }
+    *counter = 0;
+  }
+}
+
+// y += a x with a = (ar, ai) or, when ap != nullptr, a = *ap (device).
+__global__ void __launch_bounds__(kThreads) k_axpy(int64_t n, double ar, double ai, const double* __restrict__ ap,
+                                                   const cplx* __restrict__ x, cplx* __restrict__ y) {
+  if (ap) {
+    ar = ap[0];
+    ai = ap[1];
+  }
+  const cplx a = mk(ar, ai);
+  GRID_STRIDE(i, n) { y[i] += a * x[i]; }
+}
+
+// y = s * x with a real scale read from device (1/norm) or given.
+__global__ void __launch_bounds__(kThreads) k_scale_copy(int64_t n, double s, const double* __restrict__ sp,
+                                                         int invert_sqrt, const cplx* __restrict__ x,
+                                                         cplx* __restrict__ y) {
+  if (sp) s = invert_sqrt ? 1.0 / sqrt(sp[0]) : sp[0];
+  GRID_STRIDE(i, n) {
+    cplx v = x[i];
+    y[i] = mk(v.x * s, v.y * s);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_sub(int64_t n, const cplx* __restrict__ b, const cplx* __restrict__ t,
+                                                  cplx* __restrict__ r) {
+  GRID_STRIDE(i, n) { r[i] = b[i] - t[i]; }
+}
+
+}  // namespace ehmg

@@ -1,0 +1,1052 @@
+// ehmg_solver.cu -- host runtime of the B200 multigrid path and its C ABI.
+//
+// C++ host code drives hand-written sm_100a kernels (ehmg_kernels.cuh,
+// ehmg_stencil3d.cuh) on one CUDA stream per handle:
+//   * OpHandle      -- operator.hpp:40 OpData on HBM (packed cell media)
+//   * VankaHandle   -- vanka.hpp:27 VankaSmoother (device factor cache)
+//   * MgHandle      -- multigrid.hpp:70 Multigrid (re-discretised levels,
+//                      V/W/K cycles, exact coarsest solve via an LU-derived
+//                      inverse resident in HBM)
+//   * Fgmres        -- krylov.hpp:65 fgmres on device vectors with host
+//                      Givens/Hessenberg bookkeeping
+// Everything the reference does per cycle runs on the GPU; the host only
+// sequences launches and makes the Krylov control decisions.
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ehmg_b200.h"
+#include "ehmg_kernels.cuh"
+#include "ehmg_stencil3d.cuh"
+
+namespace ehmg {
+
+// ------------------------------------------------------------------ errors
+struct Err : std::runtime_error {
+  int code;
+  Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+static thread_local std::string g_last_error;
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw Err(EHMG_ECUDA, std::string("cuda: ") + cudaGetErrorString(e_) + " at " #x);  \
+  } while (0)
+#define CKS(x)                                                                         \
+  do {                                                                                 \
+    cusolverStatus_t e_ = (x);                                                         \
+    if (e_ != CUSOLVER_STATUS_SUCCESS)                                                 \
+      throw Err(EHMG_ECUDA, "cusolver status " + std::to_string((int)e_) + " at " #x); \
+  } while (0)
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return EHMG_OK;
+  } catch (const Err& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return EHMG_ERUNTIME;
+  }
+}
+
+// --------------------------------------------------------------- profiling
+// Optional per-launch CUDA-event timing (bench roofline): events recorded on
+// the launching stream around every kernel of the cycle, tagged with the
+// kernel name and the multigrid level.
+struct ProfRec {
+  const char* name;
+  int level;
+  cudaEvent_t a, b;
+};
+static bool g_prof = false;
+static thread_local int g_level = -1;
+static std::vector<ProfRec> g_recs;
+struct Prof {
+  ProfRec r{};
+  cudaStream_t s;
+  bool on;
+  Prof(const char* name, cudaStream_t s_) : s(s_), on(g_prof) {
+    if (!on) return;
+    r.name = name;
+    r.level = g_level;
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, s);
+  }
+  ~Prof() {
+    if (!on) return;
+    cudaEventRecord(r.b, s);
+    g_recs.push_back(r);
+  }
+};
+
+// ----------------------------------------------------------------- memory
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DBuf() = default;
+  explicit DBuf(int64_t n_) { alloc(n_); }
+  void alloc(int64_t n_) {
+    release();
+    n = n_;
+    if (n > 0) CK(cudaMalloc(&p, sizeof(T) * n));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
+static void validate_grid(int nd, const int* dims, double h) {
+  if (nd != 2 && nd != 3) throw Err(EHMG_EINVAL, "grid: 2D or 3D only");
+  if (!(h > 0)) throw Err(EHMG_EINVAL, "grid: h must be positive");
+  for (int a = 0; a < nd; ++a)
+    if (dims[a] < 2) throw Err(EHMG_EINVAL, "grid: need >= 2 cells per axis");
+}
+
+// media.hpp:27 MediaModel::validate
+static void validate_media(int64_t n, const double* lam, const double* mu, const double* rho,
+                           const double* gam) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(rho[i] > 0)) throw Err(EHMG_EINVAL, "media: rho must be positive");
+    if (!(mu[i] > 0)) throw Err(EHMG_EINVAL, "media: mu must be positive");
+    if (!(lam[i] + mu[i] > 0)) throw Err(EHMG_EINVAL, "media: lambda+mu must be positive");
+    if (!(gam[i] >= 0)) throw Err(EHMG_EINVAL, "media: gamma must be nonnegative");
+  }
+}
+
+// Raw cell media on the device (lambda, mu, rho, gamma) + packed form.
+struct DevMedia {
+  DBuf<double> raw[4];
+  DBuf<Cell> packed;
+  void upload(int64_t n, const double* const* f, cudaStream_t s) {
+    for (int q = 0; q < 4; ++q) {
+      raw[q].alloc(n);
+      CK(cudaMemcpyAsync(raw[q].p, f[q], sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    }
+    pack(n, s);
+  }
+  void pack(int64_t n, cudaStream_t s) {
+    packed.alloc(n);
+    k_pack_media<<<grid_for(n), kThreads, 0, s>>>(n, raw[0].p, raw[1].p, raw[2].p, raw[3].p,
+                                                   packed.p);
+    CK(cudaGetLastError());
+  }
+  void coarsen_into(const Geo& gf, DevMedia& out, const Geo& gc, cudaStream_t s) const {
+    for (int q = 0; q < 4; ++q) out.raw[q].alloc(gc.ncells);
+    k_coarsen_media<<<grid_for(gc.ncells), kThreads, 0, s>>>(
+        gf.nd, gf.n[0], gf.n[1], gf.n[2], gc.ncells, raw[0].p, raw[1].p, raw[2].p, raw[3].p,
+        out.raw[0].p, out.raw[1].p, out.raw[2].p, out.raw[3].p);
+    CK(cudaGetLastError());
+    out.pack(gc.ncells, s);
+  }
+  void drop_raw() {
+    for (auto& r : raw) r.release();
+  }
+};
+
+// ----------------------------------------------------------- level kernels
+// r = b - A x (b != null) or y = A x.
+static void launch_residual(const Geo& g, const OpPar& P, const Cell* m, const cplx* x,
+                            const cplx* b, cplx* y, cudaStream_t s) {
+  Prof pf(b ? "residual" : "apply", s);
+  if (g.nd == 3 && stencil3d_supported(g)) {
+    launch_stencil3d(g, P, m, x, b, y, s);
+  } else if (g.nd == 3) {
+    k_apply_generic<3><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
+  } else {
+    k_apply_generic<2><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
+  }
+  CK(cudaGetLastError());
+}
+
+static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, const cplx* in,
+                            cplx* out, bool accumulate, cudaStream_t s) {
+  const Geo& gto = restricting ? gc : gf;
+  Prof pf(restricting ? "restrict" : "prolong_add", s);
+  if (gf.nd == 3)
+    k_transfer<3><<<grid_for(gto.ndofs, 148 * 64), kThreads, 0, s>>>(gf, gc, restricting, in, out,
+                                                                     accumulate);
+  else
+    k_transfer<2><<<grid_for(gto.ndofs, 148 * 64), kThreads, 0, s>>>(gf, gc, restricting, in, out,
+                                                                     accumulate);
+  CK(cudaGetLastError());
+}
+
+static Geo coarse_geo(const Geo& g) {
+  int d[3];
+  for (int a = 0; a < g.nd; ++a) d[a] = g.n[a] / 2;
+  return make_geo(g.nd, d, 2.0 * g.h);
+}
+
+// Vanka factor cache + red-black / lexicographic sweeps on one level.
+struct Smoother {
+  int full = 1, stride = 0;
+  DBuf<cplx> cache, delta;
+  void build(const Geo& g, const OpPar& P, const Cell* m, int full_, cudaStream_t s) {
+    full = full_;
+    stride = g.nd * ((full ? 4 : 2) + 4) + 1;
+    cache.alloc(g.ncells * stride);
+    delta.alloc(g.ncells * (2 * g.nd + 1));
+    DBuf<int> bad(1);
+    bad.zero(s);
+    if (g.nd == 3)
+      k_vanka_build<3><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, bad.p);
+    else
+      k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, bad.p);
+    CK(cudaGetLastError());
+    int hb = 0;
+    CK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hb) throw Err(EHMG_ERUNTIME, "vanka: singular local cell system");
+  }
+  void sweep(const Geo& g, const OpPar& P, const Cell* m, const cplx* b, cplx* x, double w,
+             int order, cudaStream_t s) {
+    if (order == 0) {
+      if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, m, full, cache.p, b, x, w);
+      else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, m, full, cache.p, b, x, w);
+      CK(cudaGetLastError());
+      return;
+    }
+    const int64_t nt = colour_threads(g);
+    for (int color = 0; color < 2; ++color) {
+      if (g.nd == 3) {
+        {
+          Prof pf("vanka_corr", s);
+          k_vanka_corr<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, b, x,
+                                                                      color, delta.p);
+        }
+        Prof pf("vanka_apply", s);
+        k_vanka_apply<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, color, delta.p, w, x);
+      } else {
+        k_vanka_corr<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, b, x,
+                                                                    color, delta.p);
+        k_vanka_apply<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, color, delta.p, w, x);
+      }
+      CK(cudaGetLastError());
+    }
+  }
+};
+
+// --------------------------------------------------------------- BLAS-1
+struct Blas {
+  cudaStream_t s = nullptr;
+  DBuf<double2> partial;
+  DBuf<unsigned> counter;
+  DBuf<double> scal;  // [0..1] last result, [2..3] coef, [4..] hessenberg column
+  void init(cudaStream_t s_, int ncol) {
+    s = s_;
+    partial.alloc(kRedBlocks);
+    counter.alloc(1);
+    counter.zero(s);
+    scal.alloc(8 + 2 * (ncol + 2));
+    scal.zero(s);
+  }
+  double* res() { return scal.p; }
+  double* coef() { return scal.p + 2; }
+  double* wpre() { return scal.p + 4; }
+  double* wn() { return scal.p + 6; }
+  double* hcol(int i) { return scal.p + 8 + 2 * i; }
+  void reduce(int mode, int64_t n, const cplx* x, const cplx* y, double* out, double* coef_,
+              double* hacc) {
+    k_reduce<<<kRedBlocks, kThreads, 0, s>>>(mode, n, x, y, partial.p, counter.p, out, coef_, hacc);
+    CK(cudaGetLastError());
+  }
+  double norm_host(int64_t n, const cplx* x) {
+    reduce(1, n, x, nullptr, res(), nullptr, nullptr);
+    double h[2];
+    CK(cudaMemcpyAsync(h, res(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return std::sqrt(h[0]);
+  }
+  void axpy(int64_t n, cplx a, const double* ap, const cplx* x, cplx* y) {
+    k_axpy<<<grid_for(n, 148 * 16), kThreads, 0, s>>>(n, a.x, a.y, ap, x, y);
+    CK(cudaGetLastError());
+  }
+  void scale_copy(int64_t n, double sc, const cplx* x, cplx* y) {
+    k_scale_copy<<<grid_for(n, 148 * 16), kThreads, 0, s>>>(n, sc, nullptr, 0, x, y);
+    CK(cudaGetLastError());
+  }
+  void sub(int64_t n, const cplx* b, const cplx* t, cplx* r) {
+    k_sub<<<grid_for(n, 148 * 16), kThreads, 0, s>>>(n, b, t, r);
+    CK(cudaGetLastError());
+  }
+};
+
+// ----------------------------------------------------------------- FGMRES
+// krylov.hpp:65, restated on device vectors. The preconditioned vectors
+// are stored (flexible variant); Arnoldi uses modified Gram-Schmidt with one
+// optional re-orthogonalisation pass; Givens rotations on the host.
+struct Fgmres {
+  int64_t n = 0;
+  int m = 0;
+  std::vector<std::unique_ptr<DBuf<cplx>>> V, Z;
+  DBuf<cplx> r, w;
+  Blas blas;
+
+  void init(int64_t n_, int m_, cudaStream_t s) {
+    if (n == n_ && m == m_) return;
+    n = n_;
+    m = m_;
+    V.clear();
+    Z.clear();
+    for (int i = 0; i <= m; ++i) V.emplace_back(new DBuf<cplx>(n));
+    for (int i = 0; i < m; ++i) Z.emplace_back(new DBuf<cplx>(n));
+    r.alloc(n);
+    w.alloc(n);
+    blas.init(s, m + 1);
+  }
+
+  using Fn = std::function<void(const cplx*, cplx*)>;
+
+  ehmg_krylov_result run(const Fn& A, const Fn& M, const cplx* b, cplx* x,
+                         const ehmg_krylov_options& opt, std::vector<double>& hist) {
+    cudaStream_t s = blas.s;
+    ehmg_krylov_result res{1, 0, 1.0, 0};
+    const double bnorm = blas.norm_host(n, b);
+    if (bnorm == 0.0) {
+      CK(cudaMemsetAsync(x, 0, sizeof(cplx) * n, s));
+      res.status = 0;
+      res.relres = 0.0;
+      return res;
+    }
+    const double target = opt.rtol * bnorm;
+    A(x, w.p);
+    blas.sub(n, b, w.p, r.p);
+    double beta = blas.norm_host(n, r.p);
+    hist.push_back(beta / bnorm);
+    res.relres = beta / bnorm;
+    if (beta <= target) {
+      res.status = 0;
+      return res;
+    }
+    std::vector<cplx> H((size_t)(m + 1) * m, mk(0, 0));
+    auto HH = [&](int i, int j) -> cplx& { return H[(size_t)i * m + j]; };
+    std::vector<double> gc(m, 0.0);
+    std::vector<cplx> gs(m, mk(0, 0)), g(m + 1, mk(0, 0)), y(m, mk(0, 0));
+    std::vector<double> hbuf(8 + 2 * (m + 2));
+    double prev_cycle = beta;
+    int stall = 0;
+    while (res.iterations < opt.max_iterations) {
+      blas.scale_copy(n, 1.0 / beta, r.p, V[0]->p);
+      for (auto& q : g) q = mk(0, 0);
+      g[0] = mk(beta, 0);
+      bool broke = false;
+      int j = 0;
+      while (j < m && res.iterations < opt.max_iterations) {
+        M(V[j]->p, Z[j]->p);
+        A(Z[j]->p, w.p);
+        blas.reduce(1, n, w.p, nullptr, blas.wpre(), nullptr, nullptr);
+        for (int i = 0; i <= j; ++i) {
+          blas.reduce(0, n, V[i]->p, w.p, blas.hcol(i), blas.coef(), nullptr);
+          blas.axpy(n, mk(0, 0), blas.coef(), V[i]->p, w.p);
+        }
+        blas.reduce(1, n, w.p, nullptr, blas.wn(), nullptr, nullptr);
+        CK(cudaMemcpyAsync(hbuf.data(), blas.scal.p, sizeof(double) * (8 + 2 * (j + 1)),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const double wpre = std::sqrt(hbuf[4]);
+        double wn = std::sqrt(hbuf[6]);
+        if (wn < 0.70710678 * wpre) {  // one re-orthogonalisation pass
+          for (int i = 0; i <= j; ++i) {
+            blas.reduce(0, n, V[i]->p, w.p, blas.res(), blas.coef(), blas.hcol(i));
+            blas.axpy(n, mk(0, 0), blas.coef(), V[i]->p, w.p);
+          }
+          blas.reduce(1, n, w.p, nullptr, blas.wn(), nullptr, nullptr);
+          CK(cudaMemcpyAsync(hbuf.data(), blas.scal.p, sizeof(double) * (8 + 2 * (j + 1)),
+                             cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
+          wn = std::sqrt(hbuf[6]);
+        }
+        for (int i = 0; i <= j; ++i) HH(i, j) = mk(hbuf[8 + 2 * i], hbuf[9 + 2 * i]);
+        HH(j + 1, j) = mk(wn, 0);
+        ++res.iterations;
+        if (!(wn > 1e-14 * (wpre > 0 ? wpre : 1.0))) {
+          broke = true;
+        } else {
+          blas.scale_copy(n, 1.0 / wn, w.p, V[j + 1]->p);
+        }
+        for (int i = 0; i < j; ++i) {
+          const cplx a = HH(i, j), bb = HH(i + 1, j);
+          HH(i, j) = gc[i] * a + gs[i] * bb;
+          HH(i + 1, j) = -(conj(gs[i]) * a) + gc[i] * bb;
+        }
+        const cplx h1 = HH(j, j), h2 = HH(j + 1, j);
+        const double t = std::sqrt(abs2(h1) + abs2(h2));
+        const double ah1 = std::hypot(h1.x, h1.y);
+        if (t == 0.0) {
+          gc[j] = 1.0;
+          gs[j] = mk(0, 0);
+        } else if (ah1 == 0.0) {
+          gc[j] = 0.0;
+          gs[j] = mk(1, 0);
+        } else {
+          gc[j] = ah1 / t;
+          gs[j] = (mk(h1.x / ah1, h1.y / ah1) * conj(h2)) * (1.0 / t);
+        }
+        HH(j, j) = gc[j] * h1 + gs[j] * h2;
+        HH(j + 1, j) = mk(0, 0);
+        const cplx gj = g[j];
+        g[j] = gc[j] * gj;
+        g[j + 1] = -(conj(gs[j]) * gj);
+        const double est = std::hypot(g[j + 1].x, g[j + 1].y);
+        hist.push_back(est / bnorm);
+        ++j;
+        if (broke || est <= target) break;
+      }
+      for (int i = j - 1; i >= 0; --i) {
+        cplx v = g[i];
+        for (int l = i + 1; l < j; ++l) v -= HH(i, l) * y[l];
+        if (std::hypot(HH(i, i).x, HH(i, i).y) == 0.0) {
+          res.status = 2;
+          return res;
+        }
+        y[i] = cdiv(v, HH(i, i));
+      }
+      for (int i = 0; i < j; ++i) blas.axpy(n, y[i], nullptr, Z[i]->p, x);
+      A(x, w.p);
+      blas.sub(n, b, w.p, r.p);
+      beta = blas.norm_host(n, r.p);
+      res.relres = beta / bnorm;
+      if (beta <= target) {
+        res.status = 0;
+        return res;
+      }
+      if (broke) {
+        res.status = 2;
+        return res;
+      }
+      if (beta > opt.stall_factor * prev_cycle) {
+        if (++stall >= opt.stall_cycles) {
+          res.status = 3;
+          return res;
+        }
+      } else {
+        stall = 0;
+      }
+      prev_cycle = beta;
+    }
+    res.status = 1;
+    return res;
+  }
+};
+
+}  // namespace ehmg
+
+using namespace ehmg;
+
+// ------------------------------------------------------------- handles
+struct ehmg_op_s {
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  Geo g;
+  OpPar P;
+  DevMedia media;
+  DBuf<cplx> hx, hy, hb;  // staging for EHMG_HOST calls
+  ~ehmg_op_s() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+struct ehmg_vanka_s {
+  ehmg_op op;
+  Smoother sm;
+};
+
+struct Level {
+  Geo g;
+  OpPar P;
+  DevMedia media;
+  Smoother sm;
+  DBuf<cplx> r, bc, ec;
+  Fgmres inner;  // K-cycle acceleration on this level
+};
+
+struct ehmg_mg_s {
+  int dev = 0;
+  cudaStream_t s = nullptr;
+  ehmg_mg_options opt;
+  std::vector<std::unique_ptr<Level>> L;
+  DBuf<cplx> ainv;  // row-major inverse of the coarsest operator
+  int64_t nco = 0;
+  DBuf<cplx> hx, hy;
+  ~ehmg_mg_s() {
+    L.clear();
+    if (s) cudaStreamDestroy(s);
+  }
+
+  void cycle_at(int l, const cplx* b, cplx* x);
+  void precondition(const cplx* r, cplx* z) {
+    CK(cudaMemsetAsync(z, 0, sizeof(cplx) * L[0]->g.ndofs, s));
+    cycle_at(0, r, z);
+  }
+};
+
+// multigrid.hpp:217 cycle_at
+void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
+  const int nl = (int)L.size();
+  g_level = l;
+  if (l + 1 == nl) {
+    Prof pf("coarse_solve", s);
+    k_gemv_rows<<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, ainv.p, b, x);
+    CK(cudaGetLastError());
+    return;
+  }
+  Level& lev = *L[l];
+  Level& nxt = *L[l + 1];
+  for (int q = 0; q < opt.nu1; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.packed.p, b, x, opt.damping, opt.sweep, s);
+  launch_residual(lev.g, lev.P, lev.media.packed.p, x, b, lev.r.p, s);
+  launch_transfer(lev.g, nxt.g, true, lev.r.p, nxt.bc.p, false, s);
+  CK(cudaMemsetAsync(nxt.ec.p, 0, sizeof(cplx) * nxt.g.ndofs, s));
+  const bool next_coarsest = (l + 2 == nl);
+  switch (opt.cycle) {
+    case 0:
+    case 1:
+      cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      break;
+    case 2:
+      cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      if (!next_coarsest) cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      break;
+    default:
+      if (next_coarsest) {
+        cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      } else {
+        ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol,
+                               0.99, 2};
+        nxt.inner.init(nxt.g.ndofs, opt.k_inner_iterations, s);
+        std::vector<double> hist;
+        Fgmres::Fn A = [&](const cplx* in, cplx* out) {
+          launch_residual(nxt.g, nxt.P, nxt.media.packed.p, in, nullptr, out, s);
+        };
+        Fgmres::Fn M = [&](const cplx* in, cplx* out) {
+          CK(cudaMemsetAsync(out, 0, sizeof(cplx) * nxt.g.ndofs, s));
+          cycle_at(l + 1, in, out);
+        };
+        nxt.inner.run(A, M, nxt.bc.p, nxt.ec.p, ko, hist);
+      }
+      break;
+  }
+  g_level = l;
+  launch_transfer(lev.g, nxt.g, false, nxt.ec.p, x, true, s);
+  for (int q = 0; q < opt.nu2; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.packed.p, b, x, opt.damping, opt.sweep, s);
+}
+
+// ------------------------------------------------------------ helpers
+static int64_t ndofs_of(int nd, const int* dims) {
+  int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+  return make_geo(nd, d, 1.0).ndofs;
+}
+
+static void to_dev(const double* src, DBuf<cplx>& stage, int64_t n, int where, cudaStream_t s,
+                   const cplx** out) {
+  if (where == EHMG_DEVICE) {
+    *out = reinterpret_cast<const cplx*>(src);
+    return;
+  }
+  if (stage.n < n) stage.alloc(n);
+  CK(cudaMemcpyAsync(stage.p, src, sizeof(cplx) * n, cudaMemcpyHostToDevice, s));
+  *out = stage.p;
+}
+
+static cplx* out_dev(double* dst, DBuf<cplx>& stage, int64_t n, int where) {
+  if (where == EHMG_DEVICE) return reinterpret_cast<cplx*>(dst);
+  if (stage.n < n) stage.alloc(n);
+  return stage.p;
+}
+
+static void from_dev(double* dst, const cplx* dev, int64_t n, int where, cudaStream_t s) {
+  if (where == EHMG_DEVICE) {
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  CK(cudaMemcpyAsync(dst, dev, sizeof(cplx) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+static void check_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw Err(EHMG_ECUDA, "no CUDA device: the B200 path has no CPU fallback");
+}
+
+// Exact coarsest solve: assemble A (row-major == A^T column-major), LU it
+// with cuSOLVER and solve against the identity, leaving A^{-1} row-major.
+static void build_coarse_inverse(const Geo& g, const OpPar& P, const Cell* m, DBuf<cplx>& ainv,
+                                 cudaStream_t s) {
+  const int64_t N = g.ndofs;
+  if (N > 40000) throw Err(EHMG_ERANGE, "assemble_sparse: grid exceeds DOF budget of 40000");
+  DBuf<cplx> A(N * N);
+  A.zero(s);
+  const int nwin = g.nd == 3 ? 125 : 25;
+  const int64_t total = N * (g.nd + 1) * nwin;
+  if (g.nd == 3) k_coarse_matrix<3><<<grid_for(total, 148 * 64), kThreads, 0, s>>>(g, P, m, A.p);
+  else k_coarse_matrix<2><<<grid_for(total, 148 * 64), kThreads, 0, s>>>(g, P, m, A.p);
+  CK(cudaGetLastError());
+  ainv.alloc(N * N);
+  k_identity<<<grid_for(N * N, 148 * 64), kThreads, 0, s>>>(N, ainv.p);
+  CK(cudaGetLastError());
+  cusolverDnHandle_t h;
+  CKS(cusolverDnCreate(&h));
+  CKS(cusolverDnSetStream(h, s));
+  int lwork = 0;
+  CKS(cusolverDnZgetrf_bufferSize(h, (int)N, (int)N, (cuDoubleComplex*)A.p, (int)N, &lwork));
+  DBuf<cplx> work(lwork > 0 ? lwork : 1);
+  DBuf<int> ipiv(N), info(1);
+  CKS(cusolverDnZgetrf(h, (int)N, (int)N, (cuDoubleComplex*)A.p, (int)N, (cuDoubleComplex*)work.p,
+                       ipiv.p, info.p));
+  int hinfo = 0;
+  CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hinfo != 0) {
+    cusolverDnDestroy(h);
+    throw Err(EHMG_ERUNTIME, "multigrid: coarsest LU factorization failed");
+  }
+  CKS(cusolverDnZgetrs(h, CUBLAS_OP_N, (int)N, (int)N, (cuDoubleComplex*)A.p, (int)N, ipiv.p,
+                       (cuDoubleComplex*)ainv.p, (int)N, info.p));
+  CK(cudaStreamSynchronize(s));
+  cusolverDnDestroy(h);
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* ehmg_last_error(void) { return g_last_error.c_str(); }
+const char* ehmg_version(void) { return "ehmg_b200 0.1 (sm_100a)"; }
+
+int ehmg_set_device(int device) {
+  return guard([&] {
+    check_device();
+    CK(cudaSetDevice(device));
+  });
+}
+
+int ehmg_op_create(int nd, const int* dims, double h, const double* lambda, const double* mu,
+                   const double* rho, const double* gamma, double beta, double omega,
+                   double alpha, ehmg_op* out) {
+  return guard([&] {
+    validate_grid(nd, dims, h);
+    check_device();
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    auto op = std::make_unique<ehmg_op_s>();
+    CK(cudaGetDevice(&op->dev));
+    CK(cudaStreamCreateWithFlags(&op->s, cudaStreamNonBlocking));
+    op->g = make_geo(nd, d, h);
+    validate_media(op->g.ncells, lambda, mu, rho, gamma);
+    op->P = OpPar{beta, omega * omega, alpha};
+    const double* f[4] = {lambda, mu, rho, gamma};
+    op->media.upload(op->g.ncells, f, op->s);
+    op->media.drop_raw();
+    CK(cudaStreamSynchronize(op->s));
+    *out = op.release();
+  });
+}
+
+int ehmg_op_destroy(ehmg_op op) {
+  return guard([&] { delete op; });
+}
+
+int64_t ehmg_op_n_dofs(ehmg_op op) { return op ? op->g.ndofs : -1; }
+uint64_t ehmg_op_stream(ehmg_op op) { return op ? (uint64_t)(uintptr_t)op->s : 0; }
+
+int ehmg_apply_mixed_operator(ehmg_op op, const double* x, double* y, int where) {
+  return guard([&] {
+    const int64_t n = op->g.ndofs;
+    const cplx* dx;
+    to_dev(x, op->hx, n, where, op->s, &dx);
+    cplx* dy = out_dev(y, op->hy, n, where);
+    launch_residual(op->g, op->P, op->media.packed.p, dx, nullptr, dy, op->s);
+    from_dev(y, dy, n, where, op->s);
+  });
+}
+
+int ehmg_residual(ehmg_op op, const double* b, const double* x, double* r, int where) {
+  return guard([&] {
+    const int64_t n = op->g.ndofs;
+    const cplx *dx, *db;
+    to_dev(x, op->hx, n, where, op->s, &dx);
+    to_dev(b, op->hb, n, where, op->s, &db);
+    cplx* dr = out_dev(r, op->hy, n, where);
+    launch_residual(op->g, op->P, op->media.packed.p, dx, db, dr, op->s);
+    from_dev(r, dr, n, where, op->s);
+  });
+}
+
+int ehmg_vanka_create(ehmg_op op, int mode, ehmg_vanka* out) {
+  return guard([&] {
+    auto v = std::make_unique<ehmg_vanka_s>();
+    v->op = op;
+    v->sm.build(op->g, op->P, op->media.packed.p, mode == 0 ? 1 : 0, op->s);
+    *out = v.release();
+  });
+}
+
+int ehmg_vanka_destroy(ehmg_vanka v) {
+  return guard([&] { delete v; });
+}
+
+int ehmg_vanka_per_cell_complex_count(ehmg_vanka v) { return v ? v->sm.stride : -1; }
+
+int ehmg_vanka_cache(ehmg_vanka v, double* out) {
+  return guard([&] {
+    CK(cudaMemcpyAsync(out, v->sm.cache.p, sizeof(cplx) * v->sm.cache.n, cudaMemcpyDeviceToHost,
+                       v->op->s));
+    CK(cudaStreamSynchronize(v->op->s));
+  });
+}
+
+int ehmg_vanka_sweep(ehmg_vanka v, const double* b, double* x, double w, int order, int nsweeps,
+                     int where) {
+  return guard([&] {
+    ehmg_op op = v->op;
+    const int64_t n = op->g.ndofs;
+    const cplx* db;
+    to_dev(b, op->hb, n, where, op->s, &db);
+    cplx* dx;
+    if (where == EHMG_DEVICE) {
+      dx = reinterpret_cast<cplx*>(x);
+    } else {
+      if (op->hx.n < n) op->hx.alloc(n);
+      CK(cudaMemcpyAsync(op->hx.p, x, sizeof(cplx) * n, cudaMemcpyHostToDevice, op->s));
+      dx = op->hx.p;
+    }
+    for (int q = 0; q < nsweeps; ++q) v->sm.sweep(op->g, op->P, op->media.packed.p, db, dx, w, order, op->s);
+    from_dev(x, dx, n, where, op->s);
+  });
+}
+
+static int transfer_abi(int nd, const int* dims_f, const double* in, double* out, int where,
+                        bool restricting) {
+  return guard([&] {
+    validate_grid(nd, dims_f, 1.0);
+    for (int a = 0; a < nd; ++a)
+      if (dims_f[a] % 2 != 0 || dims_f[a] / 2 < 2)
+        throw Err(EHMG_EINVAL, "coarsen_grid: dims must be even and >= 4");
+    check_device();
+    int d[3] = {dims_f[0], dims_f[1], nd == 3 ? dims_f[2] : 1};
+    Geo gf = make_geo(nd, d, 1.0), gc = coarse_geo(gf);
+    const int64_t nin = restricting ? gf.ndofs : gc.ndofs, nout = restricting ? gc.ndofs : gf.ndofs;
+    cudaStream_t s = 0;
+    DBuf<cplx> si, so;
+    const cplx* di;
+    to_dev(in, si, nin, where, s, &di);
+    cplx* dout = out_dev(out, so, nout, where);
+    launch_transfer(gf, gc, restricting, di, dout, false, s);
+    from_dev(out, dout, nout, where, s);
+  });
+}
+
+int ehmg_restrict_field(int nd, const int* dims_f, const double* xf, double* xc, int where) {
+  return transfer_abi(nd, dims_f, xf, xc, where, true);
+}
+int ehmg_prolong_field(int nd, const int* dims_f, const double* xc, double* xf, int where) {
+  return transfer_abi(nd, dims_f, xc, xf, where, false);
+}
+
+int ehmg_coarsen_media(int nd, const int* dims_f, const double* fine, double* coarse) {
+  return guard([&] {
+    validate_grid(nd, dims_f, 1.0);
+    for (int a = 0; a < nd; ++a)
+      if (dims_f[a] % 2 != 0 || dims_f[a] / 2 < 2)
+        throw Err(EHMG_EINVAL, "coarsen_grid: dims must be even and >= 4");
+    check_device();
+    int d[3] = {dims_f[0], dims_f[1], nd == 3 ? dims_f[2] : 1};
+    Geo gf = make_geo(nd, d, 1.0), gc = coarse_geo(gf);
+    DBuf<double> in(gf.ncells), o(gc.ncells);
+    CK(cudaMemcpy(in.p, fine, sizeof(double) * gf.ncells, cudaMemcpyHostToDevice));
+    k_coarsen_media<<<grid_for(gc.ncells), kThreads>>>(nd, gf.n[0], gf.n[1], gf.n[2], gc.ncells,
+                                                       in.p, in.p, in.p, in.p, o.p, o.p, o.p, o.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(coarse, o.p, sizeof(double) * gc.ncells, cudaMemcpyDeviceToHost));
+  });
+}
+
+// media.hpp:95 (host-side media preparation; not on the per-cycle path)
+int ehmg_attenuation_profile(int nd, const int* dims, double gamma_phys, int L, double gamma_max,
+                             int absorb_top, double* out) {
+  return guard([&] {
+    if (L < 0) throw Err(EHMG_EINVAL, "sponge: negative layer width");
+    if (L > 0)
+      for (int a = 0; a < nd; ++a)
+        if (2 * L >= dims[a]) throw Err(EHMG_EINVAL, "sponge: 2*layer_width must be < dims on every axis");
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    for (int64_t c2 = 0; c2 < d[2]; ++c2)
+      for (int64_t c1 = 0; c1 < d[1]; ++c1)
+        for (int64_t c0 = 0; c0 < d[0]; ++c0) {
+          int c[3] = {(int)c0, (int)c1, (int)c2};
+          double ramp = 0;
+          if (L > 0)
+            for (int a = 0; a < nd; ++a) {
+              int dist_lo = c[a], dist_hi = d[a] - 1 - c[a];
+              bool skip_lo = absorb_top ? false : (a == nd - 1);
+              if (!skip_lo && dist_lo < L) {
+                double q = double(L - dist_lo) / L;
+                ramp = std::max(ramp, q * q);
+              }
+              if (dist_hi < L) {
+                double q = double(L - dist_hi) / L;
+                ramp = std::max(ramp, q * q);
+              }
+            }
+          out[c0 + d[0] * (c1 + d[1] * c2)] = L == 0 ? gamma_phys : gamma_phys + gamma_max * ramp;
+        }
+  });
+}
+
+int ehmg_multigrid_create(int nd, const int* dims, double h, const double* lambda,
+                          const double* mu, const double* rho, const double* gamma, double beta,
+                          double omega, double alpha, const ehmg_mg_options* opt, ehmg_mg* out) {
+  return guard([&] {
+    if (opt->n_levels < 2) throw Err(EHMG_EINVAL, "multigrid: need at least 2 levels");
+    if (opt->cycle == 0 && opt->n_levels != 2)
+      throw Err(EHMG_EINVAL, "multigrid: two_grid cycle requires exactly 2 levels");
+    validate_grid(nd, dims, h);
+    check_device();
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    auto mg = std::make_unique<ehmg_mg_s>();
+    mg->opt = *opt;
+    CK(cudaGetDevice(&mg->dev));
+    CK(cudaStreamCreateWithFlags(&mg->s, cudaStreamNonBlocking));
+    cudaStream_t s = mg->s;
+    Geo g = make_geo(nd, d, h);
+    validate_media(g.ncells, lambda, mu, rho, gamma);
+    // every level but the last must coarsen (transfer.hpp:25 can_coarsen)
+    {
+      Geo t = g;
+      for (int l = 0; l + 1 < opt->n_levels; ++l) {
+        for (int a = 0; a < nd; ++a)
+          if (t.n[a] % 2 != 0 || t.n[a] / 2 < 2)
+            throw Err(EHMG_EINVAL, "multigrid: grid cannot support requested levels");
+        t = coarse_geo(t);
+      }
+    }
+    const OpPar P{beta, omega * omega, alpha};
+    for (int l = 0; l < opt->n_levels; ++l) {
+      auto lev = std::make_unique<Level>();
+      lev->g = l == 0 ? g : coarse_geo(mg->L[l - 1]->g);
+      lev->P = P;
+      if (l == 0) {
+        const double* f[4] = {lambda, mu, rho, gamma};
+        lev->media.upload(g.ncells, f, s);
+      } else {
+        mg->L[l - 1]->media.coarsen_into(mg->L[l - 1]->g, lev->media, lev->g, s);
+      }
+      const bool coarsest = (l + 1 == opt->n_levels);
+      if (!coarsest) {
+        lev->sm.build(lev->g, P, lev->media.packed.p, opt->vanka_mode == 0 ? 1 : 0, s);
+        lev->r.alloc(lev->g.ndofs);
+      }
+      if (l > 0) {
+        lev->bc.alloc(lev->g.ndofs);
+        lev->ec.alloc(lev->g.ndofs);
+      }
+      mg->L.push_back(std::move(lev));
+    }
+    for (auto& lev : mg->L) lev->media.drop_raw();
+    Level& cl = *mg->L.back();
+    mg->nco = cl.g.ndofs;
+    build_coarse_inverse(cl.g, P, cl.media.packed.p, mg->ainv, s);
+    CK(cudaStreamSynchronize(s));
+    *out = mg.release();
+  });
+}
+
+int ehmg_multigrid_destroy(ehmg_mg mg) {
+  return guard([&] { delete mg; });
+}
+int ehmg_multigrid_n_levels(ehmg_mg mg) { return mg ? (int)mg->L.size() : -1; }
+uint64_t ehmg_multigrid_stream(ehmg_mg mg) { return mg ? (uint64_t)(uintptr_t)mg->s : 0; }
+
+int ehmg_multigrid_cycle(ehmg_mg mg, const double* b, double* x, int where) {
+  return guard([&] {
+    const int64_t n = mg->L[0]->g.ndofs;
+    const cplx* db;
+    to_dev(b, mg->hy, n, where, mg->s, &db);
+    cplx* dx;
+    if (where == EHMG_DEVICE) {
+      dx = reinterpret_cast<cplx*>(x);
+    } else {
+      if (mg->hx.n < n) mg->hx.alloc(n);
+      CK(cudaMemcpyAsync(mg->hx.p, x, sizeof(cplx) * n, cudaMemcpyHostToDevice, mg->s));
+      dx = mg->hx.p;
+    }
+    mg->cycle_at(0, db, dx);
+    from_dev(x, dx, n, where, mg->s);
+  });
+}
+
+int ehmg_multigrid_precondition(ehmg_mg mg, const double* r, double* z, int where) {
+  return guard([&] {
+    const int64_t n = mg->L[0]->g.ndofs;
+    const cplx* dr;
+    to_dev(r, mg->hy, n, where, mg->s, &dr);
+    cplx* dz = out_dev(z, mg->hx, n, where);
+    mg->precondition(dr, dz);
+    from_dev(z, dz, n, where, mg->s);
+  });
+}
+
+int ehmg_multigrid_time_precondition(ehmg_mg mg, const double* r_dev, double* z_dev, int count,
+                                     double* ms) {
+  return guard([&] {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, mg->s));
+    for (int i = 0; i < count; ++i)
+      mg->precondition(reinterpret_cast<const cplx*>(r_dev), reinterpret_cast<cplx*>(z_dev));
+    CK(cudaEventRecord(b, mg->s));
+    CK(cudaEventSynchronize(b));
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, a, b));
+    *ms = f;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+int ehmg_profile_enable(int on) {
+  return guard([&] {
+    g_prof = on != 0;
+    for (auto& r : g_recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_recs.clear();
+  });
+}
+
+// Aggregate recorded launches: one line "name level count total_ms" per
+// (kernel, level) into buf (newline separated).
+int ehmg_profile_report(char* buf, int cap) {
+  return guard([&] {
+    struct Agg {
+      std::string name;
+      int level;
+      int count;
+      double ms;
+    };
+    std::vector<Agg> agg;
+    for (auto& r : g_recs) {
+      CK(cudaEventSynchronize(r.b));
+      float f = 0;
+      CK(cudaEventElapsedTime(&f, r.a, r.b));
+      bool found = false;
+      for (auto& a : agg)
+        if (a.name == r.name && a.level == r.level) {
+          a.count++;
+          a.ms += f;
+          found = true;
+        }
+      if (!found) agg.push_back({r.name, r.level, 1, (double)f});
+    }
+    std::string out;
+    for (auto& a : agg)
+      out += a.name + " " + std::to_string(a.level) + " " + std::to_string(a.count) + " " +
+             std::to_string(a.ms) + "\n";
+    std::snprintf(buf, (size_t)cap, "%s", out.c_str());
+  });
+}
+
+int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int where,
+                      const ehmg_krylov_options* opt, ehmg_krylov_result* res, double* history,
+                      int history_cap) {
+  return guard([&] {
+    const int64_t n = A->g.ndofs;
+    if (M && M->L[0]->g.ndofs != n) throw Err(EHMG_EINVAL, "fgmres: operator/preconditioner size mismatch");
+    cudaStream_t s = M ? M->s : A->s;
+    // keep the operator on the solver stream
+    const cplx* db;
+    DBuf<cplx> sb, sx;
+    to_dev(b, sb, n, where, s, &db);
+    cplx* dx;
+    if (where == EHMG_DEVICE) {
+      dx = reinterpret_cast<cplx*>(x);
+    } else {
+      sx.alloc(n);
+      CK(cudaMemcpyAsync(sx.p, x, sizeof(cplx) * n, cudaMemcpyHostToDevice, s));
+      dx = sx.p;
+    }
+    Fgmres fg;
+    fg.init(n, opt->restart, s);
+    Fgmres::Fn Af = [&](const cplx* in, cplx* out) {
+      launch_residual(A->g, A->P, A->media.packed.p, in, nullptr, out, s);
+    };
+    Fgmres::Fn Mf = [&](const cplx* in, cplx* out) {
+      if (M) M->precondition(in, out);
+      else CK(cudaMemcpyAsync(out, in, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, s));
+    };
+    std::vector<double> hist;
+    *res = fg.run(Af, Mf, db, dx, *opt, hist);
+    res->n_history = (int)hist.size();
+    if (history)
+      for (int i = 0; i < (int)hist.size() && i < history_cap; ++i) history[i] = hist[i];
+    from_dev(x, dx, n, where, s);
+  });
+}
+
+int ehmg_field_dot(int64_t n, const double* x, const double* y, double* out) {
+  return guard([&] {
+    Blas b;
+    b.init(0, 1);
+    b.reduce(0, n, (const cplx*)x, (const cplx*)y, b.res(), nullptr, nullptr);
+    CK(cudaMemcpy(out, b.res(), 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+int ehmg_field_norm(int64_t n, const double* x, double* out) {
+  return guard([&] {
+    Blas b;
+    b.init(0, 1);
+    *out = b.norm_host(n, (const cplx*)x);
+  });
+}
+int ehmg_field_axpy(int64_t n, double ar, double ai, const double* x, double* y) {
+  return guard([&] {
+    Blas b;
+    b.init(0, 1);
+    b.axpy(n, mk(ar, ai), nullptr, (const cplx*)x, (cplx*)y);
+    CK(cudaDeviceSynchronize());
+  });
+}
+
+int ehmg_device_alloc(int64_t bytes, void** out) {
+  return guard([&] {
+    check_device();
+    CK(cudaMalloc(out, (size_t)bytes));
+  });
+}
+int ehmg_device_free(void* p) {
+  return guard([&] { CK(cudaFree(p)); });
+}
+int ehmg_memcpy(void* dst, const void* src, int64_t bytes, int kind) {
+  return guard([&] {
+    cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                 : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+    CK(cudaMemcpy(dst, src, (size_t)bytes, k));
+  });
+}
+
+}  // extern "C"

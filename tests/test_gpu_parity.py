@@ -1,0 +1,188 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the C oracle.
+
+Tolerances (north_star): operator apply <= 1e-12 relative, one V-cycle
+<= 1e-10 relative, FGMRES iteration count within +-1 of the reference.
+"""
+import numpy as np
+import pytest
+
+import paper_2307_03242_b200 as E
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-12
+CYCLE_TOL = 1e-10
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def emedia(c):
+    return E.MediaModel(c["lam"], c["mu"], c["rho"], c["gam"])
+
+
+def rand_media(rng, dims, gscale=0.05):
+    n = int(np.prod(dims))
+    return (3 * rng.uniform(.5, 2, n), rng.uniform(.5, 2, n), rng.uniform(.5, 2, n),
+            gscale * rng.uniform(.5, 2, n))
+
+
+def rfield(rng, n):
+    return rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+
+
+def test_golden_through_cuda(golden):
+    for c in golden:
+        k, dims, h = c["kind"], c["dims"], c["h"]
+        g = E.StaggeredGrid(dims, h)
+        if k == "apply":
+            beta, omega, alpha = c["par"]
+            D = E.make_opdata(g, emedia(c), E.OperatorParams(beta, omega, alpha))
+            assert rel(E.apply_mixed_operator(D, c["x"]), c["y"]) < APPLY_TOL
+        elif k == "vanka":
+            beta, omega, alpha = c["par"]
+            D = E.make_opdata(g, emedia(c), E.OperatorParams(beta, omega, alpha))
+            sm = E.VankaSmoother("full" if int(c["mode"]) == 0 else "economic")
+            assert rel(sm.cache(D).ravel(), c["cache"]) < 1e-12
+            x = c["x"].copy()
+            order = "red_black" if int(c["order"]) == 1 else "lexicographic"
+            sm.sweep(D, c["b"], x, float(c["w"]), order, nsweeps=int(c["nsweeps"]))
+            assert rel(x, c["xs"]) < 1e-11
+        elif k == "transfer":
+            gc = E.coarsen_grid(g)
+            assert rel(E.restrict_field(g, gc, c["xf"]), c["r"]) < 1e-15
+            assert rel(E.prolong_field(g, gc, c["xc"]), c["p"]) < 1e-15
+        elif k == "coarsen":
+            m = E.MediaModel(c["v"], c["v"], c["v"], c["v"])
+            assert rel(E.coarsen_media(g, m).lambda_, c["c"]) < 1e-15
+        elif k == "mg":
+            beta, omega, alpha = c["par"]
+            nu = int(c["nu"])
+            opt = E.MgOptions(n_levels=int(c["nl"]), cycle=str(c["cyc"]), nu1=nu, nu2=nu,
+                              damping=0.55, vanka_mode=str(c["vmode"]), sweep=str(c["sweep"]))
+            mg = E.Multigrid(g, emedia(c), E.OperatorParams(beta, omega, alpha), opt)
+            x = np.zeros_like(c["b"])
+            mg.cycle(c["b"], x)
+            mg.cycle(c["b"], x)
+            assert rel(x, c["x"]) < CYCLE_TOL
+        elif k == "solve":
+            beta, omega, alpha = c["par"]
+            opt = E.MgOptions(n_levels=int(c["nl"]), cycle="v", nu1=2, nu2=2,
+                              damping=float(c["w"]), vanka_mode="full", sweep="red_black")
+            med = emedia(c)
+            mg = E.Multigrid(g, med, E.OperatorParams(beta, omega, alpha), opt)
+            D0 = E.make_opdata(g, med, E.OperatorParams(beta, omega, 0.0))
+            x = np.zeros_like(c["b"])
+            res = E.fgmres(D0, mg, c["b"], x, E.KrylovOptions(restart=10))
+            assert res.status == str(c["status"])
+            assert abs(res.iterations - int(c["iterations"])) <= 1
+            assert rel(x, c["x"]) < 1e-6
+
+
+@pytest.mark.parametrize("dims", [(64, 48), (128, 128), (24, 20, 16), (32, 32, 32), (40, 24, 36)])
+@pytest.mark.parametrize("beta", [1.0, 2 / 3])
+def test_apply_vs_oracle(dims, beta):
+    rng = np.random.default_rng(hash((dims, beta)) % 2**32)
+    lam, mu, rho, gam = rand_media(rng, dims)
+    h = 1.0 / dims[0]
+    omega, alpha = 2 * np.pi * dims[0] / 10, 0.15
+    x = rfield(rng, O.n_dofs(dims))
+    D = E.make_opdata(E.StaggeredGrid(dims, h), E.MediaModel(lam, mu, rho, gam),
+                      E.OperatorParams(beta, omega, alpha))
+    y = E.apply_mixed_operator(D, x)
+    yr = O.Op(dims, h, O.Media(lam, mu, rho, gam), beta, omega, alpha).apply(x)
+    assert rel(y, yr) < APPLY_TOL
+    b = rfield(rng, O.n_dofs(dims))
+    r = E.residual(D, b, x)
+    assert rel(r, b - yr) < APPLY_TOL
+
+
+@pytest.mark.parametrize("dims,nl", [((64, 64), 3), ((32, 32, 32), 3), ((32, 16, 24), 3)])
+def test_vcycle_vs_oracle(dims, nl):
+    rng = np.random.default_rng(5)
+    lam, mu, rho, gam = rand_media(rng, dims)
+    h = 1.0 / dims[0]
+    omega = 2 * np.pi * dims[0] / 10
+    b = rfield(rng, O.n_dofs(dims))
+    opt = E.MgOptions(n_levels=nl, cycle="v", nu1=2, nu2=2, damping=0.35, vanka_mode="full",
+                      sweep="red_black")
+    mg = E.Multigrid(E.StaggeredGrid(dims, h), E.MediaModel(lam, mu, rho, gam),
+                     E.OperatorParams(2 / 3, omega, 0.3), opt)
+    z = mg.precondition(b)
+    zr = O.MG(dims, h, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.3, n_levels=nl, cycle="v",
+              nu1=2, nu2=2, damping=0.35).precondition(b)
+    assert rel(z, zr) < CYCLE_TOL
+
+
+def test_kcycle_and_wcycle_vs_oracle():
+    rng = np.random.default_rng(9)
+    dims = (32, 16)
+    lam, mu, rho, gam = rand_media(rng, dims)
+    h = 1.0 / 32
+    omega = 2 * np.pi * 32 / 10
+    b = rfield(rng, O.n_dofs(dims))
+    for cyc in ("w", "k"):
+        opt = E.MgOptions(n_levels=3, cycle=cyc, nu1=1, nu2=1, damping=0.55, vanka_mode="full",
+                          sweep="red_black")
+        mg = E.Multigrid(E.StaggeredGrid(dims, h), E.MediaModel(lam, mu, rho, gam),
+                         E.OperatorParams(2 / 3, omega, 0.3), opt)
+        z = mg.precondition(b)
+        zr = O.MG(dims, h, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.3, n_levels=3, cycle=cyc,
+                  damping=0.55).precondition(b)
+        assert rel(z, zr) < (CYCLE_TOL if cyc == "w" else 1e-8)
+
+
+def test_fgmres_iterations_vs_oracle_2d():
+    dims = (128, 128)
+    g = E.StaggeredGrid(dims, 1 / 128)
+    sp = E.SpongeConfig(16)
+    n = g.n_cells()
+    gam = O.attenuation(dims, 0.01, 16)
+    lam, mu, rho = np.full(n, 2.0), np.ones(n), np.ones(n)
+    omega = 2 * np.pi / (10 / 128)
+    b = E.make_point_source(g, 0, (64, 64))
+    opt = E.MgOptions(n_levels=4, cycle="v", nu1=2, nu2=2, damping=0.25, vanka_mode="full",
+                      sweep="red_black")
+    med = E.MediaModel(lam, mu, rho, gam)
+    mg = E.Multigrid(g, med, E.OperatorParams(2 / 3, omega, 0.5), opt)
+    D0 = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.0))
+    x = np.zeros(g.n_dofs(), complex)
+    res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=400))
+    om = O.MG(dims, 1 / 128, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.5, n_levels=4, cycle="v",
+              nu1=2, nu2=2, damping=0.25)
+    xr, info = om.solve(O.Op(dims, 1 / 128, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.0), b,
+                        restart=10, max_iterations=400)
+    assert res.status == info["status"]
+    assert abs(res.iterations - info["iterations"]) <= 1
+    assert rel(x, xr) < 1e-5
+    # the reported residual is the true residual
+    r = E.residual(D0, b, x)
+    assert np.linalg.norm(r) / np.linalg.norm(b) == pytest.approx(res.relres, rel=1e-6)
+
+
+def test_full_size_properties_3d():
+    """At the bench size (256^3 cells): linearity of the apply and of one
+    V-cycle, and the residual identity r = b - A x, on device buffers."""
+    import torch
+    n = 256
+    dims = (n, n, n)
+    g = E.StaggeredGrid(dims, 1.0 / n)
+    med = E.MediaModel.homogeneous(g, 2.0, 1.0, 1.0, 0.01)
+    med.gamma = E.build_attenuation_profile(g, 0.01, E.SpongeConfig(24))
+    omega = 2 * np.pi / (10 / n)
+    D = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.5))
+    N = g.n_dofs()
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(N, dtype=torch.complex128, device="cuda", generator=gen)
+    y = torch.randn(N, dtype=torch.complex128, device="cuda", generator=gen)
+    a = 0.3 - 1.7j
+    Ax = E.apply_mixed_operator(D, x)
+    Ay = E.apply_mixed_operator(D, y)
+    Axy = E.apply_mixed_operator(D, (a * x + y).contiguous())
+    lin = (Axy - (a * Ax + Ay)).abs().max() / Axy.abs().max()
+    assert lin.item() < 1e-13
+    r = E.residual(D, y, x)
+    assert ((r - (y - Ax)).abs().max() / r.abs().max()).item() < 1e-14

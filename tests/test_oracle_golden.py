@@ -1,0 +1,205 @@
+"""CPU: pin the C oracle (oracle/ehmg_oracle.c) to the reference.
+
+1. Golden vectors produced by the reference itself (oracle/_ref, built from
+   the unmodified reference headers) -- tests/golden/golden.npz.
+2. Known-answer values asserted by the reference's own tests
+   (/root/reference/proj/tests/*.cpp, cited per test).
+3. Direct randomized comparison against oracle/_ref when it is present.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+
+def media_of(c):
+    return O.Media(c["lam"], c["mu"], c["rho"], c["gam"])
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def test_golden_cases(golden):
+    seen = set()
+    for c in golden:
+        k, dims, h = c["kind"], c["dims"], c["h"]
+        seen.add(k)
+        if k == "apply":
+            beta, omega, alpha = c["par"]
+            op = O.Op(dims, h, media_of(c), beta, omega, alpha)
+            assert rel(op.apply(c["x"]), c["y"]) < 1e-13
+            assert rel(op.schur(c["x"]), c["ys"]) < 1e-13
+        elif k == "vanka":
+            beta, omega, alpha = c["par"]
+            op = O.Op(dims, h, media_of(c), beta, omega, alpha)
+            v = O.Vanka(op, int(c["mode"]))
+            assert rel(v.cache().ravel(), c["cache"]) < 1e-13
+            x = c["x"]
+            for _ in range(int(c["nsweeps"])):
+                x = v.sweep(c["b"], x, float(c["w"]), int(c["order"]))
+            assert rel(x, c["xs"]) < 1e-12
+        elif k == "transfer":
+            assert rel(O.restrict(dims, c["xf"]), c["r"]) < 1e-15
+            assert rel(O.prolong(dims, c["xc"]), c["p"]) < 1e-15
+        elif k == "coarsen":
+            assert rel(O.coarsen(dims, c["v"]), c["c"]) < 1e-15
+        elif k == "sponge":
+            g = O.attenuation(dims, 0.01, int(c["L"]), 1.0, bool(c["top"]))
+            assert np.array_equal(g, c["g"])
+        elif k == "mg":
+            beta, omega, alpha = c["par"]
+            nu = int(c["nu"])
+            mg = O.MG(dims, h, media_of(c), beta, omega, alpha, n_levels=int(c["nl"]),
+                      cycle=str(c["cyc"]), nu1=nu, nu2=nu, damping=0.55, vanka=str(c["vmode"]),
+                      sweep=str(c["sweep"]))
+            x = np.zeros_like(c["b"])
+            x = mg.cycle(c["b"], x)
+            x = mg.cycle(c["b"], x)
+            assert rel(x, c["x"]) < 1e-10
+        elif k == "solve":
+            beta, omega, alpha = c["par"]
+            mg = O.MG(dims, h, media_of(c), beta, omega, alpha, n_levels=int(c["nl"]), cycle="v",
+                      nu1=2, nu2=2, damping=float(c["w"]))
+            A0 = O.Op(dims, h, media_of(c), beta, omega, 0.0)
+            x, info = mg.solve(A0, c["b"], restart=10)
+            assert info["status"] == str(c["status"])
+            assert abs(info["iterations"] - int(c["iterations"])) <= 1
+            assert rel(x, c["x"]) < 1e-6
+    assert seen == {"apply", "vanka", "transfer", "coarsen", "sponge", "mg", "solve"}
+
+
+# ------------------------------------------------ reference known answers
+def _lin(box, idx):
+    r = idx[-1]
+    for a in range(len(box) - 2, -1, -1):
+        r = r * box[a] + idx[a]
+    return r
+
+
+def _off(dims):
+    shapes = O.comp_shapes(dims)
+    offs, o = [], 0
+    for s in shapes:
+        offs.append(o)
+        o += int(np.prod(s))
+    return offs, shapes
+
+
+def test_delta_responses():
+    """test_transfer.cpp:74 -- per-component stencil conventions."""
+    df = (8, 8)
+    dc = (4, 4)
+    of, sf = _off(df)
+    oc, scs = _off(dc)
+    xf = np.zeros(O.n_dofs(df), complex)
+    xf[of[0] + _lin(sf[0], (4, 4))] = 1
+    assert O.restrict(df, xf)[oc[0] + _lin(scs[0], (2, 2))].real == pytest.approx(0.25)
+    xf[:] = 0
+    xf[of[2] + _lin(sf[2], (4, 4))] = 1
+    assert O.restrict(df, xf)[oc[2] + _lin(scs[2], (2, 2))].real == pytest.approx(0.25)
+    xc = np.zeros(O.n_dofs(dc), complex)
+    xc[oc[2] + _lin(scs[2], (2, 2))] = 1
+    p = O.prolong(df, xc)
+    for i in (4, 5):
+        for j in (4, 5):
+            assert p[of[2] + _lin(sf[2], (i, j))].real == pytest.approx(9 / 16)
+    assert p[of[2] + _lin(sf[2], (6, 6))].real == pytest.approx(1 / 16)
+    xc[:] = 0
+    xc[oc[0] + _lin(scs[0], (2, 2))] = 1
+    p = O.prolong(df, xc)
+    assert p[of[0] + _lin(sf[0], (4, 4))].real == pytest.approx(0.75)
+    assert p[of[0] + _lin(sf[0], (5, 4))].real == pytest.approx(0.375)
+
+
+def test_transfers_preserve_constants_and_kill_checkerboard():
+    """test_transfer.cpp:112 / :140"""
+    for df in [(8, 6), (4, 6, 4)]:
+        dc = [d // 2 for d in df]
+        assert np.abs(O.restrict(df, np.ones(O.n_dofs(df), complex)) - 1).max() < 1e-15
+        assert np.abs(O.prolong(df, np.ones(O.n_dofs(dc), complex)) - 1).max() < 1e-15
+    df = (8, 8)
+    of, sf = _off(df)
+    x = np.zeros(O.n_dofs(df), complex)
+    p = np.array([[1.0 if (i + j) % 2 == 0 else -1.0 for i in range(8)] for j in range(8)]).ravel()
+    x[of[2]:] = p
+    oc, _ = _off((4, 4))
+    assert np.abs(O.restrict(df, x)[oc[2]:]).max() < 1e-15
+
+
+def test_vanka_cache_footprint():
+    """test_smoothers.cpp:134 -- 17/13 (2D) and 25/19 (3D) complex per cell."""
+    for dims, full, econ in [((4, 4), 17, 13), ((4, 4, 4), 25, 19)]:
+        n = O.n_cells(dims)
+        m = O.Media(np.full(n, 2.0), np.ones(n), np.ones(n), np.zeros(n))
+        op = O.Op(dims, 0.25, m, 2 / 3, 3.0, 0.1)
+        assert O.Vanka(op, 0).cache().shape[1] == full
+        assert O.Vanka(op, 1).cache().shape[1] == econ
+
+
+def test_pressure_row_nnz_and_structure():
+    """test_operator.cpp:75 / :94 / :132 / :153"""
+    dims = (8, 8)
+    n = O.n_cells(dims)
+    m = O.Media(np.full(n, 4.0), np.ones(n), np.ones(n), np.zeros(n))
+    of, _ = _off(dims)
+    row = of[2] + _lin(dims, (4, 4))
+    A = O.Op(dims, 0.125, m, 2 / 3, 3.0, 0.0).dense()
+    assert np.count_nonzero(A[row]) == 13
+    A1 = O.Op(dims, 0.125, m, 1.0, 3.0, 0.0).dense()
+    assert np.count_nonzero(A1[row]) == 5
+    rng = np.random.default_rng(3)
+    dims = (6, 5)
+    n = O.n_cells(dims)
+    mr = O.Media(3 * rng.uniform(.5, 2, n), rng.uniform(.5, 2, n), rng.uniform(.5, 2, n),
+                 0.05 * rng.uniform(.5, 2, n))
+    of, _ = _off(dims)
+    A = O.Op(dims, 0.2, mr, 2 / 3, 4.0, 0.1).dense()
+    assert np.abs(A[of[0]:of[1], of[1]:of[2]]).max() == 0.0  # u_x rows never touch u_y
+    A0 = O.Op(dims, 0.2, mr, 2 / 3, 4.0, 0.0).dense()
+    Aa = O.Op(dims, 0.2, mr, 2 / 3, 4.0, 0.25).dense()
+    d = Aa - A0
+    assert np.abs(d[of[2]:]).max() == 0.0
+    assert np.abs(d.real).max() < 1e-14 and np.abs(d.imag).max() > 0.1
+    mz = O.Media(mr.lam, mr.mu, mr.rho, np.zeros(n))
+    assert np.abs(O.Op(dims, 0.2, mz, 2 / 3, 0.0, 0.0).dense().imag).max() == 0.0
+
+
+def test_schur_matches_dense_elimination():
+    """test_operator.cpp:108 -- pressure elimination vs dense Schur complement."""
+    rng = np.random.default_rng(17)
+    dims = (6, 6)
+    n = O.n_cells(dims)
+    m = O.Media(3 * rng.uniform(.5, 2, n), rng.uniform(.5, 2, n), rng.uniform(.5, 2, n),
+                0.05 * rng.uniform(.5, 2, n))
+    op = O.Op(dims, 1 / 6, m, 2 / 3, 5.5, 0.12)
+    A = op.dense()
+    nu = O.n_dofs(dims) - n
+    S = A[:nu, :nu] - A[:nu, nu:] @ np.linalg.inv(A[nu:, nu:]) @ A[nu:, :nu]
+    x = rng.uniform(-1, 1, op.n) + 1j * rng.uniform(-1, 1, op.n)
+    x[nu:] = 0
+    ys = op.schur(x)
+    assert rel(S @ x[:nu], ys[:nu]) < 1e-12
+
+
+def test_point_source_and_sponge():
+    """test_grid.cpp:95 and media.hpp:95 examples."""
+    g = O.attenuation((40, 40), 0.01, 0)
+    assert np.all(g == 0.01)
+    g = O.attenuation((50, 50), 0.01, 20)
+    assert g.max() == pytest.approx(0.01 + 1.0)
+    with pytest.raises(ValueError):
+        O.attenuation((30, 30), 0.01, 20)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_oracle_matches_reference_randomized():
+    rng = np.random.default_rng(11)
+    for dims in [(10, 6), (7, 9), (6, 4, 5), (4, 6, 6)]:
+        n = O.n_cells(dims)
+        m = O.Media(3 * rng.uniform(.5, 2, n), rng.uniform(.5, 2, n), rng.uniform(.5, 2, n),
+                    0.05 * rng.uniform(.5, 2, n))
+        for beta in (1.0, 2 / 3, 0.55):
+            x = rng.uniform(-1, 1, O.n_dofs(dims)) + 1j * rng.uniform(-1, 1, O.n_dofs(dims))
+            y = O.Op(dims, 0.1, m, beta, 7.0, 0.2).apply(x)
+            assert rel(y, O.ref_apply(dims, 0.1, m, beta, 7.0, 0.2, x)) < 1e-14
