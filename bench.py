@@ -160,10 +160,8 @@ def alg_bytes(kernel, n, level):
         return 16 * 3 * N + 32 * C
     if kernel == "apply":
         return 16 * 2 * N + 32 * C
-    if kernel == "vanka_corr":     # x neighbourhood, b at owned DOFs, media, cache + delta of half the cells
-        return 16 * N + 16 * (Nu + C // 2) + 32 * C + 16 * 25 * (C // 2) + 16 * 7 * (C // 2)
-    if kernel == "vanka_apply":
-        return 16 * 7 * (C // 2) + 2 * 16 * (Nu + C // 2)
+    if kernel == "vanka_update":   # colour-half of the factor cache, r and x at the owned DOFs
+        return 16 * 25 * (C // 2) + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
     if kernel == "restrict":
         return 16 * N + 16 * ndofs(level_dims(n, level + 1))
     if kernel == "prolong_add":

@@ -158,47 +158,80 @@ EH_HD bool colour_cell(const Geo& g, int64_t t, int color, int* c) {
   return ((c[0] + c[1] + c[2]) & 1) == color;
 }
 
-// Red-black phase 1: corrections of every cell of `color` from the state at
-// the start of the colour (vanka.hpp:205), deferred into `delta`.
+// Index of cell c within its colour class (inverse of colour_cell).
+EH_HD int64_t colour_index(const Geo& g, const int* c) {
+  if (g.n[0] % 2 == 0) return ((int64_t)c[1] + (int64_t)g.n[1] * c[2]) * (g.n[0] / 2) + c[0] / 2;
+  return g.clin(c);
+}
+
+// Factor cache re-laid out per colour, component-major (SoA): entry e of the
+// cell with colour index t of colour col lives at soa[(col*stride + e)*nt + t],
+// so a warp of same-colour cells reads each entry fully coalesced.
 template <int ND>
-__global__ void __launch_bounds__(kThreads) k_vanka_corr(Geo g, OpPar P, const Cell* __restrict__ m, int full,
-                                                         const cplx* __restrict__ cache,
-                                                         const cplx* __restrict__ b,
-                                                         const cplx* __restrict__ x, int color,
-                                                         cplx* __restrict__ delta) {
-  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
-  const int nl = 2 * ND + 1;
-  FieldAcc A{x};
-  GRID_STRIDE(t, colour_threads(g)) {
+__global__ void k_vanka_to_soa(Geo g, int stride, const cplx* __restrict__ aos, cplx* __restrict__ soa,
+                               int inverse) {
+  const int64_t nt = colour_threads(g);
+  GRID_STRIDE(u, 2 * nt) {
+    const int col = (int)(u / nt);
+    const int64_t t = u % nt;
     int c[3];
-    if (!colour_cell(g, t, color, c)) continue;
+    if (!colour_cell(g, t, col, c)) continue;
     const int64_t ci = g.clin(c);
-    cplx du[2 * ND], dp;
-    vanka_corr<ND>(g, P, m, full, cache + ci * stride, b, A, c, du, dp);
-    cplx* slot = delta + ci * nl;
-    for (int q = 0; q < 2 * ND; ++q) slot[q] = du[q];
-    slot[2 * ND] = dp;
+    for (int e = 0; e < stride; ++e) {
+      const int64_t si = ((int64_t)col * stride + e) * nt + t;
+      if (inverse) const_cast<cplx*>(aos)[ci * stride + e] = soa[si];
+      else soa[si] = aos[ci * stride + e];
+    }
   }
 }
 
-// Red-black phase 2: x += w * delta on the DOFs owned by cells of `color`.
-// Cells of one colour share no DOFs, so the writes commute.
+// Red-black colour update (vanka.hpp:157 + :184): r = b - A x was computed
+// for the state at the start of the colour (vanka.hpp:205); every cell of
+// `color` solves its local system from r and adds w * correction to the DOFs
+// it owns. Cells of one colour share no DOFs, so the in-place writes commute.
 template <int ND>
-__global__ void __launch_bounds__(kThreads) k_vanka_apply(Geo g, int color, const cplx* __restrict__ delta,
-                                                          double w, cplx* __restrict__ x) {
-  const int nl = 2 * ND + 1;
-  GRID_STRIDE(t, colour_threads(g)) {
+__global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, int full, const cplx* __restrict__ soa,
+                                                           const cplx* __restrict__ r, int color, double w,
+                                                           cplx* __restrict__ x) {
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
+  const int blk_w = full ? 8 : 6;
+  const int64_t nt = colour_threads(g);
+  GRID_STRIDE(t, nt) {
     int c[3];
     if (!colour_cell(g, t, color, c)) continue;
-    const int64_t ci = g.clin(c);
-    const cplx* slot = delta + ci * nl;
+    const cplx* q = soa + (int64_t)color * stride * nt + t;
+    auto Q = [&](int e) { return q[(int64_t)e * nt]; };
+    const int64_t pi = g.off[ND] + g.clin(c);
+    int64_t fi[ND][2];
+    cplx rr[ND][2];
+    cplx dpa = r[pi];
+#pragma unroll
     for (int k = 0; k < ND; ++k) {
       int f1[3];
       sh(c, k, 1, f1);
-      x[g.off[k] + g.flin(k, c)] += w * slot[2 * k];
-      x[g.off[k] + g.flin(k, f1)] += w * slot[2 * k + 1];
+      fi[k][0] = g.off[k] + g.flin(k, c);
+      fi[k][1] = g.off[k] + g.flin(k, f1);
+      rr[k][0] = r[fi[k][0]];
+      rr[k][1] = r[fi[k][1]];
+      const int hk = k * blk_w + (full ? 6 : 4);
+      dpa -= Q(hk) * rr[k][0] + Q(hk + 1) * rr[k][1];
     }
-    x[g.off[ND] + ci] += w * slot[2 * ND];
+    const cplx dp = Q(stride - 1) * dpa;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const int bk = k * blk_w, gk = bk + (full ? 4 : 2);
+      cplx du0, du1;
+      if (full) {
+        du0 = Q(bk + 0) * rr[k][0] + Q(bk + 1) * rr[k][1] - Q(gk) * dp;
+        du1 = Q(bk + 2) * rr[k][0] + Q(bk + 3) * rr[k][1] - Q(gk + 1) * dp;
+      } else {
+        du0 = Q(bk + 0) * rr[k][0] - Q(gk) * dp;
+        du1 = Q(bk + 1) * rr[k][1] - Q(gk + 1) * dp;
+      }
+      x[fi[k][0]] += w * du0;
+      x[fi[k][1]] += w * du1;
+    }
+    x[pi] += w * dp;
   }
 }
 
@@ -212,8 +245,11 @@ __global__ void k_vanka_lex(Geo g, OpPar P, const Cell* __restrict__ m, int full
   FieldAcc A{x};
   for (int64_t ci = 0; ci < g.ncells; ++ci) {
     int c[3] = {(int)(ci % g.n[0]), (int)((ci / g.n[0]) % g.n[1]), (int)(ci / ((int64_t)g.n[0] * g.n[1]))};
-    cplx du[2 * ND], dp;
-    vanka_corr<ND>(g, P, m, full, cache + ci * stride, b, A, c, du, dp);
+    cplx du[2 * ND], dp, q[4 * 8 + 1];
+    const int color = (c[0] + c[1] + c[2]) & 1;
+    const int64_t nt = colour_threads(g), t = colour_index(g, c);
+    for (int e = 0; e < stride; ++e) q[e] = cache[((int64_t)color * stride + e) * nt + t];
+    vanka_corr<ND>(g, P, m, full, q, b, A, c, du, dp);
     for (int k = 0; k < ND; ++k) {
       int f1[3];
       sh(c, k, 1, f1);

@@ -203,49 +203,59 @@ static Geo coarse_geo(const Geo& g) {
 }
 
 // Vanka factor cache + red-black / lexicographic sweeps on one level.
+// Red-black colour = fused residual kernel (stencil) + coalesced local
+// solve/update kernel reading the colour-major SoA factor cache.
 struct Smoother {
   int full = 1, stride = 0;
-  DBuf<cplx> cache, delta;
+  DBuf<cplx> soa, res;
   void build(const Geo& g, const OpPar& P, const Cell* m, int full_, cudaStream_t s) {
     full = full_;
     stride = g.nd * ((full ? 4 : 2) + 4) + 1;
-    cache.alloc(g.ncells * stride);
-    delta.alloc(g.ncells * (2 * g.nd + 1));
-    DBuf<int> bad(1);
-    bad.zero(s);
-    if (g.nd == 3)
-      k_vanka_build<3><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, bad.p);
-    else
-      k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, bad.p);
+    {
+      DBuf<cplx> aos(g.ncells * stride);
+      DBuf<int> bad(1);
+      bad.zero(s);
+      if (g.nd == 3)
+        k_vanka_build<3><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, aos.p, bad.p);
+      else
+        k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, aos.p, bad.p);
+      CK(cudaGetLastError());
+      int hb = 0;
+      CK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (hb) throw Err(EHMG_ERUNTIME, "vanka: singular local cell system");
+      const int64_t nt = colour_threads(g);
+      soa.alloc(2 * nt * stride);
+      if (g.nd == 3) k_vanka_to_soa<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, aos.p, soa.p, 0);
+      else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, aos.p, soa.p, 0);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));
+    }
+    res.alloc(g.ndofs);
+  }
+  // reference (AoS, vanka.hpp:72) layout of the cache, for inspection
+  void cache_aos(const Geo& g, cplx* out, cudaStream_t s) const {
+    const int64_t nt = colour_threads(g);
+    if (g.nd == 3) k_vanka_to_soa<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, out, soa.p, 1);
+    else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, out, soa.p, 1);
     CK(cudaGetLastError());
-    int hb = 0;
-    CK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (hb) throw Err(EHMG_ERUNTIME, "vanka: singular local cell system");
   }
   void sweep(const Geo& g, const OpPar& P, const Cell* m, const cplx* b, cplx* x, double w,
              int order, cudaStream_t s) {
     if (order == 0) {
-      if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, m, full, cache.p, b, x, w);
-      else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, m, full, cache.p, b, x, w);
+      if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, m, full, soa.p, b, x, w);
+      else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, m, full, soa.p, b, x, w);
       CK(cudaGetLastError());
       return;
     }
     const int64_t nt = colour_threads(g);
     for (int color = 0; color < 2; ++color) {
-      if (g.nd == 3) {
-        {
-          Prof pf("vanka_corr", s);
-          k_vanka_corr<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, b, x,
-                                                                      color, delta.p);
-        }
-        Prof pf("vanka_apply", s);
-        k_vanka_apply<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, color, delta.p, w, x);
-      } else {
-        k_vanka_corr<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, P, m, full, cache.p, b, x,
-                                                                    color, delta.p);
-        k_vanka_apply<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, color, delta.p, w, x);
-      }
+      launch_residual(g, P, m, x, b, res.p, s);
+      Prof pf("vanka_update", s);
+      if (g.nd == 3)
+        k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, color, w, x);
+      else
+        k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, color, w, x);
       CK(cudaGetLastError());
     }
   }
@@ -712,8 +722,10 @@ int ehmg_vanka_per_cell_complex_count(ehmg_vanka v) { return v ? v->sm.stride : 
 
 int ehmg_vanka_cache(ehmg_vanka v, double* out) {
   return guard([&] {
-    CK(cudaMemcpyAsync(out, v->sm.cache.p, sizeof(cplx) * v->sm.cache.n, cudaMemcpyDeviceToHost,
-                       v->op->s));
+    const Geo& g = v->op->g;
+    DBuf<cplx> aos(g.ncells * v->sm.stride);
+    v->sm.cache_aos(g, aos.p, v->op->s);
+    CK(cudaMemcpyAsync(out, aos.p, sizeof(cplx) * aos.n, cudaMemcpyDeviceToHost, v->op->s));
     CK(cudaStreamSynchronize(v->op->s));
   });
 }
