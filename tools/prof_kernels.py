@@ -1,0 +1,47 @@
+"""Short driver for ncu captures of the hot kernels at the bench size.
+
+    python tools/prof_kernels.py [--n 256] [--what apply|cycle]
+"""
+import argparse
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2307_03242_b200 as E  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--what", default="apply")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    n = a.n
+    g = E.StaggeredGrid((n, n, n), 1.0 / n)
+    med = E.MediaModel.homogeneous(g, 2.0, 1.0, 1.0, 0.01)
+    med.gamma = E.build_attenuation_profile(g, 0.01, E.SpongeConfig(min(24, n // 4)))
+    omega = 2 * math.pi / (10 / n)
+    N = g.n_dofs()
+    r = torch.randn(N, dtype=torch.complex128, device="cuda")
+    y = torch.empty_like(r)
+    if a.what == "apply":
+        D = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.5))
+        for _ in range(a.reps):
+            E.residual(D, r, r, y)
+    else:
+        opt = E.MgOptions(n_levels=5 if n >= 64 else 3, cycle="v", nu1=2, nu2=2, damping=0.25,
+                          vanka_mode="full", sweep="red_black")
+        mg = E.Multigrid(g, med, E.OperatorParams(2 / 3, omega, 0.5), opt)
+        for _ in range(a.reps):
+            mg.precondition(r, y)
+    torch.cuda.synchronize()
+    print("ok", float(y.abs().max()))
+
+
+if __name__ == "__main__":
+    main()
