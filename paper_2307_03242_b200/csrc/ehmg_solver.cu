@@ -138,10 +138,30 @@ static void validate_media(int64_t n, const double* lam, const double* mu, const
   }
 }
 
-// Raw cell media on the device (lambda, mu, rho, gamma) + packed form.
+// Cell media views: packed {mu, rho, gamma, 1/(lambda+mu)} per cell for the
+// generic kernels, and the same four fields as consecutive arrays (SoA) for
+// the TMA-staged 3D stencil.
+struct MediaRef {
+  const Cell* packed;
+  const double* soa;
+};
+
+__global__ void k_media_soa(int64_t n, const Cell* __restrict__ in, double* __restrict__ out) {
+  GRID_STRIDE(i, n) {
+    const Cell c = in[i];
+    out[i] = c.x;
+    out[n + i] = c.y;
+    out[2 * n + i] = c.z;
+    out[3 * n + i] = c.w;
+  }
+}
+
+// Raw cell media on the device (lambda, mu, rho, gamma) + packed forms.
 struct DevMedia {
   DBuf<double> raw[4];
   DBuf<Cell> packed;
+  DBuf<double> soa;
+  MediaRef ref() const { return MediaRef{packed.p, soa.p}; }
   void upload(int64_t n, const double* const* f, cudaStream_t s) {
     for (int q = 0; q < 4; ++q) {
       raw[q].alloc(n);
@@ -153,6 +173,9 @@ struct DevMedia {
     packed.alloc(n);
     k_pack_media<<<grid_for(n), kThreads, 0, s>>>(n, raw[0].p, raw[1].p, raw[2].p, raw[3].p,
                                                    packed.p);
+    CK(cudaGetLastError());
+    soa.alloc(4 * n);
+    k_media_soa<<<grid_for(n), kThreads, 0, s>>>(n, packed.p, soa.p);
     CK(cudaGetLastError());
   }
   void coarsen_into(const Geo& gf, DevMedia& out, const Geo& gc, cudaStream_t s) const {
@@ -170,11 +193,12 @@ struct DevMedia {
 
 // ----------------------------------------------------------- level kernels
 // r = b - A x (b != null) or y = A x.
-static void launch_residual(const Geo& g, const OpPar& P, const Cell* m, const cplx* x,
+static void launch_residual(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* x,
                             const cplx* b, cplx* y, cudaStream_t s) {
   Prof pf(b ? "residual" : "apply", s);
+  const Cell* m = mr.packed;
   if (g.nd == 3 && stencil3d_supported(g)) {
-    launch_stencil3d(g, P, m, x, b, y, s);
+    launch_stencil3d(g, P, mr.soa, x, b, y, s);
   } else if (g.nd == 3) {
     k_apply_generic<3><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
   } else {
@@ -240,8 +264,9 @@ struct Smoother {
     else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, out, soa.p, 1);
     CK(cudaGetLastError());
   }
-  void sweep(const Geo& g, const OpPar& P, const Cell* m, const cplx* b, cplx* x, double w,
+  void sweep(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
              int order, cudaStream_t s) {
+    const Cell* m = mr.packed;
     if (order == 0) {
       if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, m, full, soa.p, b, x, w);
       else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, m, full, soa.p, b, x, w);
@@ -250,7 +275,7 @@ struct Smoother {
     }
     const int64_t nt = colour_threads(g);
     for (int color = 0; color < 2; ++color) {
-      launch_residual(g, P, m, x, b, res.p, s);
+      launch_residual(g, P, mr, x, b, res.p, s);
       Prof pf("vanka_update", s);
       if (g.nd == 3)
         k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, color, w, x);
@@ -527,8 +552,8 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
   }
   Level& lev = *L[l];
   Level& nxt = *L[l + 1];
-  for (int q = 0; q < opt.nu1; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.packed.p, b, x, opt.damping, opt.sweep, s);
-  launch_residual(lev.g, lev.P, lev.media.packed.p, x, b, lev.r.p, s);
+  for (int q = 0; q < opt.nu1; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s);
+  launch_residual(lev.g, lev.P, lev.media.ref(), x, b, lev.r.p, s);
   launch_transfer(lev.g, nxt.g, true, lev.r.p, nxt.bc.p, false, s);
   CK(cudaMemsetAsync(nxt.ec.p, 0, sizeof(cplx) * nxt.g.ndofs, s));
   const bool next_coarsest = (l + 2 == nl);
@@ -550,7 +575,7 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
         nxt.inner.init(nxt.g.ndofs, opt.k_inner_iterations, s);
         std::vector<double> hist;
         Fgmres::Fn A = [&](const cplx* in, cplx* out) {
-          launch_residual(nxt.g, nxt.P, nxt.media.packed.p, in, nullptr, out, s);
+          launch_residual(nxt.g, nxt.P, nxt.media.ref(), in, nullptr, out, s);
         };
         Fgmres::Fn M = [&](const cplx* in, cplx* out) {
           CK(cudaMemsetAsync(out, 0, sizeof(cplx) * nxt.g.ndofs, s));
@@ -562,7 +587,7 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
   }
   g_level = l;
   launch_transfer(lev.g, nxt.g, false, nxt.ec.p, x, true, s);
-  for (int q = 0; q < opt.nu2; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.packed.p, b, x, opt.damping, opt.sweep, s);
+  for (int q = 0; q < opt.nu2; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s);
 }
 
 // ------------------------------------------------------------ helpers
@@ -688,7 +713,7 @@ int ehmg_apply_mixed_operator(ehmg_op op, const double* x, double* y, int where)
     const cplx* dx;
     to_dev(x, op->hx, n, where, op->s, &dx);
     cplx* dy = out_dev(y, op->hy, n, where);
-    launch_residual(op->g, op->P, op->media.packed.p, dx, nullptr, dy, op->s);
+    launch_residual(op->g, op->P, op->media.ref(), dx, nullptr, dy, op->s);
     from_dev(y, dy, n, where, op->s);
   });
 }
@@ -700,7 +725,7 @@ int ehmg_residual(ehmg_op op, const double* b, const double* x, double* r, int w
     to_dev(x, op->hx, n, where, op->s, &dx);
     to_dev(b, op->hb, n, where, op->s, &db);
     cplx* dr = out_dev(r, op->hy, n, where);
-    launch_residual(op->g, op->P, op->media.packed.p, dx, db, dr, op->s);
+    launch_residual(op->g, op->P, op->media.ref(), dx, db, dr, op->s);
     from_dev(r, dr, n, where, op->s);
   });
 }
@@ -745,7 +770,7 @@ int ehmg_vanka_sweep(ehmg_vanka v, const double* b, double* x, double w, int ord
       CK(cudaMemcpyAsync(op->hx.p, x, sizeof(cplx) * n, cudaMemcpyHostToDevice, op->s));
       dx = op->hx.p;
     }
-    for (int q = 0; q < nsweeps; ++q) v->sm.sweep(op->g, op->P, op->media.packed.p, db, dx, w, order, op->s);
+    for (int q = 0; q < nsweeps; ++q) v->sm.sweep(op->g, op->P, op->media.ref(), db, dx, w, order, op->s);
     from_dev(x, dx, n, where, op->s);
   });
 }
@@ -1005,7 +1030,7 @@ int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int wher
     Fgmres fg;
     fg.init(n, opt->restart, s);
     Fgmres::Fn Af = [&](const cplx* in, cplx* out) {
-      launch_residual(A->g, A->P, A->media.packed.p, in, nullptr, out, s);
+      launch_residual(A->g, A->P, A->media.ref(), in, nullptr, out, s);
     };
     Fgmres::Fn Mf = [&](const cplx* in, cplx* out) {
       if (M) M->precondition(in, out);

@@ -82,7 +82,7 @@ def test_golden_through_cuda(golden):
             assert rel(x, c["x"]) < 1e-6
 
 
-@pytest.mark.parametrize("dims", [(64, 48), (128, 128), (24, 20, 16), (32, 32, 32), (40, 24, 36)])
+@pytest.mark.parametrize("dims", [(64, 48), (128, 128), (24, 20, 16), (32, 32, 32), (40, 24, 36), (24, 20, 80), (66, 10, 12)])
 @pytest.mark.parametrize("beta", [1.0, 2 / 3])
 def test_apply_vs_oracle(dims, beta):
     rng = np.random.default_rng(hash((dims, beta)) % 2**32)
