@@ -213,100 +213,100 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
       cplx d00 = mk(0, 0), d11 = mk(0, 0);
 
       if (act) {
-        // F00: cell, pair +x, in-plane axis y
+        // Every shared-memory value this position needs is loaded once into
+        // registers (grouped per component to bound register pressure).
+        const double al = P.alpha, w2 = P.omega2;
+        const double mc00 = MUc[ui], mc_l = MUc[ui - 1], mc_b = MUc[ui - S3_UX], mc_lb = MUc[ui - 1 - S3_UX];
+        const double mm00 = MUm[ui], mm_l = MUm[ui - 1], mm_b = MUm[ui - S3_UX];
+        // mu on the edges (operator.hpp:108 order: first axis outer, second inner)
+        const double mu01 = (mc_lb + mc_l + mc_b + mc00) * mu01s;
+        const double mu02 = (mm_l + mc_l + mm00 + mc00) * (ix * izc);
+        const double mu12 = (mm_b + mc_b + mm00 + mc00) * (iy * izc);
+        const double* RHc = S.rho[z & 3];
+        const double* RHp = S.rho[(z + 1) & 3];
+        const double* GAc = S.gam[z & 3];
+        const double* GAp = S.gam[(z + 1) & 3];
+        const double rp00 = RHp[ui], gp00 = GAp[ui];
+        auto md = [&](double sr, double sg, double ic) {
+          const double rho_f = sr * ic, gam_f = sg * ic + al;
+          return mk(w2 * rho_f, -w2 * gam_f * rho_f);
+        };
+        const bool zin = z + 1 >= 0 && z + 1 < n2;
+        const int qb = (z + 1) & 1;
+        // ---- component 0: F00 (cell, +x pair, in-plane y), F01 (edge01, -y pair, in-plane x)
         {
-          auto dn = [&](int o) { return V0[ui + o + 1] - V0[ui + o]; };
-          const cplx rn = dn(-S3_UX) + dn(S3_UX) + 2.0 * dn(0);
-          const cplx s = r00m + rn + 2.0 * r00c;
-          const cplx v = beta * (U0[ui + 1] - U0[ui]) + w * s;
-          d00 = v * (P.inv_wsum[fl00 | zA] * ih);
-          S.f[0][t] = MUc[ui] * d00;
+          const cplx vmm = V0[ui - S3_UX - 1], vm0 = V0[ui - S3_UX], vmp = V0[ui - S3_UX + 1];
+          const cplx v0m = V0[ui - 1], v00 = V0[ui], v0p = V0[ui + 1];
+          const cplx vp0 = V0[ui + S3_UX], vpp = V0[ui + S3_UX + 1];
+          const cplx u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - S3_UX];
+          const cplx rn0 = (vmp - vm0) + (vpp - vp0) + 2.0 * (v0p - v00);
+          const cplx sz0 = r00m + rn0 + 2.0 * r00c;
+          d00 = (beta * (u0p - u00) + w * sz0) * (P.inv_wsum[fl00 | zA] * ih);
+          S.f[0][t] = mc00 * d00;
           r00m = r00c;
-          r00c = rn;
-        }
-        // F11: cell, pair +y, in-plane axis x
-        {
-          auto dn = [&](int o) { return V1[ui + o + S3_UX] - V1[ui + o]; };
-          const cplx rn = dn(-1) + dn(1) + 2.0 * dn(0);
-          const cplx s = r11m + rn + 2.0 * r11c;
-          const cplx v = beta * (U1[ui + S3_UX] - U1[ui]) + w * s;
-          d11 = v * (P.inv_wsum[zB | fl11] * ih);
-          S.f[1][t] = MUc[ui] * d11;
-          r11m = r11c;
-          r11c = rn;
-        }
-        // mu on the (0,1) edge at plane z (cells x-1..x, y-1..y; operator.hpp:108 order)
-        const double mu01 = (MUc[ui - 1 - S3_UX] + MUc[ui - 1] + MUc[ui - S3_UX] + MUc[ui]) * mu01s;
-        // F01: edge (0,1), pair u0(b)-u0(b-y), in-plane axis x
-        {
-          auto dn = [&](int o) { return V0[ui + o] - V0[ui + o - S3_UX]; };
-          const cplx rn = dn(-1) + dn(1) + 2.0 * dn(0);
-          const cplx s = r01m + rn + 2.0 * r01c;
-          const cplx v = beta * (U0[ui] - U0[ui - S3_UX]) + w * s;
-          S.f[2][t] = mu01 * (v * (P.inv_wsum[zB | fl01] * ih));
+          r00c = rn0;
+          const cplx rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
+          const cplx sz1 = r01m + rn1 + 2.0 * r01c;
+          S.f[2][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[zB | fl01] * ih));
           r01m = r01c;
-          r01c = rn;
+          r01c = rn1;
+          S.di[1][t] = v00 - u00;  // d02 at edge (q, z+1)
+          S.q[qb][0][t] = (zin && q0ok) ? md(RHp[ui - 1] + rp00, GAp[ui - 1] + gp00, ix) * v00 : mk(0, 0);
         }
-        // F10: edge (0,1), pair u1(b)-u1(b-x), in-plane axis y
+        // ---- component 1: F11 (cell, +y pair, in-plane x), F10 (edge01, -x pair, in-plane y)
         {
-          auto dn = [&](int o) { return V1[ui + o] - V1[ui + o - 1]; };
-          const cplx rn = dn(-S3_UX) + dn(S3_UX) + 2.0 * dn(0);
-          const cplx s = r10m + rn + 2.0 * r10c;
-          const cplx v = beta * (U1[ui] - U1[ui - 1]) + w * s;
-          S.f[3][t] = mu01 * (v * (P.inv_wsum[zB | fl10] * ih));
+          const cplx vmm = V1[ui - S3_UX - 1], vm0 = V1[ui - S3_UX];
+          const cplx v0m = V1[ui - 1], v00 = V1[ui], v0p = V1[ui + 1];
+          const cplx vpm = V1[ui + S3_UX - 1], vp0 = V1[ui + S3_UX], vpp = V1[ui + S3_UX + 1];
+          const cplx u00 = U1[ui], up0 = U1[ui + S3_UX], u0m = U1[ui - 1];
+          const cplx rn0 = (vpm - v0m) + (vpp - v0p) + 2.0 * (vp0 - v00);
+          const cplx sz0 = r11m + rn0 + 2.0 * r11c;
+          d11 = (beta * (up0 - u00) + w * sz0) * (P.inv_wsum[zB | fl11] * ih);
+          S.f[1][t] = mc00 * d11;
+          r11m = r11c;
+          r11c = rn0;
+          const cplx rn1 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
+          const cplx sz1 = r10m + rn1 + 2.0 * r10c;
+          S.f[3][t] = mu01 * ((beta * (u00 - u0m) + w * sz1) * (P.inv_wsum[zB | fl10] * ih));
           r10m = r10c;
-          r10c = rn;
+          r10c = rn1;
+          S.di[2][t] = v00 - u00;  // d12 at edge (q, z+1)
+          S.q[qb][1][t] =
+              (zin && q1ok) ? md(RHp[ui - S3_UX] + rp00, GAp[ui - S3_UX] + gp00, iy) * v00 : mk(0, 0);
         }
-        // F20: edge (0,2) at plane z, pair u2(b)-u2(b-x), in-plane axis y
+        // ---- component 2: F20 (edge02, -x pair, in-plane y), F21 (edge12, -y pair, in-plane x)
         {
-          const double mu02 = (MUm[ui - 1] + MUc[ui - 1] + MUm[ui] + MUc[ui]) * (ix * izc);
-          auto dn = [&](int o) { return V2[ui + o] - V2[ui + o - 1]; };
-          const cplx rn = dn(-S3_UX) + dn(S3_UX) + 2.0 * dn(0);
-          const cplx s = r20m + rn + 2.0 * r20c;
-          const cplx v = beta * (U2[ui] - U2[ui - 1]) + w * s;
-          S.f[4][t] = mu02 * (v * (P.inv_wsum[fl20 | zC] * ih));
+          const cplx vmm = V2[ui - S3_UX - 1], vm0 = V2[ui - S3_UX], vmp = V2[ui - S3_UX + 1];
+          const cplx v0m = V2[ui - 1], v00 = V2[ui], v0p = V2[ui + 1];
+          const cplx vpm = V2[ui + S3_UX - 1], vp0 = V2[ui + S3_UX];
+          const cplx u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - S3_UX];
+          const cplx rn0 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
+          const cplx sz0 = r20m + rn0 + 2.0 * r20c;
+          S.f[4][t] = mu02 * ((beta * (u00 - u0m) + w * sz0) * (P.inv_wsum[fl20 | zC] * ih));
           r20m = r20c;
-          r20c = rn;
-        }
-        // F21: edge (1,2) at plane z, pair u2(b)-u2(b-y), in-plane axis x
-        {
-          const double mu12 = (MUm[ui - S3_UX] + MUc[ui - S3_UX] + MUm[ui] + MUc[ui]) * (iy * izc);
-          auto dn = [&](int o) { return V2[ui + o] - V2[ui + o - S3_UX]; };
-          const cplx rn = dn(-1) + dn(1) + 2.0 * dn(0);
-          const cplx s = r21m + rn + 2.0 * r21c;
-          const cplx v = beta * (U2[ui] - U2[ui - S3_UX]) + w * s;
-          S.f[5][t] = mu12 * (v * (P.inv_wsum[fl21 | zC] * ih));
+          r20c = rn0;
+          const cplx rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
+          const cplx sz1 = r21m + rn1 + 2.0 * r21c;
+          S.f[5][t] = mu12 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[fl21 | zC] * ih));
           r21m = r21c;
-          r21c = rn;
-        }
-        // in-plane difference fields
-        S.di[0][t] = V2[ui] - U2[ui];  // d22 at cell (q, z)
-        S.di[1][t] = V0[ui] - U0[ui];  // d02 at edge (q, z+1)
-        S.di[2][t] = V1[ui] - U1[ui];  // d12 at edge (q, z+1)
-        // mass products at plane z+1 (operator.hpp:132, :365)
-        {
-          const double* RHc = S.rho[z & 3];
-          const double* RHp = S.rho[(z + 1) & 3];
-          const double* GAc = S.gam[z & 3];
-          const double* GAp = S.gam[(z + 1) & 3];
-          const double al = P.alpha, w2 = P.omega2;
-          auto md = [&](double sr, double sg, double ic) {
-            const double rho_f = sr * ic, gam_f = sg * ic + al;
-            return mk(w2 * rho_f, -w2 * gam_f * rho_f);
-          };
-          const bool zin = z + 1 >= 0 && z + 1 < n2;
-          cplx q0 = mk(0, 0), q1 = mk(0, 0), q2 = mk(0, 0);
-          if (zin && q0ok) q0 = md(RHp[ui - 1] + RHp[ui], GAp[ui - 1] + GAp[ui], ix) * V0[ui];
-          if (zin && q1ok) q1 = md(RHp[ui - S3_UX] + RHp[ui], GAp[ui - S3_UX] + GAp[ui], iy) * V1[ui];
-          if (z + 1 >= 0 && z + 1 <= n2 && q2ok) q2 = md(RHc[ui] + RHp[ui], GAc[ui] + GAp[ui], izp) * V2[ui];
-          S.q[(z + 1) & 1][0][t] = q0;
-          S.q[(z + 1) & 1][1][t] = q1;
-          S.q[(z + 1) & 1][2][t] = q2;
+          r21c = rn1;
+          S.di[0][t] = v00 - u00;  // d22 at cell (q, z)
+          S.q[qb][2][t] = (z + 1 >= 0 && z + 1 <= n2 && q2ok)
+                              ? md(RHc[ui] + rp00, GAc[ui] + gp00, izp) * v00
+                              : mk(0, 0);
         }
       }
       __syncthreads();
 
       if (interior) {
+        // residual mode: fetch b for this plane's rows early (latency overlap)
+        cplx bb0 = mk(0, 0), bb1 = mk(0, 0), bb2 = mk(0, 0), bb3 = mk(0, 0);
+        if (b && z >= zb) {
+          if (v0 && z < n2) bb0 = __ldg(&b[o0 + s0 * z]);
+          if (v1 && z < n2) bb1 = __ldg(&b[o1 + s1 * z]);
+          if (v2) bb2 = __ldg(&b[o2 + s2 * z]);
+          if (v2 && z < n2) bb3 = __ldg(&b[o3 + s2 * z]);
+        }
         auto filt = [&](const cplx* D) {
           const cplx a = D[t - 1 - S3_FX] + D[t + 1 - S3_FX] + 2.0 * D[t - S3_FX];
           const cplx c = D[t - 1 + S3_FX] + D[t + 1 + S3_FX] + 2.0 * D[t + S3_FX];
@@ -343,8 +343,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             out += (f02c - f02p) * ih;
             out -= mass(0, qc0, qm0, mc0 + czz);
             out += (pc - Pc[ui - 1]) * ih;
-            const int64_t r = o0 + s0 * z;
-            y[r] = b ? b[r] - out : out;
+            y[o0 + s0 * z] = b ? bb0 - out : out;
           }
           if (v1 && z < n2) {  // u1 row
             cplx out = (S.f[3][t] - S.f[3][t + 1]) * ih;
@@ -352,8 +351,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             out += (f12c - f12p) * ih;
             out -= mass(1, qc1, qm1, mc1 + czz);
             out += (pc - Pc[ui - S3_UX]) * ih;
-            const int64_t r = o1 + s1 * z;
-            y[r] = b ? b[r] - out : out;
+            y[o1 + s1 * z] = b ? bb1 - out : out;
           }
           if (v2) {  // u2 row (z <= n2)
             cplx out = (S.f[4][t] - S.f[4][t + 1]) * ih;
@@ -361,16 +359,14 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             out += (f22m - f22) * ih;
             out -= mass(2, qc2, qm2, mc2 + lz + hz1);
             out += (pc - S.p[pm][ui]) * ih;
-            const int64_t r = o2 + s2 * z;
-            y[r] = b ? b[r] - out : out;
+            y[o2 + s2 * z] = b ? bb2 - out : out;
           }
           if (v2 && z < n2) {  // p row (operator.hpp:416)
             cplx out = d00;
             out += d11;
             out += d22;
             out += S.ilm[z & 3][ui] * pc;
-            const int64_t r = o3 + s2 * z;
-            y[r] = b ? b[r] - out : out;
+            y[o3 + s2 * z] = b ? bb3 - out : out;
           }
         }
         f02c = f02p;
