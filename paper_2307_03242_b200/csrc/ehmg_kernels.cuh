@@ -272,53 +272,61 @@ EH_HD void renorm(Taps& t) {
   for (int i = 0; i < t.cnt; ++i) s += t.w[i];
   for (int i = 0; i < t.cnt; ++i) t.w[i] /= s;
 }
+// Tap rows written out per case (no dynamic indexing, registers only); the
+// renormalisation divides by the same partial sums as renorm_row.
 EH_HD Taps restrict_taps(int i, int n_fine, bool face) {
   Taps t;
-  t.cnt = 0;
   if (face) {
-    const double ws[3] = {0.25, 0.5, 0.25};
-    for (int q = 0; q < 3; ++q) {
-      int f = 2 * i + q - 1;
-      if (f >= 0 && f < n_fine) {
-        t.idx[t.cnt] = f;
-        t.w[t.cnt++] = ws[q];
-      }
+    const bool lo = 2 * i - 1 >= 0, hi = 2 * i + 1 < n_fine;
+    if (lo && hi) {
+      t.cnt = 3;
+      t.idx[0] = 2 * i - 1, t.idx[1] = 2 * i, t.idx[2] = 2 * i + 1;
+      t.w[0] = 0.25, t.w[1] = 0.5, t.w[2] = 0.25;
+    } else if (lo) {
+      t.cnt = 2;
+      t.idx[0] = 2 * i - 1, t.idx[1] = 2 * i, t.idx[2] = 0;
+      t.w[0] = 0.25 / 0.75, t.w[1] = 0.5 / 0.75, t.w[2] = 0;
+    } else if (hi) {
+      t.cnt = 2;
+      t.idx[0] = 2 * i, t.idx[1] = 2 * i + 1, t.idx[2] = 0;
+      t.w[0] = 0.5 / 0.75, t.w[1] = 0.25 / 0.75, t.w[2] = 0;
+    } else {
+      t.cnt = 1;
+      t.idx[0] = 2 * i, t.idx[1] = t.idx[2] = 0;
+      t.w[0] = 1.0, t.w[1] = t.w[2] = 0;
     }
-    renorm(t);
   } else {
     t.cnt = 2;
-    t.idx[0] = 2 * i;
-    t.w[0] = 0.5;
-    t.idx[1] = 2 * i + 1;
-    t.w[1] = 0.5;
+    t.idx[0] = 2 * i, t.idx[1] = 2 * i + 1, t.idx[2] = 0;
+    t.w[0] = 0.5, t.w[1] = 0.5, t.w[2] = 0;
   }
   return t;
 }
 EH_HD Taps prolong_taps(int f, int n_fine, bool face) {
   Taps t;
+  t.idx[2] = 0;
+  t.w[2] = 0;
   if (face) {
     if (f % 2 == 0) {
       t.cnt = 1;
-      t.idx[0] = f / 2;
-      t.w[0] = 1.0;
+      t.idx[0] = f / 2, t.idx[1] = 0;
+      t.w[0] = 1.0, t.w[1] = 0;
     } else {
       t.cnt = 2;
-      t.idx[0] = f / 2;
-      t.w[0] = 0.5;
-      t.idx[1] = f / 2 + 1;
-      t.w[1] = 0.5;
+      t.idx[0] = f / 2, t.idx[1] = f / 2 + 1;
+      t.w[0] = 0.5, t.w[1] = 0.5;
     }
   } else {
-    int nc = n_fine / 2, c = f / 2, far = (f % 2 == 0) ? c - 1 : c + 1;
-    t.cnt = 1;
-    t.idx[0] = c;
-    t.w[0] = 0.75;
+    const int nc = n_fine / 2, c = f / 2, far = (f % 2 == 0) ? c - 1 : c + 1;
     if (far >= 0 && far < nc) {
-      t.idx[1] = far;
-      t.w[1] = 0.25;
       t.cnt = 2;
+      t.idx[0] = c, t.idx[1] = far;
+      t.w[0] = 0.75, t.w[1] = 0.25;  // sum 1: renormalisation is the identity
+    } else {
+      t.cnt = 1;
+      t.idx[0] = c, t.idx[1] = 0;
+      t.w[0] = 0.75 / 0.75, t.w[1] = 0;
     }
-    renorm(t);
   }
   return t;
 }
@@ -363,6 +371,75 @@ __global__ void __launch_bounds__(kThreads) k_transfer(Geo gf, Geo gc, int restr
     }
     out[r] = accumulate ? out[r] + s2 : s2;
   }
+}
+
+// 3D transfers, one launch per component, 3D thread grid (no index
+// division). Same tap rules and contraction order as k_transfer.
+template <int C>
+__global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const cplx* __restrict__ xf,
+                                                   cplx* __restrict__ xc) {
+  const int o0 = blockIdx.x * 32 + threadIdx.x, o1 = blockIdx.y * 8 + threadIdx.y, o2 = blockIdx.z;
+  const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1);
+  if (o0 >= D0 || o1 >= D1) return;
+  const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
+  const Taps t0 = restrict_taps(o0, F0, C == 0);
+  const Taps t1 = restrict_taps(o1, F1, C == 1);
+  const Taps t2 = restrict_taps(o2, gf.n[2] + (C == 2), C == 2);
+  const cplx* base = xf + gf.off[C];
+  cplx s2 = mk(0, 0);
+#pragma unroll
+  for (int q2 = 0; q2 < 3; ++q2) {
+    if (q2 >= t2.cnt) break;
+    cplx s1 = mk(0, 0);
+#pragma unroll
+    for (int q1 = 0; q1 < 3; ++q1) {
+      if (q1 >= t1.cnt) break;
+      const cplx* row = base + (int64_t)F0 * (t1.idx[q1] + (int64_t)F1 * t2.idx[q2]);
+      cplx s0 = mk(0, 0);
+#pragma unroll
+      for (int q0 = 0; q0 < 3; ++q0) {
+        if (q0 >= t0.cnt) break;
+        s0 += t0.w[q0] * row[t0.idx[q0]];
+      }
+      s1 += t1.w[q1] * s0;
+    }
+    s2 += t2.w[q2] * s1;
+  }
+  xc[gc.off[C] + o0 + (int64_t)D0 * (o1 + (int64_t)D1 * o2)] = s2;
+}
+
+template <int C>
+__global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const cplx* __restrict__ xc,
+                                                  cplx* __restrict__ xf, int accumulate) {
+  const int f0 = blockIdx.x * 32 + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y, f2 = blockIdx.z;
+  const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
+  if (f0 >= F0 || f1 >= F1) return;
+  const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1);
+  const Taps t0 = prolong_taps(f0, F0, C == 0);
+  const Taps t1 = prolong_taps(f1, F1, C == 1);
+  const Taps t2 = prolong_taps(f2, gf.n[2] + (C == 2), C == 2);
+  const cplx* base = xc + gc.off[C];
+  cplx s2 = mk(0, 0);
+#pragma unroll
+  for (int q2 = 0; q2 < 2; ++q2) {
+    if (q2 >= t2.cnt) break;
+    cplx s1 = mk(0, 0);
+#pragma unroll
+    for (int q1 = 0; q1 < 2; ++q1) {
+      if (q1 >= t1.cnt) break;
+      const cplx* row = base + (int64_t)D0 * (t1.idx[q1] + (int64_t)D1 * t2.idx[q2]);
+      cplx s0 = mk(0, 0);
+#pragma unroll
+      for (int q0 = 0; q0 < 2; ++q0) {
+        if (q0 >= t0.cnt) break;
+        s0 += t0.w[q0] * row[t0.idx[q0]];
+      }
+      s1 += t1.w[q1] * s0;
+    }
+    s2 += t2.w[q2] * s1;
+  }
+  cplx* o = xf + gf.off[C] + f0 + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
+  *o = accumulate ? *o + s2 : s2;
 }
 
 // ------------------------------------------------------------------ media

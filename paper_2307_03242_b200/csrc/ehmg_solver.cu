@@ -211,12 +211,27 @@ static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, cons
                             cplx* out, bool accumulate, cudaStream_t s) {
   const Geo& gto = restricting ? gc : gf;
   Prof pf(restricting ? "restrict" : "prolong_add", s);
-  if (gf.nd == 3)
-    k_transfer<3><<<grid_for(gto.ndofs, 148 * 64), kThreads, 0, s>>>(gf, gc, restricting, in, out,
-                                                                     accumulate);
-  else
+  if (gf.nd == 3) {
+    const dim3 blk(32, 8);
+    for (int c = 0; c < 4; ++c) {
+      const int d0 = gto.n[0] + (c == 0), d1 = gto.n[1] + (c == 1), d2 = gto.n[2] + (c == 2);
+      const dim3 grd((d0 + 31) / 32, (d1 + 7) / 8, c < 3 ? d2 : gto.n[2]);
+      if (restricting) {
+        if (c == 0) k_restrict3<0><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        else if (c == 1) k_restrict3<1><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        else if (c == 2) k_restrict3<2><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        else k_restrict3<3><<<grd, blk, 0, s>>>(gf, gc, in, out);
+      } else {
+        if (c == 0) k_prolong3<0><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        else if (c == 1) k_prolong3<1><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        else if (c == 2) k_prolong3<2><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        else k_prolong3<3><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+      }
+    }
+  } else {
     k_transfer<2><<<grid_for(gto.ndofs, 148 * 64), kThreads, 0, s>>>(gf, gc, restricting, in, out,
                                                                      accumulate);
+  }
   CK(cudaGetLastError());
 }
 

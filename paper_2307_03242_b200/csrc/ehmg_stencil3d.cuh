@@ -29,6 +29,8 @@
 
 #include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 
+#include <vector>
+
 #include "ehmg_core.cuh"
 
 namespace ehmg {
@@ -414,8 +416,14 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P) {
   }
   s.ntiles_x = (g.n[0] + 1 + S3_TX - 1) / S3_TX;
   s.ntiles_y = (g.n[1] + 1 + S3_TY - 1) / S3_TY;
-  s.nchunks = (g.n[2] + S3_ZCHUNK / 2) / S3_ZCHUNK;
-  if (s.nchunks < 1) s.nchunks = 1;
+  // z-chunks: ~32 planes on big levels; on small levels split further (down to
+  // 4 planes per chunk) until there are >= 2 items per SM to keep the chip busy.
+  const int tiles = s.ntiles_x * s.ntiles_y;
+  int nch = (g.n[2] + S3_ZCHUNK / 2) / S3_ZCHUNK;
+  const int want = (2 * 148 + tiles - 1) / tiles;
+  const int cap = g.n[2] / 4 > 0 ? g.n[2] / 4 : 1;
+  if (nch < want) nch = want < cap ? want : cap;
+  s.nchunks = nch < 1 ? 1 : nch;
   return s;
 }
 
@@ -466,16 +474,46 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  S3Maps M;
+  // tensor maps depend only on (buffer, media, dims): cache them so the
+  // per-launch host cost is a lookup (buffers are fixed per level).
+  struct Entry {
+    const void* x;
+    const void* m;
+    int n[3];
+    S3Maps M;
+  };
+  static std::vector<Entry> cache;
+  static size_t next = 0;
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
-  for (int k = 0; k < 3; ++k)
-    s3_encode(&M.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * S3_UX);
-  s3_encode(&M.p, x + g.off[3], 2 * n0, n1, n2, 2 * S3_UX);
-  const int64_t nc = g.ncells;
-  s3_encode(&M.mu, media_soa + 0 * nc, n0, n1, n2, S3_UX);
-  s3_encode(&M.rho, media_soa + 1 * nc, n0, n1, n2, S3_UX);
-  s3_encode(&M.gam, media_soa + 2 * nc, n0, n1, n2, S3_UX);
-  s3_encode(&M.ilm, media_soa + 3 * nc, n0, n1, n2, S3_UX);
+  const S3Maps* Mp = nullptr;
+  for (const Entry& e : cache)
+    if (e.x == x && e.m == media_soa && e.n[0] == n0 && e.n[1] == n1 && e.n[2] == n2) {
+      Mp = &e.M;
+      break;
+    }
+  if (!Mp) {
+    Entry e;
+    e.x = x;
+    e.m = media_soa;
+    e.n[0] = n0, e.n[1] = n1, e.n[2] = n2;
+    for (int k = 0; k < 3; ++k)
+      s3_encode(&e.M.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * S3_UX);
+    s3_encode(&e.M.p, x + g.off[3], 2 * n0, n1, n2, 2 * S3_UX);
+    const int64_t nc = g.ncells;
+    s3_encode(&e.M.mu, media_soa + 0 * nc, n0, n1, n2, S3_UX);
+    s3_encode(&e.M.rho, media_soa + 1 * nc, n0, n1, n2, S3_UX);
+    s3_encode(&e.M.gam, media_soa + 2 * nc, n0, n1, n2, S3_UX);
+    s3_encode(&e.M.ilm, media_soa + 3 * nc, n0, n1, n2, S3_UX);
+    if (cache.size() < 256) {
+      cache.push_back(e);
+      Mp = &cache.back().M;
+    } else {
+      cache[next] = e;
+      Mp = &cache[next].M;
+      next = (next + 1) % cache.size();
+    }
+  }
+  const S3Maps M = *Mp;
   const S3Params sp = make_s3params(g, P);
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
