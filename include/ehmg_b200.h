@@ -108,6 +108,27 @@ uint64_t ehmg_multigrid_stream(ehmg_mg mg);
 int ehmg_multigrid_time_precondition(ehmg_mg mg, const double* r_dev, double* z_dev, int count,
                                      double* ms);
 
+/* ---- z-slab decomposed multigrid (north_star subsystem (6); no reference
+ *      counterpart -- the reference is single-node CPU). Fine levels are split
+ *      into z-slabs with 2 ghost planes exchanged after every field update;
+ *      levels with z extent <= agg_n2 are agglomerated (replicated). In one
+ *      process all slabs live on the current device and exchange by device
+ *      copies; results equal ehmg_multigrid_precondition (same options).
+ * plan: la = number of distributed levels, z0[0..nslabs] = level-0 slab
+ *       boundaries (pure host function, no device needed). */
+typedef struct ehmg_slab_mg_s* ehmg_slab_mg;
+int ehmg_slab_plan(int n2, int n_levels, int nslabs, int agg_n2, int* la, int* z0);
+int ehmg_slab_multigrid_create(int ndim, const int* dims, double h, const double* lambda,
+                               const double* mu, const double* rho, const double* gamma,
+                               double beta, double omega, double alpha,
+                               const ehmg_mg_options* opt, int nslabs, int agg_n2,
+                               ehmg_slab_mg* out);
+int ehmg_slab_multigrid_destroy(ehmg_slab_mg mg);
+int ehmg_slab_multigrid_levels(ehmg_slab_mg mg, int* distributed, int* total);
+int ehmg_slab_multigrid_precondition(ehmg_slab_mg mg, const double* r, double* z, int where);
+/* bytes moved by ghost exchanges + agglomeration during the last precondition */
+int64_t ehmg_slab_multigrid_exchanged_bytes(ehmg_slab_mg mg);
+
 /* Per-launch CUDA-event profiling of the cycle kernels (bench roofline).
  * report: one "kernel level count total_ms" line per (kernel, level). */
 int ehmg_profile_enable(int on);

@@ -47,12 +47,16 @@ EH_HD cplx cdiv(cplx a, cplx b) {
 
 // --------------------------------------------------------------- geometry
 // One level of the staggered grid (grid.hpp:64). 2D grids carry n[2] = 1.
+// A z-slab window of a global grid stores cell planes [zoff, zoff + n[2])
+// (and u2 faces [zoff, zoff + n[2]]); n/off/ndofs describe the local
+// storage, gn2 the global plane count that decides boundary semantics.
 struct Geo {
   int nd;
   int n[3];
   double h, inv_h;
   int64_t off[4];
   int64_t ndofs, ncells;
+  int zoff, gn2;
 
   EH_HD int fdim(int k, int a) const { return n[a] + (a == k ? 1 : 0); }
   EH_HD bool face_ok(int k, const int* f) const {
@@ -105,7 +109,18 @@ inline Geo make_geo(int nd, const int* dims, double h) {
   for (int k = nd + 1; k < 4; ++k) g.off[k] = o;
   g.ncells = (int64_t)g.n[0] * g.n[1] * g.n[2];
   g.ndofs = o + g.ncells;
+  g.zoff = 0;
+  g.gn2 = g.n[2];
   return g;
+}
+
+// Local geometry of the cell-plane window [z0, z1) of a global 3D grid.
+inline Geo make_window(const Geo& G, int z0, int z1) {
+  int d[3] = {G.n[0], G.n[1], z1 - z0};
+  Geo w = make_geo(G.nd, d, G.h);
+  w.zoff = z0;
+  w.gn2 = G.gn2;
+  return w;
 }
 
 // Operator parameters (operator.hpp:27 OperatorParams). The attenuation

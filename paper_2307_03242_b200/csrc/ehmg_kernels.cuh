@@ -40,12 +40,15 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(Geo g, OpPar P, cons
 // Layout per cell (complex): for each component k
 //   full: Uinv00 Uinv01 Uinv10 Uinv11 g0 g1 h0 h1; economic: Uinv0 Uinv1 g0 g1 h0 h1
 // then 1/s.
+// Cells of the z-window [z0, z0 + nz) of the (global) grid g; the cache is
+// indexed by the window-local cell.
 template <int ND>
 __global__ void k_vanka_build(Geo g, OpPar P, const Cell* __restrict__ m, int full,
-                              cplx* __restrict__ cache, int* __restrict__ bad) {
+                              cplx* __restrict__ cache, int* __restrict__ bad, int z0, int nz) {
   const int stride = ND * ((full ? 4 : 2) + 4) + 1;
-  GRID_STRIDE(ci, g.ncells) {
-    int c[3] = {(int)(ci % g.n[0]), (int)((ci / g.n[0]) % g.n[1]), (int)(ci / ((int64_t)g.n[0] * g.n[1]))};
+  const int64_t nloc = (int64_t)g.n[0] * g.n[1] * nz;
+  GRID_STRIDE(ci, nloc) {
+    int c[3] = {(int)(ci % g.n[0]), (int)((ci / g.n[0]) % g.n[1]), (int)(ci / ((int64_t)g.n[0] * g.n[1])) + z0};
     cplx* q = cache + ci * stride;
     cplx sum_cg = mk(0, 0);
     for (int k = 0; k < ND; ++k) {
@@ -375,33 +378,40 @@ __global__ void __launch_bounds__(kThreads) k_transfer(Geo gf, Geo gc, int restr
 
 // 3D transfers, one launch per component, 3D thread grid (no index
 // division). Same tap rules and contraction order as k_transfer.
+// 3D transfers, one launch per component, 3D thread grid (no index
+// division). Same tap rules and contraction order as k_transfer. Both grids
+// may be z-slab windows: taps along z follow the global grid, reads outside
+// the fine/coarse window storage contribute zero (garbage ghost region).
 template <int C>
 __global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const cplx* __restrict__ xf,
                                                    cplx* __restrict__ xc) {
   const int o0 = blockIdx.x * 32 + threadIdx.x, o1 = blockIdx.y * 8 + threadIdx.y, o2 = blockIdx.z;
   const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1);
   if (o0 >= D0 || o1 >= D1) return;
-  const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
+  const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1), F2 = gf.n[2] + (C == 2);
   const Taps t0 = restrict_taps(o0, F0, C == 0);
   const Taps t1 = restrict_taps(o1, F1, C == 1);
-  const Taps t2 = restrict_taps(o2, gf.n[2] + (C == 2), C == 2);
+  const Taps t2 = restrict_taps(o2 + gc.zoff, gf.gn2 + (C == 2), C == 2);
   const cplx* base = xf + gf.off[C];
   cplx s2 = mk(0, 0);
 #pragma unroll
   for (int q2 = 0; q2 < 3; ++q2) {
     if (q2 >= t2.cnt) break;
+    const int z = t2.idx[q2] - gf.zoff;
     cplx s1 = mk(0, 0);
+    if (z >= 0 && z < F2) {
 #pragma unroll
-    for (int q1 = 0; q1 < 3; ++q1) {
-      if (q1 >= t1.cnt) break;
-      const cplx* row = base + (int64_t)F0 * (t1.idx[q1] + (int64_t)F1 * t2.idx[q2]);
-      cplx s0 = mk(0, 0);
+      for (int q1 = 0; q1 < 3; ++q1) {
+        if (q1 >= t1.cnt) break;
+        const cplx* row = base + (int64_t)F0 * (t1.idx[q1] + (int64_t)F1 * z);
+        cplx s0 = mk(0, 0);
 #pragma unroll
-      for (int q0 = 0; q0 < 3; ++q0) {
-        if (q0 >= t0.cnt) break;
-        s0 += t0.w[q0] * row[t0.idx[q0]];
+        for (int q0 = 0; q0 < 3; ++q0) {
+          if (q0 >= t0.cnt) break;
+          s0 += t0.w[q0] * row[t0.idx[q0]];
+        }
+        s1 += t1.w[q1] * s0;
       }
-      s1 += t1.w[q1] * s0;
     }
     s2 += t2.w[q2] * s1;
   }
@@ -414,27 +424,30 @@ __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const cplx* __
   const int f0 = blockIdx.x * 32 + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y, f2 = blockIdx.z;
   const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
   if (f0 >= F0 || f1 >= F1) return;
-  const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1);
+  const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1), D2 = gc.n[2] + (C == 2);
   const Taps t0 = prolong_taps(f0, F0, C == 0);
   const Taps t1 = prolong_taps(f1, F1, C == 1);
-  const Taps t2 = prolong_taps(f2, gf.n[2] + (C == 2), C == 2);
+  const Taps t2 = prolong_taps(f2 + gf.zoff, gf.gn2 + (C == 2), C == 2);
   const cplx* base = xc + gc.off[C];
   cplx s2 = mk(0, 0);
 #pragma unroll
   for (int q2 = 0; q2 < 2; ++q2) {
     if (q2 >= t2.cnt) break;
+    const int z = t2.idx[q2] - gc.zoff;
     cplx s1 = mk(0, 0);
+    if (z >= 0 && z < D2) {
 #pragma unroll
-    for (int q1 = 0; q1 < 2; ++q1) {
-      if (q1 >= t1.cnt) break;
-      const cplx* row = base + (int64_t)D0 * (t1.idx[q1] + (int64_t)D1 * t2.idx[q2]);
-      cplx s0 = mk(0, 0);
+      for (int q1 = 0; q1 < 2; ++q1) {
+        if (q1 >= t1.cnt) break;
+        const cplx* row = base + (int64_t)D0 * (t1.idx[q1] + (int64_t)D1 * z);
+        cplx s0 = mk(0, 0);
 #pragma unroll
-      for (int q0 = 0; q0 < 2; ++q0) {
-        if (q0 >= t0.cnt) break;
-        s0 += t0.w[q0] * row[t0.idx[q0]];
+        for (int q0 = 0; q0 < 2; ++q0) {
+          if (q0 >= t0.cnt) break;
+          s0 += t0.w[q0] * row[t0.idx[q0]];
+        }
+        s1 += t1.w[q1] * s0;
       }
-      s1 += t1.w[q1] * s0;
     }
     s2 += t2.w[q2] * s1;
   }

@@ -189,6 +189,23 @@ struct DevMedia {
   void drop_raw() {
     for (auto& r : raw) r.release();
   }
+  // raw arrays copied from another (global) media set, then packed
+  void copy_from(const DevMedia& o, int64_t n, cudaStream_t s) {
+    for (int q = 0; q < 4; ++q) {
+      raw[q].alloc(n);
+      CK(cudaMemcpyAsync(raw[q].p, o.raw[q].p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    }
+    pack(n, s);
+  }
+  // the cell-plane window [z0, z1) of a global media set (packed + SoA)
+  void window_of(const DevMedia& o, const Geo& gg, int z0, int z1, cudaStream_t s) {
+    const int64_t plane = (int64_t)gg.n[0] * gg.n[1], n = plane * (z1 - z0);
+    packed.alloc(n);
+    CK(cudaMemcpyAsync(packed.p, o.packed.p + plane * z0, sizeof(Cell) * n, cudaMemcpyDeviceToDevice, s));
+    soa.alloc(4 * n);
+    k_media_soa<<<grid_for(n), kThreads, 0, s>>>(n, packed.p, soa.p);
+    CK(cudaGetLastError());
+  }
 };
 
 // ----------------------------------------------------------- level kernels
@@ -247,17 +264,22 @@ static Geo coarse_geo(const Geo& g) {
 struct Smoother {
   int full = 1, stride = 0;
   DBuf<cplx> soa, res;
-  void build(const Geo& g, const OpPar& P, const Cell* m, int full_, cudaStream_t s) {
+  // Cache for the cells of `gg` (global grid, global packed media m), or of
+  // its z-window [z0, z1) when z1 >= 0; sweeps then run on the window geometry.
+  void build(const Geo& gg, const OpPar& P, const Cell* m, int full_, cudaStream_t s, int z0 = 0,
+             int z1 = -1) {
     full = full_;
-    stride = g.nd * ((full ? 4 : 2) + 4) + 1;
+    stride = gg.nd * ((full ? 4 : 2) + 4) + 1;
+    const Geo g = z1 < 0 ? gg : make_window(gg, z0, z1);
+    const int nz = z1 < 0 ? gg.n[2] : z1 - z0;
     {
       DBuf<cplx> aos(g.ncells * stride);
       DBuf<int> bad(1);
       bad.zero(s);
       if (g.nd == 3)
-        k_vanka_build<3><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, aos.p, bad.p);
+        k_vanka_build<3><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(gg, P, m, full, aos.p, bad.p, z0, nz);
       else
-        k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(g, P, m, full, aos.p, bad.p);
+        k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(gg, P, m, full, aos.p, bad.p, 0, 1);
       CK(cudaGetLastError());
       int hb = 0;
       CK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -288,16 +310,20 @@ struct Smoother {
       CK(cudaGetLastError());
       return;
     }
+    for (int color = 0; color < 2; ++color) colour_phase(g, P, mr, b, x, w, color, s);
+  }
+  // One red-black colour (global parity `color`; windows shift the local parity).
+  void colour_phase(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
+                    int color, cudaStream_t s) {
     const int64_t nt = colour_threads(g);
-    for (int color = 0; color < 2; ++color) {
-      launch_residual(g, P, mr, x, b, res.p, s);
-      Prof pf("vanka_update", s);
-      if (g.nd == 3)
-        k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, color, w, x);
-      else
-        k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, color, w, x);
-      CK(cudaGetLastError());
-    }
+    const int lc = color ^ (g.zoff & 1);
+    launch_residual(g, P, mr, x, b, res.p, s);
+    Prof pf("vanka_update", s);
+    if (g.nd == 3)
+      k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, lc, w, x);
+    else
+      k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, lc, w, x);
+    CK(cudaGetLastError());
   }
 };
 
@@ -681,6 +707,47 @@ static void build_coarse_inverse(const Geo& g, const OpPar& P, const Cell* m, DB
   cusolverDnDestroy(h);
 }
 
+// Build a hierarchy of `nlevels` levels below grid g from host media (host)
+// or from a device media set with raw arrays (src).
+static std::unique_ptr<ehmg_mg_s> build_mg(const Geo& g, const double* const* host, const DevMedia* src,
+                                           const OpPar& P, const ehmg_mg_options& opt, int nlevels) {
+  auto mg = std::make_unique<ehmg_mg_s>();
+  mg->opt = opt;
+  mg->opt.n_levels = nlevels;
+  CK(cudaGetDevice(&mg->dev));
+  CK(cudaStreamCreateWithFlags(&mg->s, cudaStreamNonBlocking));
+  cudaStream_t s = mg->s;
+  for (int l = 0; l < nlevels; ++l) {
+    auto lev = std::make_unique<Level>();
+    lev->g = l == 0 ? g : coarse_geo(mg->L[l - 1]->g);
+    lev->P = P;
+    if (l == 0) {
+      if (host) lev->media.upload(g.ncells, host, s);
+      else lev->media.copy_from(*src, g.ncells, s);
+    } else {
+      mg->L[l - 1]->media.coarsen_into(mg->L[l - 1]->g, lev->media, lev->g, s);
+    }
+    const bool coarsest = (l + 1 == nlevels);
+    if (!coarsest) {
+      lev->sm.build(lev->g, P, lev->media.packed.p, opt.vanka_mode == 0 ? 1 : 0, s);
+      lev->r.alloc(lev->g.ndofs);
+    }
+    if (l > 0) {
+      lev->bc.alloc(lev->g.ndofs);
+      lev->ec.alloc(lev->g.ndofs);
+    }
+    mg->L.push_back(std::move(lev));
+  }
+  for (auto& lev : mg->L) lev->media.drop_raw();
+  Level& cl = *mg->L.back();
+  mg->nco = cl.g.ndofs;
+  build_coarse_inverse(cl.g, P, cl.media.packed.p, mg->ainv, s);
+  CK(cudaStreamSynchronize(s));
+  return mg;
+}
+
+#include "ehmg_slab.cuh"
+
 // ------------------------------------------------------------------ C ABI
 extern "C" {
 
@@ -878,11 +945,6 @@ int ehmg_multigrid_create(int nd, const int* dims, double h, const double* lambd
     validate_grid(nd, dims, h);
     check_device();
     int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
-    auto mg = std::make_unique<ehmg_mg_s>();
-    mg->opt = *opt;
-    CK(cudaGetDevice(&mg->dev));
-    CK(cudaStreamCreateWithFlags(&mg->s, cudaStreamNonBlocking));
-    cudaStream_t s = mg->s;
     Geo g = make_geo(nd, d, h);
     validate_media(g.ncells, lambda, mu, rho, gamma);
     // every level but the last must coarsen (transfer.hpp:25 can_coarsen)
@@ -896,35 +958,72 @@ int ehmg_multigrid_create(int nd, const int* dims, double h, const double* lambd
       }
     }
     const OpPar P{beta, omega * omega, alpha};
-    for (int l = 0; l < opt->n_levels; ++l) {
-      auto lev = std::make_unique<Level>();
-      lev->g = l == 0 ? g : coarse_geo(mg->L[l - 1]->g);
-      lev->P = P;
-      if (l == 0) {
-        const double* f[4] = {lambda, mu, rho, gamma};
-        lev->media.upload(g.ncells, f, s);
-      } else {
-        mg->L[l - 1]->media.coarsen_into(mg->L[l - 1]->g, lev->media, lev->g, s);
-      }
-      const bool coarsest = (l + 1 == opt->n_levels);
-      if (!coarsest) {
-        lev->sm.build(lev->g, P, lev->media.packed.p, opt->vanka_mode == 0 ? 1 : 0, s);
-        lev->r.alloc(lev->g.ndofs);
-      }
-      if (l > 0) {
-        lev->bc.alloc(lev->g.ndofs);
-        lev->ec.alloc(lev->g.ndofs);
-      }
-      mg->L.push_back(std::move(lev));
-    }
-    for (auto& lev : mg->L) lev->media.drop_raw();
-    Level& cl = *mg->L.back();
-    mg->nco = cl.g.ndofs;
-    build_coarse_inverse(cl.g, P, cl.media.packed.p, mg->ainv, s);
-    CK(cudaStreamSynchronize(s));
-    *out = mg.release();
+    const double* f[4] = {lambda, mu, rho, gamma};
+    *out = build_mg(g, f, nullptr, P, *opt, opt->n_levels).release();
   });
 }
+
+// ---- z-slab decomposition (ehmg_slab.cuh) -------------------------------
+int ehmg_slab_plan(int n2, int n_levels, int nslabs, int agg_n2, int* la, int* z0) {
+  return guard([&] {
+    SlabPlan p = make_slab_plan(n2, n_levels, nslabs, agg_n2);
+    *la = p.La;
+    for (int q = 0; q <= nslabs; ++q) z0[q] = p.z0[q];
+  });
+}
+
+int ehmg_slab_multigrid_create(int nd, const int* dims, double h, const double* lambda,
+                               const double* mu, const double* rho, const double* gamma,
+                               double beta, double omega, double alpha,
+                               const ehmg_mg_options* opt, int nslabs, int agg_n2,
+                               ehmg_slab_mg* out) {
+  return guard([&] {
+    if (opt->n_levels < 2) throw Err(EHMG_EINVAL, "multigrid: need at least 2 levels");
+    validate_grid(nd, dims, h);
+    check_device();
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    Geo g = make_geo(nd, d, h);
+    validate_media(g.ncells, lambda, mu, rho, gamma);
+    {
+      Geo t = g;
+      for (int l = 0; l + 1 < opt->n_levels; ++l) {
+        for (int a = 0; a < nd; ++a)
+          if (t.n[a] % 2 != 0 || t.n[a] / 2 < 2)
+            throw Err(EHMG_EINVAL, "multigrid: grid cannot support requested levels");
+        t = coarse_geo(t);
+      }
+    }
+    const OpPar P{beta, omega * omega, alpha};
+    const double* f[4] = {lambda, mu, rho, gamma};
+    *out = build_slab_mg(g, f, P, *opt, nslabs, agg_n2).release();
+  });
+}
+
+int ehmg_slab_multigrid_destroy(ehmg_slab_mg mg) {
+  return guard([&] { delete mg; });
+}
+
+int ehmg_slab_multigrid_levels(ehmg_slab_mg mg, int* distributed, int* total) {
+  return guard([&] {
+    *distributed = mg->plan.La;
+    *total = mg->plan.nl;
+  });
+}
+
+int ehmg_slab_multigrid_precondition(ehmg_slab_mg mg, const double* r, double* z, int where) {
+  return guard([&] {
+    const int64_t n = mg->G[0].ndofs;
+    DBuf<cplx> sr, sz;
+    const cplx* dr;
+    to_dev(r, sr, n, where, mg->s, &dr);
+    cplx* dz = out_dev(z, sz, n, where);
+    mg->exchanged_bytes = 0;
+    mg->precondition(dr, dz);
+    from_dev(z, dz, n, where, mg->s);
+  });
+}
+
+int64_t ehmg_slab_multigrid_exchanged_bytes(ehmg_slab_mg mg) { return mg ? mg->exchanged_bytes : -1; }
 
 int ehmg_multigrid_destroy(ehmg_mg mg) {
   return guard([&] { delete mg; });

@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
   const int ui = (fx + 1) + S3_UX * (fy + 1);  // own U-local index
   const bool interior = act && fx >= 1 && fx <= S3_TX && fy >= 1 && fy <= S3_TY;
   const double beta = P.beta, w = P.w, ih = g.inv_h, wn = P.wn;
-  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];  // local storage extents
+  const int zoff = g.zoff, n2g = g.gn2;               // global z semantics (slab windows)
 
   if (t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[0])));
@@ -208,9 +209,10 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
       const double* MUm = S.mu[(z - 1) & 3];
       const double* MUc = S.mu[z & 3];
       const double* MUp = S.mu[(z + 1) & 3];
-      // uniform z quantities
-      const int lz = z >= 1, hz0 = z + 1 < n2, hz1 = z + 1 < n2 + 1;
-      const double izc = s3_inv(lz + (z < n2)), izp = s3_inv((z + 1 >= 1) + (z + 1 < n2));
+      // uniform z quantities (global plane index zg decides the boundary rules)
+      const int zg = z + zoff;
+      const int lz = zg >= 1, hz0 = zg + 1 < n2g, hz1 = zg + 1 < n2g + 1;
+      const double izc = s3_inv(lz + (zg < n2g)), izp = s3_inv((zg + 1 >= 1) + (zg + 1 < n2g));
       const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
       cplx d00 = mk(0, 0), d11 = mk(0, 0);
 
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
           const double rho_f = sr * ic, gam_f = sg * ic + al;
           return mk(w2 * rho_f, -w2 * gam_f * rho_f);
         };
-        const bool zin = z + 1 >= 0 && z + 1 < n2;
+        const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
         const int qb = (z + 1) & 1;
         // ---- component 0: F00 (cell, +x pair, in-plane y), F01 (edge01, -y pair, in-plane x)
         {
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
           r21m = r21c;
           r21c = rn1;
           S.di[0][t] = v00 - u00;  // d22 at cell (q, z)
-          S.q[qb][2][t] = (z + 1 >= 0 && z + 1 <= n2 && q2ok)
+          S.q[qb][2][t] = (zg + 1 >= 0 && zg + 1 <= n2g && q2ok)
                               ? md(RHc[ui] + rp00, GAc[ui] + gp00, izp) * v00
                               : mk(0, 0);
         }

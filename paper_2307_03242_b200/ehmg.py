@@ -103,6 +103,16 @@ def lib():
         L.ehmg_field_norm.argtypes = [i64, vp, dp]
         L.ehmg_field_axpy.argtypes = [i64, C.c_double, C.c_double, vp, vp]
         L.ehmg_set_device.argtypes = [C.c_int]
+        L.ehmg_slab_plan.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, ip, ip]
+        L.ehmg_slab_multigrid_create.argtypes = [C.c_int, ip, C.c_double, vp, vp, vp, vp,
+                                                 C.c_double, C.c_double, C.c_double,
+                                                 C.POINTER(_MgOpts), C.c_int, C.c_int,
+                                                 C.POINTER(vp)]
+        L.ehmg_slab_multigrid_destroy.argtypes = [vp]
+        L.ehmg_slab_multigrid_levels.argtypes = [vp, ip, ip]
+        L.ehmg_slab_multigrid_precondition.argtypes = [vp, vp, vp, C.c_int]
+        L.ehmg_slab_multigrid_exchanged_bytes.argtypes = [vp]
+        L.ehmg_slab_multigrid_exchanged_bytes.restype = i64
         L.ehmg_profile_enable.argtypes = [C.c_int]
         L.ehmg_profile_report.argtypes = [C.c_char_p, C.c_int]
         _lib = L
@@ -565,6 +575,78 @@ class Multigrid:
         pz, _ = _ptr(z_dev, self.n, writable=True)
         _check(lib().ehmg_multigrid_time_precondition(self._h, pr, pz, count, C.byref(ms)))
         return ms.value
+
+
+# ------------------------------------------------------- z-slab decomposition
+SLAB_GHOST = 2
+
+
+def slab_plan(n2: int, n_levels: int, nslabs: int, agg_n2: int = 64):
+    """Slab partition of the z axis (pure host): (distributed levels, level-0
+    boundaries). Boundaries are multiples of 2**La; every distributed level
+    keeps >= 4 owned planes per slab."""
+    la = C.c_int(0)
+    z0 = (C.c_int * (nslabs + 1))()
+    _check(lib().ehmg_slab_plan(n2, n_levels, nslabs, agg_n2, C.byref(la), z0))
+    return la.value, [z0[i] for i in range(nslabs + 1)]
+
+
+def slab_windows(n2: int, n_levels: int, nslabs: int, agg_n2: int = 64, level: int = 0):
+    """[(Z0, Z1, W0, W1)] per slab at `level`: owned cell planes and stored
+    window (owned +- SLAB_GHOST planes, clipped)."""
+    la, z0 = slab_plan(n2, n_levels, nslabs, agg_n2)
+    if level >= la:
+        raise ValueError("level is agglomerated (replicated), not distributed")
+    nl = n2 >> level
+    out = []
+    for q in range(nslabs):
+        a, b = z0[q] >> level, z0[q + 1] >> level
+        out.append((a, b, max(0, a - SLAB_GHOST), min(nl, b + SLAB_GHOST)))
+    return out
+
+
+class SlabMultigrid:
+    """The shifted-Laplacian hierarchy decomposed into z-slabs (north_star
+    (6)): fine levels sharded with ghost-plane exchange, levels with z extent
+    <= agg_n2 agglomerated. Same options and results as Multigrid."""
+
+    def __init__(self, grid: StaggeredGrid, media: MediaModel, par: OperatorParams,
+                 opt: MgOptions, nslabs: int, agg_n2: int = 64):
+        o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
+                    0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
+                    opt.k_inner_iterations, opt.k_inner_rtol)
+        arrs = media.arrays(grid)
+        h = C.c_void_p()
+        _check(lib().ehmg_slab_multigrid_create(grid.ndim, _dims_arr(grid.dims), grid.h,
+                                                *[a.ctypes.data for a in arrs], par.beta,
+                                                par.omega, par.alpha, C.byref(o), nslabs, agg_n2,
+                                                C.byref(h)))
+        self._h = h
+        self.n = grid.n_dofs()
+        self.nslabs = nslabs
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "_h", None):
+            _lib.ehmg_slab_multigrid_destroy(self._h)
+            self._h = None
+
+    def levels(self):
+        d, t = C.c_int(0), C.c_int(0)
+        _check(lib().ehmg_slab_multigrid_levels(self._h, C.byref(d), C.byref(t)))
+        return d.value, t.value
+
+    def exchanged_bytes(self) -> int:
+        return int(lib().ehmg_slab_multigrid_exchanged_bytes(self._h))
+
+    def precondition(self, r, z=None):
+        if z is None:
+            z = np.zeros(self.n, np.complex128) if not _is_device(r) else r.new_empty(self.n)
+        pr, wr = _ptr(r, self.n)
+        pz, wz = _ptr(z, self.n, writable=True)
+        if wr != wz:
+            raise ValueError("r and z must both be host arrays or both device tensors")
+        _check(lib().ehmg_slab_multigrid_precondition(self._h, pr, pz, wr))
+        return z
 
 
 # ----------------------------------------------------------------- Krylov
