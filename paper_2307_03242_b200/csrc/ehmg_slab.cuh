@@ -2,14 +2,16 @@
 //
 // Fine levels are split into z-slabs: slab s owns cell planes [Z0, Z1) (and
 // u2 faces [Z0, Z1), plus face n2 on the last slab) and stores the window
-// [Z0-G, Z1+G) (G = 2 ghost planes, clipped to the grid). Kernels run on the
+// [Z0-3, Z1+2) (ghost planes, clipped to the grid; one extra plane below
+// because the u2 mass row of the first ghost face averages rho/gamma one
+// cell further down). Kernels run on the
 // window with global boundary semantics (Geo::zoff/gn2); values near the
 // window edge are scratch. Every operation that changes a field is followed
 // by a ghost exchange (owned planes -> neighbour ghosts), which keeps the
 // owned region bit-identical to the undecomposed cycle:
 //   * a red-black colour updates all window cells; owned DOFs only depend on
-//     residuals of owned cells and of the first ghost cell layer, which only
-//     depend on x within G = 2 planes of the owned range;
+//     residuals of owned cells and of the first ghost cell layer below, which
+//     only depend on data inside the window;
 //   * restriction reads the fine residual one plane beyond the owned range;
 //   * prolongation reads coarse ghosts refreshed by the coarse level's last
 //     exchange.
@@ -28,7 +30,7 @@ struct SlabPlan {
   std::vector<int> z0;             // level-0 slab boundaries, size nslabs+1
 };
 
-constexpr int kSlabGhost = 2;
+constexpr int kSlabGhostLo = 3, kSlabGhostHi = 2;
 
 // Partition n2 planes into nslabs slabs whose boundaries are multiples of
 // 2^La, with at least 4 owned planes on every distributed level; levels with
@@ -230,7 +232,7 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
       auto sl = std::make_unique<SlabLevel>();
       sl->Z0 = sm->plan.z0[q] >> l;
       sl->Z1 = sm->plan.z0[q + 1] >> l;
-      const int w0 = std::max(0, sl->Z0 - kSlabGhost), w1 = std::min(sm->G[l].n[2], sl->Z1 + kSlabGhost);
+      const int w0 = std::max(0, sl->Z0 - kSlabGhostLo), w1 = std::min(sm->G[l].n[2], sl->Z1 + kSlabGhostHi);
       sl->g = make_window(sm->G[l], w0, w1);
       sl->media.window_of(*gm[l], sm->G[l], w0, w1, s);
       sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1);

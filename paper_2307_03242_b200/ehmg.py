@@ -578,7 +578,7 @@ class Multigrid:
 
 
 # ------------------------------------------------------- z-slab decomposition
-SLAB_GHOST = 2
+SLAB_GHOST_LO, SLAB_GHOST_HI = 3, 2
 
 
 def slab_plan(n2: int, n_levels: int, nslabs: int, agg_n2: int = 64):
@@ -593,7 +593,7 @@ def slab_plan(n2: int, n_levels: int, nslabs: int, agg_n2: int = 64):
 
 def slab_windows(n2: int, n_levels: int, nslabs: int, agg_n2: int = 64, level: int = 0):
     """[(Z0, Z1, W0, W1)] per slab at `level`: owned cell planes and stored
-    window (owned +- SLAB_GHOST planes, clipped)."""
+    window [Z0 - 3, Z1 + 2) clipped to the grid."""
     la, z0 = slab_plan(n2, n_levels, nslabs, agg_n2)
     if level >= la:
         raise ValueError("level is agglomerated (replicated), not distributed")
@@ -601,7 +601,7 @@ def slab_windows(n2: int, n_levels: int, nslabs: int, agg_n2: int = 64, level: i
     out = []
     for q in range(nslabs):
         a, b = z0[q] >> level, z0[q + 1] >> level
-        out.append((a, b, max(0, a - SLAB_GHOST), min(nl, b + SLAB_GHOST)))
+        out.append((a, b, max(0, a - SLAB_GHOST_LO), min(nl, b + SLAB_GHOST_HI)))
     return out
 
 
