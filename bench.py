@@ -161,7 +161,7 @@ def alg_bytes(kernel, n, level):
     if kernel == "apply":
         return 16 * 2 * N + 32 * C
     if kernel == "vanka_update":   # colour-half of the factor cache, r and x at the owned DOFs
-        return 16 * 25 * (C // 2) + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
+        return 16 * 13 * (C // 2) + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
     if kernel == "restrict":
         return 16 * N + 16 * ndofs(level_dims(n, level + 1))
     if kernel == "prolong_add":

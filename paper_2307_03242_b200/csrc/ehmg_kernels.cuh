@@ -167,24 +167,128 @@ EH_HD int64_t colour_index(const Geo& g, const int* c) {
   return g.clin(c);
 }
 
-// Factor cache re-laid out per colour, component-major (SoA): entry e of the
-// cell with colour index t of colour col lives at soa[(col*stride + e)*nt + t],
+// Compact factor cache. Of the reference's per-cell entries (vanka.hpp:72:
+// Uinv, g = Uinv b, h = c Uinv per component, 1/s) only Uinv and 1/s are
+// stored: b = (1/h, -1/h) exactly and c = (c0, -c0) with c0 the centre
+// weight of the spread divergence (operator.hpp:267) at the cell, so g and h
+// are rebuilt in registers with the reference's operations. This cuts the
+// cache from 25 to 13 complex per 3D cell (full Vanka), 19 to 7 (economic).
+struct VkPar {
+  double beta, w, ih;
+  double inv_wsum[16];  // by transverse validity bits of dspread_cell
+};
+
+inline VkPar make_vkpar(const Geo& g, const OpPar& P) {
+  VkPar v;
+  v.beta = P.beta;
+  v.ih = g.inv_h;
+  const bool d3 = g.nd == 3;
+  v.w = (1.0 - P.beta) / (d3 ? 16.0 : 4.0);
+  for (int f = 0; f < 16; ++f) {
+    double wsum = P.beta;
+    if (P.beta != 1.0) {
+      if (d3) {
+        for (int s1 = -1; s1 <= 1; ++s1)
+          for (int s2 = -1; s2 <= 1; ++s2) {
+            if ((s1 == -1 && !(f & 1)) || (s1 == 1 && !(f & 2)) || (s2 == -1 && !(f & 4)) || (s2 == 1 && !(f & 8)))
+              continue;
+            wsum += v.w * (double)((s1 == 0 ? 2 : 1) * (s2 == 0 ? 2 : 1));
+          }
+      } else {
+        for (int st = -1; st <= 1; ++st) {
+          if ((st == -1 && !(f & 1)) || (st == 1 && !(f & 2))) continue;
+          wsum += v.w * (double)(st == 0 ? 2 : 1);
+        }
+      }
+    }
+    v.inv_wsum[f] = P.beta != 1.0 ? 1.0 / wsum : 1.0;
+  }
+  return v;
+}
+
+// c0 = p-row coefficient of u_k at face c (operator.hpp:267 on a unit probe):
+// v = beta*(-1) [+ (w*centre)*(-1)], v *= 1/wsum, v * inv_h. Windows use
+// global z (g.zoff/gn2) for the boundary bits.
+template <int ND>
+__device__ __forceinline__ double vk_c0(const VkPar& V, const Geo& g, int k, const int* c) {
+  double v = V.beta * -1.0;
+  if (V.beta != 1.0) {
+    int f;
+    if (ND == 3) {
+      const int t1 = (k + 1) % 3, t2 = (k + 2) % 3;
+      const int cg[3] = {c[0], c[1], c[2] + g.zoff};
+      const int L[3] = {g.n[0], g.n[1], g.gn2};
+      f = (cg[t1] >= 1) | ((cg[t1] + 1 < L[t1]) << 1) | ((cg[t2] >= 1) << 2) | ((cg[t2] + 1 < L[t2]) << 3);
+      v += (V.w * 4.0) * -1.0;
+    } else {
+      const int t = 1 - k;
+      f = (c[t] >= 1) | ((c[t] + 1 < g.n[t]) << 1);
+      v += (V.w * 2.0) * -1.0;
+    }
+    v = v * V.inv_wsum[f];
+  }
+  return v * V.ih;
+}
+
+// Expand a compact entry set into the reference layout (for lexicographic
+// sweeps and readback): per k [Uinv..., g0, g1, h0, h1], then 1/s.
+template <int ND>
+__device__ __forceinline__ void vk_expand(const VkPar& V, const Geo& g, int full, const int* c, const cplx* cq,
+                                          cplx* q) {
+  int o = 0;
+  for (int k = 0; k < ND; ++k) {
+    cplx U00, U01, U10, U11;
+    if (full) {
+      U00 = cq[4 * k], U01 = cq[4 * k + 1], U10 = cq[4 * k + 2], U11 = cq[4 * k + 3];
+      q[o++] = U00, q[o++] = U01, q[o++] = U10, q[o++] = U11;
+    } else {
+      U00 = cq[2 * k], U11 = cq[2 * k + 1], U01 = U10 = mk(0, 0);
+      q[o++] = U00, q[o++] = U11;
+    }
+    const cplx b0 = mk(V.ih, 0), b1 = mk(-V.ih, 0);
+    const double c0 = vk_c0<ND>(V, g, k, c);
+    const cplx k0 = mk(c0, 0), k1 = mk(-c0, 0);
+    q[o++] = U00 * b0 + U01 * b1;  // g0
+    q[o++] = U10 * b0 + U11 * b1;  // g1
+    q[o++] = k0 * U00 + k1 * U10;  // h0
+    q[o++] = k0 * U01 + k1 * U11;  // h1
+  }
+  q[o] = cq[ND * (full ? 4 : 2)];
+}
+
+// Compact cache re-laid out per colour, component-major (SoA): entry e of
+// the cell with colour index t of colour col lives at soa[(col*cs + e)*nt + t],
 // so a warp of same-colour cells reads each entry fully coalesced.
 template <int ND>
-__global__ void k_vanka_to_soa(Geo g, int stride, const cplx* __restrict__ aos, cplx* __restrict__ soa,
-                               int inverse) {
+__global__ void k_vanka_to_soa(Geo g, int full, const cplx* __restrict__ aos, cplx* __restrict__ soa) {
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1, blk = full ? 8 : 6, nu = full ? 4 : 2;
+  const int cs = ND * nu + 1;
   const int64_t nt = colour_threads(g);
   GRID_STRIDE(u, 2 * nt) {
     const int col = (int)(u / nt);
     const int64_t t = u % nt;
     int c[3];
     if (!colour_cell(g, t, col, c)) continue;
-    const int64_t ci = g.clin(c);
-    for (int e = 0; e < stride; ++e) {
-      const int64_t si = ((int64_t)col * stride + e) * nt + t;
-      if (inverse) const_cast<cplx*>(aos)[ci * stride + e] = soa[si];
-      else soa[si] = aos[ci * stride + e];
-    }
+    const cplx* a = aos + g.clin(c) * stride;
+    for (int k = 0; k < ND; ++k)
+      for (int e = 0; e < nu; ++e) soa[((int64_t)col * cs + k * nu + e) * nt + t] = a[k * blk + e];
+    soa[((int64_t)col * cs + cs - 1) * nt + t] = a[stride - 1];
+  }
+}
+
+// Readback in the reference layout (vanka.hpp:72).
+template <int ND>
+__global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict__ soa, cplx* __restrict__ aos) {
+  const int stride = ND * ((full ? 4 : 2) + 4) + 1, cs = ND * (full ? 4 : 2) + 1;
+  const int64_t nt = colour_threads(g);
+  GRID_STRIDE(u, 2 * nt) {
+    const int col = (int)(u / nt);
+    const int64_t t = u % nt;
+    int c[3];
+    if (!colour_cell(g, t, col, c)) continue;
+    cplx cq[13];
+    for (int e = 0; e < cs; ++e) cq[e] = soa[((int64_t)col * cs + e) * nt + t];
+    vk_expand<ND>(V, g, full, c, cq, aos + g.clin(c) * stride);
   }
 }
 
@@ -193,21 +297,28 @@ __global__ void k_vanka_to_soa(Geo g, int stride, const cplx* __restrict__ aos, 
 // `color` solves its local system from r and adds w * correction to the DOFs
 // it owns. Cells of one colour share no DOFs, so the in-place writes commute.
 template <int ND>
-__global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, int full, const cplx* __restrict__ soa,
+__global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int full, const cplx* __restrict__ soa,
                                                            const cplx* __restrict__ r, int color, double w,
                                                            cplx* __restrict__ x) {
-  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
-  const int blk_w = full ? 8 : 6;
+  const int nu = full ? 4 : 2, cs = ND * nu + 1;
   const int64_t nt = colour_threads(g);
   GRID_STRIDE(t, nt) {
     int c[3];
     if (!colour_cell(g, t, color, c)) continue;
-    const cplx* q = soa + (int64_t)color * stride * nt + t;
+    const cplx* q = soa + (int64_t)color * cs * nt + t;
     auto Q = [&](int e) { return q[(int64_t)e * nt]; };
     const int64_t pi = g.off[ND] + g.clin(c);
     int64_t fi[ND][2];
     cplx rr[ND][2];
     cplx dpa = r[pi];
+    const cplx b0 = mk(V.ih, 0), b1 = mk(-V.ih, 0);
+    auto loadU = [&](int k, cplx* U) {
+      if (full) {
+        U[0] = Q(4 * k), U[1] = Q(4 * k + 1), U[2] = Q(4 * k + 2), U[3] = Q(4 * k + 3);
+      } else {
+        U[0] = Q(2 * k), U[3] = Q(2 * k + 1), U[1] = U[2] = mk(0, 0);
+      }
+    };
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       int f1[3];
@@ -216,20 +327,26 @@ __global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, int full, cons
       fi[k][1] = g.off[k] + g.flin(k, f1);
       rr[k][0] = r[fi[k][0]];
       rr[k][1] = r[fi[k][1]];
-      const int hk = k * blk_w + (full ? 6 : 4);
-      dpa -= Q(hk) * rr[k][0] + Q(hk + 1) * rr[k][1];
+      cplx U[4];
+      loadU(k, U);
+      const double c0 = vk_c0<ND>(V, g, k, c);
+      const cplx k0 = mk(c0, 0), k1 = mk(-c0, 0);
+      const cplx h0 = k0 * U[0] + k1 * U[2], h1 = k0 * U[1] + k1 * U[3];
+      dpa -= h0 * rr[k][0] + h1 * rr[k][1];
     }
-    const cplx dp = Q(stride - 1) * dpa;
+    const cplx dp = Q(cs - 1) * dpa;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      const int bk = k * blk_w, gk = bk + (full ? 4 : 2);
+      cplx U[4];
+      loadU(k, U);  // second read hits L1
+      const cplx g0 = U[0] * b0 + U[1] * b1, g1 = U[2] * b0 + U[3] * b1;
       cplx du0, du1;
       if (full) {
-        du0 = Q(bk + 0) * rr[k][0] + Q(bk + 1) * rr[k][1] - Q(gk) * dp;
-        du1 = Q(bk + 2) * rr[k][0] + Q(bk + 3) * rr[k][1] - Q(gk + 1) * dp;
+        du0 = U[0] * rr[k][0] + U[1] * rr[k][1] - g0 * dp;
+        du1 = U[2] * rr[k][0] + U[3] * rr[k][1] - g1 * dp;
       } else {
-        du0 = Q(bk + 0) * rr[k][0] - Q(gk) * dp;
-        du1 = Q(bk + 1) * rr[k][1] - Q(gk + 1) * dp;
+        du0 = U[0] * rr[k][0] - g0 * dp;
+        du1 = U[3] * rr[k][1] - g1 * dp;
       }
       x[fi[k][0]] += w * du0;
       x[fi[k][1]] += w * du1;
@@ -240,18 +357,19 @@ __global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, int full, cons
 
 // Lexicographic sweep (vanka.hpp:192): inherently sequential; one thread.
 template <int ND>
-__global__ void k_vanka_lex(Geo g, OpPar P, const Cell* __restrict__ m, int full,
+__global__ void k_vanka_lex(Geo g, OpPar P, VkPar V, const Cell* __restrict__ m, int full,
                             const cplx* __restrict__ cache, const cplx* __restrict__ b,
                             cplx* __restrict__ x, double w) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  const int stride = ND * ((full ? 4 : 2) + 4) + 1;
+  const int cs = ND * (full ? 4 : 2) + 1;
   FieldAcc A{x};
   for (int64_t ci = 0; ci < g.ncells; ++ci) {
     int c[3] = {(int)(ci % g.n[0]), (int)((ci / g.n[0]) % g.n[1]), (int)(ci / ((int64_t)g.n[0] * g.n[1]))};
-    cplx du[2 * ND], dp, q[4 * 8 + 1];
+    cplx du[2 * ND], dp, q[4 * 8 + 1], cq[13];
     const int color = (c[0] + c[1] + c[2]) & 1;
     const int64_t nt = colour_threads(g), t = colour_index(g, c);
-    for (int e = 0; e < stride; ++e) q[e] = cache[((int64_t)color * stride + e) * nt + t];
+    for (int e = 0; e < cs; ++e) cq[e] = cache[((int64_t)color * cs + e) * nt + t];
+    vk_expand<ND>(V, g, full, c, cq, q);
     vanka_corr<ND>(g, P, m, full, q, b, A, c, du, dp);
     for (int k = 0; k < ND; ++k) {
       int f1[3];

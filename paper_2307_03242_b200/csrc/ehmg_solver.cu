@@ -262,7 +262,8 @@ static Geo coarse_geo(const Geo& g) {
 // Red-black colour = fused residual kernel (stencil) + coalesced local
 // solve/update kernel reading the colour-major SoA factor cache.
 struct Smoother {
-  int full = 1, stride = 0;
+  int full = 1, stride = 0;  // stride: reference (vanka.hpp:35) entries per cell
+  VkPar vk;
   DBuf<cplx> soa, res;
   // Cache for the cells of `gg` (global grid, global packed media m), or of
   // its z-window [z0, z1) when z1 >= 0; sweeps then run on the window geometry.
@@ -286,9 +287,10 @@ struct Smoother {
       CK(cudaStreamSynchronize(s));
       if (hb) throw Err(EHMG_ERUNTIME, "vanka: singular local cell system");
       const int64_t nt = colour_threads(g);
-      soa.alloc(2 * nt * stride);
-      if (g.nd == 3) k_vanka_to_soa<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, aos.p, soa.p, 0);
-      else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, aos.p, soa.p, 0);
+      vk = make_vkpar(g, P);
+      soa.alloc(2 * nt * (g.nd * (full ? 4 : 2) + 1));
+      if (g.nd == 3) k_vanka_to_soa<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, full, aos.p, soa.p);
+      else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, full, aos.p, soa.p);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(s));
     }
@@ -297,16 +299,16 @@ struct Smoother {
   // reference (AoS, vanka.hpp:72) layout of the cache, for inspection
   void cache_aos(const Geo& g, cplx* out, cudaStream_t s) const {
     const int64_t nt = colour_threads(g);
-    if (g.nd == 3) k_vanka_to_soa<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, out, soa.p, 1);
-    else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, stride, out, soa.p, 1);
+    if (g.nd == 3) k_vanka_expand<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, out);
+    else k_vanka_expand<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, out);
     CK(cudaGetLastError());
   }
   void sweep(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
              int order, cudaStream_t s) {
     const Cell* m = mr.packed;
     if (order == 0) {
-      if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, m, full, soa.p, b, x, w);
-      else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, m, full, soa.p, b, x, w);
+      if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
+      else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
       CK(cudaGetLastError());
       return;
     }
@@ -320,9 +322,9 @@ struct Smoother {
     launch_residual(g, P, mr, x, b, res.p, s);
     Prof pf("vanka_update", s);
     if (g.nd == 3)
-      k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, lc, w, x);
+      k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, res.p, lc, w, x);
     else
-      k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, full, soa.p, res.p, lc, w, x);
+      k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, res.p, lc, w, x);
     CK(cudaGetLastError());
   }
 };
