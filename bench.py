@@ -309,7 +309,7 @@ def run_b200(args, ws, rank, local):
     kernels = {f"{k}@L{lv}": {"avg_ms": round(t / c, 4), "count_per_step": c / args.steps,
                               "share": round(t / sum(p[3] for p in prof), 4),
                               "alg_GBps": round(alg_bytes(k, n, lv) / (t / c / 1e3) / 1e9, 1)}
-               for (k, lv, c, t) in prof if lv <= 0 or k == "coarse_solve"}
+               for (k, lv, c, t) in prof}
 
     # stencil throughput: the unshifted operator apply at full size
     y = torch.empty_like(r)

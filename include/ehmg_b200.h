@@ -129,6 +129,21 @@ int ehmg_slab_multigrid_precondition(ehmg_slab_mg mg, const double* r, double* z
 /* bytes moved by ghost exchanges + agglomeration during the last precondition */
 int64_t ehmg_slab_multigrid_exchanged_bytes(ehmg_slab_mg mg);
 
+/* ---- one z-slab per process (one process per GPU on one node). Ranks
+ *      rendezvous through a POSIX shared-memory segment named by `job`,
+ *      share inbox buffers through CUDA IPC (peer copies over NVLink) and
+ *      sum FGMRES reductions in rank order. Media and fields are passed as
+ *      full host arrays; each rank reads its window and writes back only the
+ *      planes it owns. Results equal the single-process solver's. */
+typedef struct ehmg_dist_s* ehmg_dist;
+int ehmg_dist_create(const char* job, int rank, int nranks, int device, int ndim, const int* dims,
+                     double h, const double* lambda, const double* mu, const double* rho,
+                     const double* gamma, double beta, double omega, double alpha,
+                     const ehmg_mg_options* opt, int agg_n2, ehmg_dist* out);
+int ehmg_dist_destroy(ehmg_dist d);
+int ehmg_dist_window(ehmg_dist d, int* z0, int* z1, int* w0, int* w1);
+int ehmg_dist_precondition(ehmg_dist d, const double* r, double* z);
+
 /* Per-launch CUDA-event profiling of the cycle kernels (bench roofline).
  * report: one "kernel level count total_ms" line per (kernel, level). */
 int ehmg_profile_enable(int on);
@@ -156,6 +171,10 @@ typedef struct {
 int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int where,
                       const ehmg_krylov_options* opt, ehmg_krylov_result* res, double* history,
                       int history_cap);
+/* FGMRES over z-slab-distributed vectors (one slab per process); b and x are
+ * full host arrays, x receives this rank's owned planes. */
+int ehmg_dist_solve(ehmg_dist d, const double* b, double* x, const ehmg_krylov_options* opt,
+                    ehmg_krylov_result* res, double* history, int history_cap);
 
 /* ---- field BLAS-1 on device buffers (grid.hpp:129 axpy, :135 scal,
  *      :142 dot, :150 norm) ------------------------------------------------ */

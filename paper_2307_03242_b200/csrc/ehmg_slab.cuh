@@ -1,29 +1,33 @@
-// ehmg_slab.cuh -- z-slab decomposed multigrid (north_star subsystem (6)).
+// ehmg_slab.cuh -- z-slab decomposed multigrid and FGMRES (north_star
+// subsystem (6)).
 //
-// Fine levels are split into z-slabs: slab s owns cell planes [Z0, Z1) (and
+// Fine levels are split into z-slabs: slab q owns cell planes [Z0, Z1) (and
 // u2 faces [Z0, Z1), plus face n2 on the last slab) and stores the window
-// [Z0-3, Z1+2) (ghost planes, clipped to the grid; one extra plane below
-// because the u2 mass row of the first ghost face averages rho/gamma one
-// cell further down). Kernels run on the
-// window with global boundary semantics (Geo::zoff/gn2); values near the
-// window edge are scratch. Every operation that changes a field is followed
-// by a ghost exchange (owned planes -> neighbour ghosts), which keeps the
-// owned region bit-identical to the undecomposed cycle:
+// [Z0-3, Z1+2) clipped to the grid (one extra ghost plane below because the
+// u2 mass row of the first ghost face averages rho/gamma one cell further
+// down). Kernels run on the window with global boundary semantics
+// (Geo::zoff/gn2); values near the window edge are scratch. Every operation
+// that changes a field is followed by a ghost exchange, which keeps the owned
+// region identical to the undecomposed computation:
 //   * a red-black colour updates all window cells; owned DOFs only depend on
 //     residuals of owned cells and of the first ghost cell layer below, which
 //     only depend on data inside the window;
 //   * restriction reads the fine residual one plane beyond the owned range;
 //   * prolongation reads coarse ghosts refreshed by the coarse level's last
 //     exchange.
-// Levels whose z extent is <= agg_n2 are agglomerated: the restricted
-// residual is gathered into one full array and every rank runs the remaining
-// levels (incl. the exact coarsest solve) redundantly, then prolongs into its
-// own window -- no scatter is needed on the way up.
+// Levels whose z extent is <= agg_n2 are agglomerated: every slab pushes its
+// restricted owned planes into each rank's full coarse array and every rank
+// runs the remaining levels (incl. the exact coarsest solve) redundantly,
+// then prolongs into its own window.
 //
-// Transport: slabs of one process exchange with device-to-device copies
-// (the in-process P-slab mode used by the tests on one GPU); across
-// processes the same plane ranges go over NCCL/NVLink (ExchangeFn hook).
+// Exchange = push owned boundary planes into the neighbour's inbox (device
+// copy; a peer pointer over NVLink when the neighbour is another process),
+// barrier, pull the inbox into the ghost planes. One code path serves the
+// in-process P-slab mode (all slabs in one process on one GPU -- the GPU
+// tests) and the one-slab-per-process mode (NodeComm + CUDA IPC).
 #pragma once
+
+#include "ehmg_comm.cuh"
 
 struct SlabPlan {
   int nslabs = 1, La = 1, nl = 2;  // distributed levels [0, La), replicated [La, nl)
@@ -60,12 +64,45 @@ static SlabPlan make_slab_plan(int n2, int nl, int nslabs, int agg_n2) {
   throw Err(EHMG_EINVAL, "slab: grid too thin for the requested number of slabs");
 }
 
+// planes of component k per z step on geometry g
+static inline int64_t slab_plane(const Geo& g, int k) { return (int64_t)(g.n[0] + (k == 0)) * (g.n[1] + (k == 1)); }
+
+struct SlabGeo {
+  Geo g;       // window geometry (local storage, global semantics)
+  int Z0, Z1;  // owned cell planes (global)
+  int W0() const { return g.zoff; }
+  int W1() const { return g.zoff + g.n[2]; }
+  // ghost planes [a, b) of component k below / above the owned range
+  void ghost(int k, bool above, int& a, int& b) const {
+    if (!above) {
+      a = W0();
+      b = Z0;
+    } else {
+      a = Z1;
+      b = W1() + (k == 2 ? 1 : 0);
+    }
+  }
+  // inbox layout: component blocks of the ghost planes, below or above
+  int64_t inbox_off(int k, bool above) const {
+    int64_t o = 0;
+    for (int c = 0; c < k; ++c) {
+      int a, b;
+      ghost(c, above, a, b);
+      o += slab_plane(g, c) * std::max(0, b - a);
+    }
+    return o;
+  }
+  int64_t inbox_size(bool above) const { return inbox_off(4, above); }
+};
+
 struct SlabLevel {
-  Geo g;           // window geometry (local storage, global semantics)
-  int Z0, Z1;      // owned cell planes (global)
-  DevMedia media;  // window media
+  SlabGeo sg;
+  bool local = false;
+  DevMedia media;  // window media (local slabs)
   Smoother sm;
-  DBuf<cplx> r, bc, ec;
+  DBuf<cplx> r, bc, ec, in_lo, in_hi, ctmp;
+  cplx* peer_lo = nullptr;  // inbox pointers (own or IPC-mapped)
+  cplx* peer_hi = nullptr;
 };
 
 struct ehmg_slab_mg_s {
@@ -74,151 +111,208 @@ struct ehmg_slab_mg_s {
   ehmg_mg_options opt;
   OpPar P;
   SlabPlan plan;
-  std::vector<Geo> G;                                        // global geometry per level
-  std::vector<std::vector<std::unique_ptr<SlabLevel>>> L;   // [level < La][slab]
-  std::unique_ptr<ehmg_mg_s> rep;                            // replicated levels [La, nl)
-  DBuf<cplx> brep, erep;                                     // level-La full rhs / correction
-  std::vector<std::unique_ptr<DBuf<cplx>>> bw, xw;          // level-0 windows
-  std::vector<std::unique_ptr<DBuf<cplx>>> ctmp;            // restriction staging (level La windows)
+  int q_lo = 0, q_hi = 0;   // local slabs [q_lo, q_hi)
+  NodeComm* comm = nullptr;  // one-slab-per-process mode
+  std::vector<Geo> G;        // global geometry per level
+  std::vector<std::vector<std::unique_ptr<SlabLevel>>> L;  // [level < La][slab]
+  std::unique_ptr<ehmg_mg_s> rep;                           // replicated levels [La, nl)
+  DBuf<cplx> brep, erep;                                    // level-La full rhs / correction (this rank)
+  std::vector<cplx*> brep_of;                               // every rank's brep (own or IPC-mapped)
+  std::vector<void*> mapped;                                // IPC mappings to close
+  std::vector<std::unique_ptr<DBuf<cplx>>> bw, xw;         // level-0 windows of local slabs
   int64_t exchanged_bytes = 0;
 
   ~ehmg_slab_mg_s() {
+    for (void* p : mapped) cudaIpcCloseMemHandle(p);
     L.clear();
     rep.reset();
     if (s) cudaStreamDestroy(s);
   }
 
   int P_() const { return plan.nslabs; }
+  bool local(int q) const { return q >= q_lo && q < q_hi; }
 
-  // bytes per z-plane of component k (faces or cells) on geometry g
-  static int64_t plane(const Geo& g, int k) {
-    return (int64_t)(g.n[0] + (k == 0)) * (g.n[1] + (k == 1));
+  void sync_barrier() {
+    CK(cudaStreamSynchronize(s));
+    if (comm) comm->barrier();
   }
-  // copy global planes [a, b) of component k between two window/full arrays
-  void copy_planes(cplx* dst, const Geo& dg, const cplx* src, const Geo& sg, int k, int a, int b) {
-    if (b <= a) return;
-    const int64_t ps = plane(dg, k);
-    CK(cudaMemcpyAsync(dst + dg.off[k] + (a - dg.zoff) * ps, src + sg.off[k] + (a - sg.zoff) * ps,
-                       sizeof(cplx) * ps * (b - a), cudaMemcpyDeviceToDevice, s));
-    exchanged_bytes += (int64_t)sizeof(cplx) * ps * (b - a);
+  void copy(cplx* dst, const cplx* src, int64_t n) {
+    if (n <= 0) return;
+    CK(cudaMemcpyAsync(dst, src, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, s));
+    exchanged_bytes += (int64_t)sizeof(cplx) * n;
+  }
+  // global planes [a, b) of component k between a window array and an inbox block
+  void to_inbox(cplx* inbox, const SlabGeo& dst, bool above, const cplx* v, const SlabGeo& src, int k) {
+    int a, b;
+    dst.ghost(k, above, a, b);
+    const int64_t ps = slab_plane(src.g, k);
+    copy(inbox + dst.inbox_off(k, above), v + src.g.off[k] + (a - src.g.zoff) * ps, ps * (b - a));
+  }
+  void from_inbox(cplx* v, const SlabGeo& dst, bool above, const cplx* inbox, int k) {
+    int a, b;
+    dst.ghost(k, above, a, b);
+    const int64_t ps = slab_plane(dst.g, k);
+    copy(v + dst.g.off[k] + (a - dst.g.zoff) * ps, inbox + dst.inbox_off(k, above), ps * (b - a));
   }
 
-  // owned planes -> neighbour ghosts, every slab boundary, all 4 components
+  // ghost exchange of one field per local slab (V indexed by slab)
   void exchange(int l, const std::vector<cplx*>& V) {
-    const int64_t before = exchanged_bytes;
-    for (int q = 0; q + 1 < P_(); ++q) {
-      SlabLevel& lo = *L[l][q];
-      SlabLevel& hi = *L[l][q + 1];
-      const int zb = lo.Z1;  // == hi.Z0
-      const int lo_top = lo.g.zoff + lo.g.n[2], hi_bot = hi.g.zoff;
-      for (int k = 0; k < 4; ++k) {
-        const bool face = (k == 2);
-        // up: lo's owned top planes -> hi's ghosts below (cells/faces [hi_bot, zb))
-        copy_planes(V[q + 1], hi.g, V[q], lo.g, k, hi_bot, zb);
-        // down: hi's owned bottom planes -> lo's ghosts above (cells [zb, lo_top), faces [zb, lo_top])
-        copy_planes(V[q], lo.g, V[q + 1], hi.g, k, zb, face ? lo_top + 1 : lo_top);
+    sync_barrier();  // neighbours finished updating owned planes and reading inboxes
+    for (int q = q_lo; q < q_hi; ++q) {
+      const SlabLevel& me = *L[l][q];
+      if (q + 1 < P_()) {
+        const SlabLevel& up = *L[l][q + 1];
+        for (int k = 0; k < 4; ++k) to_inbox(up.peer_lo, up.sg, false, V[q], me.sg, k);
+      }
+      if (q > 0) {
+        const SlabLevel& dn = *L[l][q - 1];
+        for (int k = 0; k < 4; ++k) to_inbox(dn.peer_hi, dn.sg, true, V[q], me.sg, k);
       }
     }
-    (void)before;
+    sync_barrier();  // all pushes landed
+    for (int q = q_lo; q < q_hi; ++q) {
+      SlabLevel& me = *L[l][q];
+      for (int k = 0; k < 4; ++k) {
+        if (q > 0) from_inbox(V[q], me.sg, false, me.in_lo.p, k);
+        if (q + 1 < P_()) from_inbox(V[q], me.sg, true, me.in_hi.p, k);
+      }
+    }
   }
 
-  void sweep_all(int l, const std::vector<const cplx*>& B, const std::vector<cplx*>& X) {
+  void sweep_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X) {
     for (int color = 0; color < 2; ++color) {
-      for (int q = 0; q < P_(); ++q) {
+      for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& sl = *L[l][q];
-        sl.sm.colour_phase(sl.g, P, sl.media.ref(), B[q], X[q], opt.damping, color, s);
+        sl.sm.colour_phase(sl.sg.g, P, sl.media.ref(), B[q], X[q], opt.damping, color, s);
       }
       exchange(l, X);
     }
   }
 
-  // multigrid.hpp:217 cycle_at on the distributed levels
-  void cycle(int l, const std::vector<const cplx*>& B, const std::vector<cplx*>& X) {
+  // multigrid.hpp:217 cycle_at on the distributed levels (B ghosts valid)
+  void cycle(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X) {
     const int La = plan.La, nl = plan.nl;
     for (int q = 0; q < opt.nu1; ++q) sweep_all(l, B, X);
-    for (int q = 0; q < P_(); ++q) {
+    for (int q = q_lo; q < q_hi; ++q) {
       SlabLevel& sl = *L[l][q];
-      launch_residual(sl.g, P, sl.media.ref(), X[q], B[q], sl.r.p, s);
+      launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], sl.r.p, s);
     }
     const bool next_coarsest = (l + 2 == nl);
     const int repeat = (opt.cycle == 2 && !next_coarsest) ? 2 : 1;
     if (l + 1 < La) {
-      std::vector<const cplx*> BC(P_());
-      std::vector<cplx*> BCw(P_()), EC(P_());
-      for (int q = 0; q < P_(); ++q) {
+      std::vector<cplx*> BC(P_(), nullptr), EC(P_(), nullptr);
+      for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& f = *L[l][q];
         SlabLevel& c = *L[l + 1][q];
-        launch_transfer(f.g, c.g, true, f.r.p, c.bc.p, false, s);
-        CK(cudaMemsetAsync(c.ec.p, 0, sizeof(cplx) * c.g.ndofs, s));
+        launch_transfer(f.sg.g, c.sg.g, true, f.r.p, c.bc.p, false, s);
+        CK(cudaMemsetAsync(c.ec.p, 0, sizeof(cplx) * c.sg.g.ndofs, s));
         BC[q] = c.bc.p;
-        BCw[q] = c.bc.p;
         EC[q] = c.ec.p;
       }
-      exchange(l + 1, BCw);
+      exchange(l + 1, BC);
       for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC);
-      for (int q = 0; q < P_(); ++q)
-        launch_transfer(L[l][q]->g, L[l + 1][q]->g, false, L[l + 1][q]->ec.p, X[q], true, s);
+      for (int q = q_lo; q < q_hi; ++q)
+        launch_transfer(L[l][q]->sg.g, L[l + 1][q]->sg.g, false, L[l + 1][q]->ec.p, X[q], true, s);
     } else {
-      // agglomerate: restrict each slab's owned coarse planes into the full array
+      // agglomerate: push each slab's restricted owned planes into every rank's full array
       const Geo& gc = G[La];
-      for (int q = 0; q < P_(); ++q) {
+      sync_barrier();  // every rank finished reading its brep (previous cycle)
+      for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& f = *L[l][q];
-        const int c0 = f.Z0 / 2, c1 = f.Z1 / 2;
+        const int c0 = f.sg.Z0 / 2, c1 = f.sg.Z1 / 2;
         const Geo cw = make_window(gc, c0, c1);
-        launch_transfer(f.g, cw, true, f.r.p, ctmp[q]->p, false, s);
+        launch_transfer(f.sg.g, cw, true, f.r.p, f.ctmp.p, false, s);
         const bool last = (q + 1 == P_());
-        for (int k = 0; k < 4; ++k)
-          copy_planes(brep.p, gc, ctmp[q]->p, cw, k, c0, (k == 2 && last) ? c1 + 1 : c1);
+        for (cplx* dst : brep_of)
+          for (int k = 0; k < 4; ++k) {
+            const int b = (k == 2 && last) ? c1 + 1 : c1;
+            const int64_t ps = slab_plane(gc, k);
+            copy(dst + gc.off[k] + c0 * ps, f.ctmp.p + cw.off[k], ps * (b - c0));
+          }
       }
+      sync_barrier();  // the full coarse rhs is assembled on every rank
       CK(cudaMemsetAsync(erep.p, 0, sizeof(cplx) * gc.ndofs, s));
       CK(cudaStreamSynchronize(s));
       for (int r = 0; r < repeat; ++r) rep->cycle_at(0, brep.p, erep.p);
       CK(cudaStreamSynchronize(rep->s));
-      for (int q = 0; q < P_(); ++q) launch_transfer(L[l][q]->g, gc, false, erep.p, X[q], true, s);
+      for (int q = q_lo; q < q_hi; ++q) launch_transfer(L[l][q]->sg.g, gc, false, erep.p, X[q], true, s);
     }
     for (int q = 0; q < opt.nu2; ++q) sweep_all(l, B, X);
   }
 
-  // Full-array boundary of the in-process mode: scatter r into the level-0
-  // windows (ghosts included), cycle, gather the owned planes into z.
-  void precondition(const cplx* r, cplx* z) {
-    const Geo& g0 = G[0];
-    std::vector<const cplx*> B(P_());
-    std::vector<cplx*> X(P_());
-    for (int q = 0; q < P_(); ++q) {
-      const Geo& w = L[0][q]->g;
-      for (int k = 0; k < 4; ++k)
-        copy_planes(bw[q]->p, w, r, g0, k, w.zoff, w.zoff + w.n[2] + (k == 2));
-      CK(cudaMemsetAsync(xw[q]->p, 0, sizeof(cplx) * w.ndofs, s));
-      B[q] = bw[q]->p;
-      X[q] = xw[q]->p;
-    }
+  // z = M r on the level-0 windows of the local slabs (ghosts of B refreshed here)
+  void precondition_windows(const std::vector<cplx*>& B, const std::vector<cplx*>& X) {
+    exchange(0, B);
+    for (int q = q_lo; q < q_hi; ++q)
+      CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
     cycle(0, B, X);
-    for (int q = 0; q < P_(); ++q) {
-      SlabLevel& sl = *L[0][q];
-      const bool last = (q + 1 == P_());
-      for (int k = 0; k < 4; ++k)
-        copy_planes(z, g0, xw[q]->p, sl.g, k, sl.Z0, (k == 2 && last) ? sl.Z1 + 1 : sl.Z1);
+  }
+
+  // global array <-> level-0 windows of the local slabs
+  void scatter(const cplx* full, std::vector<cplx*>& W) {
+    for (int q = q_lo; q < q_hi; ++q) {
+      const Geo& w = L[0][q]->sg.g;
+      for (int k = 0; k < 4; ++k) {
+        const int64_t ps = slab_plane(w, k);
+        CK(cudaMemcpyAsync(W[q] + w.off[k], full + G[0].off[k] + (int64_t)w.zoff * ps,
+                           sizeof(cplx) * ps * (w.n[2] + (k == 2)), cudaMemcpyDeviceToDevice, s));
+      }
     }
+  }
+  void gather(const std::vector<cplx*>& W, cplx* full) {
+    for (int q = q_lo; q < q_hi; ++q) {
+      const SlabGeo& sg = L[0][q]->sg;
+      const bool last = (q + 1 == P_());
+      for (int k = 0; k < 4; ++k) {
+        const int64_t ps = slab_plane(sg.g, k);
+        const int b = (k == 2 && last) ? sg.Z1 + 1 : sg.Z1;
+        CK(cudaMemcpyAsync(full + G[0].off[k] + (int64_t)sg.Z0 * ps, W[q] + sg.g.off[k] + (sg.Z0 - sg.g.zoff) * ps,
+                           sizeof(cplx) * ps * (b - sg.Z0), cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  std::vector<cplx*> windows(std::vector<std::unique_ptr<DBuf<cplx>>>& v) {
+    std::vector<cplx*> out(P_(), nullptr);
+    for (int q = q_lo; q < q_hi; ++q) out[q] = v[q - q_lo]->p;
+    return out;
+  }
+  // full-array boundary: scatter r (ghosts included), cycle, gather owned planes
+  void precondition(const cplx* r, cplx* z) {
+    auto B = windows(bw), X = windows(xw);
+    scatter(r, B);
+    for (int q = q_lo; q < q_hi; ++q)
+      CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
+    cycle(0, B, X);
+    gather(X, z);
     CK(cudaStreamSynchronize(s));
   }
 };
 
 static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double* const* host, const OpPar& P,
-                                                     const ehmg_mg_options& opt, int nslabs, int agg_n2) {
+                                                     const ehmg_mg_options& opt, int nslabs, int agg_n2,
+                                                     NodeComm* comm) {
   if (g0.nd != 3) throw Err(EHMG_EINVAL, "slab: z-slab decomposition is 3D only");
   if (opt.cycle == 3) throw Err(EHMG_EINVAL, "slab: K-cycles need a distributed inner Krylov (not supported)");
   if (opt.sweep != 1) throw Err(EHMG_EINVAL, "slab: only red-black sweeps decompose");
+  if (!stencil3d_supported(g0)) throw Err(EHMG_EINVAL, "slab: needs an even x extent (TMA stencil)");
   auto sm = std::make_unique<ehmg_slab_mg_s>();
   sm->opt = opt;
   sm->P = P;
+  sm->comm = comm;
   sm->plan = make_slab_plan(g0.n[2], opt.n_levels, nslabs, agg_n2);
+  if (comm) {
+    if (comm->n != nslabs) throw Err(EHMG_EINVAL, "slab: one slab per process");
+    sm->q_lo = comm->rank;
+    sm->q_hi = comm->rank + 1;
+  } else {
+    sm->q_lo = 0;
+    sm->q_hi = nslabs;
+  }
   const int La = sm->plan.La, nl = opt.n_levels;
   CK(cudaGetDevice(&sm->dev));
   CK(cudaStreamCreateWithFlags(&sm->s, cudaStreamNonBlocking));
   cudaStream_t s = sm->s;
-  if (!stencil3d_supported(g0)) throw Err(EHMG_EINVAL, "slab: needs an even x extent (TMA stencil)");
-  // global media per level [0, La]
+  // global media per level [0, La] (every rank holds them; setup only)
   std::vector<std::unique_ptr<DevMedia>> gm;
   for (int l = 0; l <= La; ++l) {
     sm->G.push_back(l == 0 ? g0 : coarse_geo(sm->G[l - 1]));
@@ -230,30 +324,68 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   for (int l = 0; l < La; ++l) {
     for (int q = 0; q < nslabs; ++q) {
       auto sl = std::make_unique<SlabLevel>();
-      sl->Z0 = sm->plan.z0[q] >> l;
-      sl->Z1 = sm->plan.z0[q + 1] >> l;
-      const int w0 = std::max(0, sl->Z0 - kSlabGhostLo), w1 = std::min(sm->G[l].n[2], sl->Z1 + kSlabGhostHi);
-      sl->g = make_window(sm->G[l], w0, w1);
-      sl->media.window_of(*gm[l], sm->G[l], w0, w1, s);
-      sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1);
-      sl->r.alloc(sl->g.ndofs);
-      if (l > 0) {
-        sl->bc.alloc(sl->g.ndofs);
-        sl->ec.alloc(sl->g.ndofs);
+      sl->sg.Z0 = sm->plan.z0[q] >> l;
+      sl->sg.Z1 = sm->plan.z0[q + 1] >> l;
+      const int w0 = std::max(0, sl->sg.Z0 - kSlabGhostLo), w1 = std::min(sm->G[l].n[2], sl->sg.Z1 + kSlabGhostHi);
+      sl->sg.g = make_window(sm->G[l], w0, w1);
+      sl->local = sm->local(q);
+      if (sl->local) {
+        sl->media.window_of(*gm[l], sm->G[l], w0, w1, s);
+        sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1);
+        sl->r.alloc(sl->sg.g.ndofs);
+        if (l > 0) {
+          sl->bc.alloc(sl->sg.g.ndofs);
+          sl->ec.alloc(sl->sg.g.ndofs);
+        }
+        sl->in_lo.alloc(std::max<int64_t>(1, sl->sg.inbox_size(false)));
+        sl->in_hi.alloc(std::max<int64_t>(1, sl->sg.inbox_size(true)));
+        sl->peer_lo = sl->in_lo.p;
+        sl->peer_hi = sl->in_hi.p;
+        if (l == La - 1) sl->ctmp.alloc(make_window(sm->G[La], sl->sg.Z0 / 2, sl->sg.Z1 / 2).ndofs);
       }
       sm->L[l].push_back(std::move(sl));
     }
   }
-  for (int q = 0; q < nslabs; ++q) {
-    sm->bw.emplace_back(new DBuf<cplx>(sm->L[0][q]->g.ndofs));
-    sm->xw.emplace_back(new DBuf<cplx>(sm->L[0][q]->g.ndofs));
-    const SlabLevel& f = *sm->L[La - 1][q];
-    sm->ctmp.emplace_back(new DBuf<cplx>(make_window(sm->G[La], f.Z0 / 2, f.Z1 / 2).ndofs));
+  for (int q = sm->q_lo; q < sm->q_hi; ++q) {
+    sm->bw.emplace_back(new DBuf<cplx>(sm->L[0][q]->sg.g.ndofs));
+    sm->xw.emplace_back(new DBuf<cplx>(sm->L[0][q]->sg.g.ndofs));
   }
   CK(cudaStreamSynchronize(s));
   sm->rep = build_mg(sm->G[La], nullptr, gm[La].get(), P, opt, nl - La);
   sm->brep.alloc(sm->G[La].ndofs);
   sm->erep.alloc(sm->G[La].ndofs);
+  sm->brep_of.push_back(sm->brep.p);
+  if (comm && comm->n > 1) {
+    // share inbox and coarse-rhs buffers through CUDA IPC (peer pointers)
+    struct Blob {
+      cudaIpcMemHandle_t h[2 * 8 + 1];
+    } mine{}, all[kCommMaxRanks];
+    const int q = comm->rank;
+    for (int l = 0; l < La; ++l) {
+      CK(cudaIpcGetMemHandle(&mine.h[2 * l], sm->L[l][q]->in_lo.p));
+      CK(cudaIpcGetMemHandle(&mine.h[2 * l + 1], sm->L[l][q]->in_hi.p));
+    }
+    CK(cudaIpcGetMemHandle(&mine.h[16], sm->brep.p));
+    comm->exchange_blob(&mine, sizeof(Blob), all);
+    sm->brep_of.clear();
+    for (int r = 0; r < comm->n; ++r) {
+      if (r == q) {
+        sm->brep_of.push_back(sm->brep.p);
+        continue;
+      }
+      auto open = [&](cudaIpcMemHandle_t h) {
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        sm->mapped.push_back(p);
+        return static_cast<cplx*>(p);
+      };
+      for (int l = 0; l < La; ++l) {
+        sm->L[l][r]->peer_lo = open(all[r].h[2 * l]);
+        sm->L[l][r]->peer_hi = open(all[r].h[2 * l + 1]);
+      }
+      sm->brep_of.push_back(open(all[r].h[16]));
+    }
+  }
   CK(cudaStreamSynchronize(s));
   return sm;
 }

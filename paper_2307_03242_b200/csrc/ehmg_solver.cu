@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/ehmg_b200.h"
+#include "ehmg_comm.cuh"
 #include "ehmg_kernels.cuh"
 #include "ehmg_stencil3d.cuh"
 
@@ -348,10 +349,45 @@ struct Blas {
   double* wpre() { return scal.p + 4; }
   double* wn() { return scal.p + 6; }
   double* hcol(int i) { return scal.p + 8 + 2 * i; }
+  // Distributed vectors (z-slab windows): reductions cover only the owned
+  // index ranges and are summed across ranks in rank order (deterministic).
+  NodeComm* comm = nullptr;
+  std::vector<std::pair<int64_t, int64_t>> owned;
+  DBuf<double> tmp;
   void reduce(int mode, int64_t n, const cplx* x, const cplx* y, double* out, double* coef_,
               double* hacc) {
-    k_reduce<<<kRedBlocks, kThreads, 0, s>>>(mode, n, x, y, partial.p, counter.p, out, coef_, hacc);
-    CK(cudaGetLastError());
+    if (owned.empty()) {
+      k_reduce<<<kRedBlocks, kThreads, 0, s>>>(mode, n, x, y, partial.p, counter.p, out, coef_, hacc);
+      CK(cudaGetLastError());
+      return;
+    }
+    if (!tmp.n) tmp.alloc(2);
+    double h[2] = {0, 0};
+    for (auto& rg : owned) {
+      k_reduce<<<kRedBlocks, kThreads, 0, s>>>(mode, rg.second - rg.first, x + rg.first, y ? y + rg.first : nullptr,
+                                               partial.p, counter.p, tmp.p, nullptr, nullptr);
+      CK(cudaGetLastError());
+      double part[2];
+      CK(cudaMemcpyAsync(part, tmp.p, sizeof(part), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      h[0] += part[0];
+      h[1] += part[1];
+    }
+    if (comm) comm->allreduce(h, 2);
+    CK(cudaMemcpyAsync(out, h, sizeof(h), cudaMemcpyHostToDevice, s));
+    if (coef_) {
+      const double c[2] = {-h[0], -h[1]};
+      CK(cudaMemcpyAsync(coef_, c, sizeof(c), cudaMemcpyHostToDevice, s));
+    }
+    if (hacc) {
+      double a[2];
+      CK(cudaMemcpyAsync(a, hacc, sizeof(a), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      a[0] += h[0];
+      a[1] += h[1];
+      CK(cudaMemcpyAsync(hacc, a, sizeof(a), cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
   }
   double norm_host(int64_t n, const cplx* x) {
     reduce(1, n, x, nullptr, res(), nullptr, nullptr);
@@ -997,7 +1033,7 @@ int ehmg_slab_multigrid_create(int nd, const int* dims, double h, const double* 
     }
     const OpPar P{beta, omega * omega, alpha};
     const double* f[4] = {lambda, mu, rho, gamma};
-    *out = build_slab_mg(g, f, P, *opt, nslabs, agg_n2).release();
+    *out = build_slab_mg(g, f, P, *opt, nslabs, agg_n2, nullptr).release();
   });
 }
 
@@ -1026,6 +1062,140 @@ int ehmg_slab_multigrid_precondition(ehmg_slab_mg mg, const double* r, double* z
 }
 
 int64_t ehmg_slab_multigrid_exchanged_bytes(ehmg_slab_mg mg) { return mg ? mg->exchanged_bytes : -1; }
+
+}  // extern "C"
+
+// ---- one slab per process (NodeComm + CUDA IPC) ---------------------------
+struct ehmg_dist_s {
+  NodeComm comm;
+  std::unique_ptr<ehmg_slab_mg_s> mg;
+  OpPar P0;  // unshifted operator (alpha = 0) for the Krylov level
+  ~ehmg_dist_s() {
+    mg.reset();
+    comm.close();
+  }
+  SlabLevel& me() { return *mg->L[0][comm.rank]; }
+  // host full array <-> this rank's level-0 window (window planes / owned planes)
+  void load_window(const double* full, cplx* w) {
+    const SlabGeo& sg = me().sg;
+    const Geo& G0 = mg->G[0];
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ps = slab_plane(sg.g, k);
+      CK(cudaMemcpyAsync(w + sg.g.off[k], reinterpret_cast<const cplx*>(full) + G0.off[k] + (int64_t)sg.g.zoff * ps,
+                         sizeof(cplx) * ps * (sg.g.n[2] + (k == 2)), cudaMemcpyHostToDevice, mg->s));
+    }
+  }
+  void store_owned(const cplx* w, double* full) {
+    const SlabGeo& sg = me().sg;
+    const Geo& G0 = mg->G[0];
+    const bool last = comm.rank + 1 == comm.n;
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ps = slab_plane(sg.g, k);
+      const int b = (k == 2 && last) ? sg.Z1 + 1 : sg.Z1;
+      CK(cudaMemcpyAsync(reinterpret_cast<cplx*>(full) + G0.off[k] + (int64_t)sg.Z0 * ps,
+                         w + sg.g.off[k] + (sg.Z0 - sg.g.zoff) * ps, sizeof(cplx) * ps * (b - sg.Z0),
+                         cudaMemcpyDeviceToHost, mg->s));
+    }
+    CK(cudaStreamSynchronize(mg->s));
+  }
+  std::vector<std::pair<int64_t, int64_t>> owned_ranges() {
+    const SlabGeo& sg = me().sg;
+    const bool last = comm.rank + 1 == comm.n;
+    std::vector<std::pair<int64_t, int64_t>> o;
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ps = slab_plane(sg.g, k);
+      const int b = (k == 2 && last) ? sg.Z1 + 1 : sg.Z1;
+      o.push_back({sg.g.off[k] + (sg.Z0 - sg.g.zoff) * ps, sg.g.off[k] + (b - sg.g.zoff) * ps});
+    }
+    return o;
+  }
+};
+
+extern "C" {
+
+int ehmg_dist_create(const char* job, int rank, int nranks, int device, int nd, const int* dims, double h,
+                     const double* lambda, const double* mu, const double* rho, const double* gamma,
+                     double beta, double omega, double alpha, const ehmg_mg_options* opt, int agg_n2,
+                     ehmg_dist* out) {
+  return guard([&] {
+    if (opt->n_levels < 2) throw Err(EHMG_EINVAL, "multigrid: need at least 2 levels");
+    validate_grid(nd, dims, h);
+    check_device();
+    CK(cudaSetDevice(device));
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    Geo g = make_geo(nd, d, h);
+    validate_media(g.ncells, lambda, mu, rho, gamma);
+    auto dd = std::make_unique<ehmg_dist_s>();
+    dd->comm.open(job, rank, nranks);
+    const OpPar P{beta, omega * omega, alpha};
+    dd->P0 = OpPar{beta, omega * omega, 0.0};
+    const double* f[4] = {lambda, mu, rho, gamma};
+    dd->mg = build_slab_mg(g, f, P, *opt, nranks, agg_n2, &dd->comm);
+    *out = dd.release();
+  });
+}
+
+int ehmg_dist_destroy(ehmg_dist d) {
+  return guard([&] { delete d; });
+}
+
+int ehmg_dist_window(ehmg_dist d, int* z0, int* z1, int* w0, int* w1) {
+  return guard([&] {
+    const SlabGeo& sg = d->me().sg;
+    *z0 = sg.Z0;
+    *z1 = sg.Z1;
+    *w0 = sg.W0();
+    *w1 = sg.W1();
+  });
+}
+
+int ehmg_dist_precondition(ehmg_dist d, const double* r, double* z) {
+  return guard([&] {
+    ehmg_slab_mg_s& mg = *d->mg;
+    const int q = d->comm.rank;
+    std::vector<cplx*> B(mg.P_(), nullptr), X(mg.P_(), nullptr);
+    B[q] = mg.bw[0]->p;
+    X[q] = mg.xw[0]->p;
+    d->load_window(r, B[q]);
+    mg.precondition_windows(B, X);
+    d->store_owned(X[q], z);
+  });
+}
+
+int ehmg_dist_solve(ehmg_dist d, const double* b, double* x, const ehmg_krylov_options* opt,
+                    ehmg_krylov_result* res, double* history, int history_cap) {
+  return guard([&] {
+    ehmg_slab_mg_s& mg = *d->mg;
+    const int q = d->comm.rank;
+    SlabLevel& me = d->me();
+    const int64_t n = me.sg.g.ndofs;
+    cudaStream_t s = mg.s;
+    DBuf<cplx> db(n), dx(n);
+    d->load_window(b, db.p);
+    dx.zero(s);
+    Fgmres fg;
+    fg.init(n, opt->restart, s);
+    fg.blas.comm = &d->comm;
+    fg.blas.owned = d->owned_ranges();
+    std::vector<cplx*> V(mg.P_(), nullptr), W(mg.P_(), nullptr);
+    Fgmres::Fn Af = [&](const cplx* in, cplx* out) {
+      V[q] = const_cast<cplx*>(in);  // ghost planes are scratch
+      mg.exchange(0, V);
+      launch_residual(me.sg.g, d->P0, me.media.ref(), in, nullptr, out, s);
+    };
+    Fgmres::Fn Mf = [&](const cplx* in, cplx* out) {
+      V[q] = const_cast<cplx*>(in);
+      W[q] = out;
+      mg.precondition_windows(V, W);
+    };
+    std::vector<double> hist;
+    *res = fg.run(Af, Mf, db.p, dx.p, *opt, hist);
+    res->n_history = (int)hist.size();
+    if (history)
+      for (int i = 0; i < (int)hist.size() && i < history_cap; ++i) history[i] = hist[i];
+    d->store_owned(dx.p, x);
+  });
+}
 
 int ehmg_multigrid_destroy(ehmg_mg mg) {
   return guard([&] { delete mg; });

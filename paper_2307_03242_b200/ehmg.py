@@ -113,6 +113,14 @@ def lib():
         L.ehmg_slab_multigrid_precondition.argtypes = [vp, vp, vp, C.c_int]
         L.ehmg_slab_multigrid_exchanged_bytes.argtypes = [vp]
         L.ehmg_slab_multigrid_exchanged_bytes.restype = i64
+        L.ehmg_dist_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, ip,
+                                       C.c_double, vp, vp, vp, vp, C.c_double, C.c_double,
+                                       C.c_double, C.POINTER(_MgOpts), C.c_int, C.POINTER(vp)]
+        L.ehmg_dist_destroy.argtypes = [vp]
+        L.ehmg_dist_window.argtypes = [vp, ip, ip, ip, ip]
+        L.ehmg_dist_precondition.argtypes = [vp, vp, vp]
+        L.ehmg_dist_solve.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_KRes), vp,
+                                      C.c_int]
         L.ehmg_profile_enable.argtypes = [C.c_int]
         L.ehmg_profile_report.argtypes = [C.c_char_p, C.c_int]
         _lib = L
@@ -647,6 +655,70 @@ class SlabMultigrid:
             raise ValueError("r and z must both be host arrays or both device tensors")
         _check(lib().ehmg_slab_multigrid_precondition(self._h, pr, pz, wr))
         return z
+
+
+class DistributedSlabSolver:
+    """One z-slab of the hierarchy per process (one process per GPU). Ranks
+    of one job meet in a shared-memory segment named `job`, exchange ghost
+    planes by peer copies (CUDA IPC) and sum reductions in rank order.
+    Fields are full host arrays; results carry this rank's owned planes."""
+
+    def __init__(self, job: str, rank: int, nranks: int, device: int, grid: StaggeredGrid,
+                 media: MediaModel, par: OperatorParams, opt: MgOptions, agg_n2: int = 64):
+        o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
+                    0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
+                    opt.k_inner_iterations, opt.k_inner_rtol)
+        arrs = media.arrays(grid)
+        h = C.c_void_p()
+        _check(lib().ehmg_dist_create(job.encode(), rank, nranks, device, grid.ndim,
+                                      _dims_arr(grid.dims), grid.h, *[a.ctypes.data for a in arrs],
+                                      par.beta, par.omega, par.alpha, C.byref(o), agg_n2,
+                                      C.byref(h)))
+        self._h = h
+        self.grid, self.n, self.rank, self.nranks = grid, grid.n_dofs(), rank, nranks
+
+    def close(self):
+        if _lib is not None and getattr(self, "_h", None):
+            _check(_lib.ehmg_dist_destroy(self._h))
+            self._h = None
+
+    __del__ = close
+
+    def window(self):
+        v = [C.c_int(0) for _ in range(4)]
+        _check(lib().ehmg_dist_window(self._h, *[C.byref(a) for a in v]))
+        return tuple(a.value for a in v)
+
+    def owned_mask(self):
+        """Boolean mask of the flat DOFs this rank owns."""
+        z0, z1, _, _ = self.window()
+        g = self.grid
+        off = g.comp_offsets() + [g.n_dofs()]
+        m = np.zeros(self.n, bool)
+        for k in range(4):
+            ps = (g.dims[0] + (k == 0)) * (g.dims[1] + (k == 1))
+            top = z1 + (1 if (k == 2 and self.rank == self.nranks - 1) else 0)
+            m[off[k] + z0 * ps:off[k] + top * ps] = True
+        return m
+
+    def precondition(self, r):
+        r = np.ascontiguousarray(r, np.complex128)
+        z = np.zeros(self.n, np.complex128)
+        _check(lib().ehmg_dist_precondition(self._h, r.ctypes.data, z.ctypes.data))
+        return z
+
+    def solve(self, b, opt: "KrylovOptions" = None):
+        opt = opt or KrylovOptions()
+        b = np.ascontiguousarray(b, np.complex128)
+        x = np.zeros(self.n, np.complex128)
+        ko = _KOpts(opt.restart, opt.max_iterations, opt.rtol, opt.stall_factor, opt.stall_cycles)
+        kr = _KRes()
+        cap = opt.max_iterations + opt.max_iterations // max(1, opt.restart) + 8
+        hist = np.zeros(cap, np.float64)
+        _check(lib().ehmg_dist_solve(self._h, b.ctypes.data, x.ctypes.data, C.byref(ko),
+                                     C.byref(kr), hist.ctypes.data, cap))
+        return x, KrylovResult(_STATUS[kr.status], kr.iterations, kr.relres,
+                               list(hist[:min(kr.n_history, cap)]))
 
 
 # ----------------------------------------------------------------- Krylov
