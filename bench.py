@@ -116,7 +116,10 @@ def dist_init(args):
     if ws > 1:
         import torch
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "b200" else "gloo"
+        ndev = torch.cuda.device_count() if args.impl == "b200" else 0
+        # NCCL needs distinct GPUs; several ranks sharing one GPU (smoke runs
+        # of the multi-rank path) fall back to gloo for the bench plumbing.
+        backend = "nccl" if ndev >= ws else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
@@ -387,6 +390,73 @@ def run_b200(args, ws, rank, local):
     return line
 
 
+def run_b200_slabs(args, ws, rank, local):
+    """N > 1: one z-slab per GPU (strong scaling of one V-cycle over the
+    fixed 257^3 problem). Ghost planes move by CUDA-IPC peer copies over
+    NVLink; levels <= 64^3 are agglomerated (replicated on every rank)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2307_03242_b200 as E
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    E.lib().ehmg_set_device(dev)
+    obj = [f"bench{os.getpid()}_{int(time.time() * 1e3) % 10**9}" if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    job = obj[0]
+    n = args.n
+    g, med, omega = build_problem(n, E)
+    opt = E.MgOptions(n_levels=LEVELS, cycle="v", nu1=2, nu2=2, damping=DAMPING,
+                      vanka_mode="full", sweep="red_black")
+    t0 = time.perf_counter()
+    d = E.DistributedSlabSolver(job, rank, ws, dev, g, med, E.OperatorParams(BETA, omega, ALPHA),
+                                opt, agg_n2=64)
+    setup_s = time.perf_counter() - t0
+    rng = np.random.default_rng(1234)
+    N = g.n_dofs()
+    r = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    d.time_precondition(r, args.warmup)
+    barrier(ws)
+    clk = ClockSampler(dev)
+    clk.start()
+    b0 = d.exchanged_bytes()
+    ms = d.time_precondition(r, args.steps)
+    halo = (d.exchanged_bytes() - b0) / args.steps
+    clocks = clk.stop()
+    ms_max = max_over_ranks(ws, ms)
+    value = args.steps / (ms_max / 1e3)
+    barrier(ws)
+    e_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        d.precondition(r)
+    e2e_ms = max_over_ranks(ws, (time.perf_counter() - t0) * 1e3)
+    z0, z1, w0, w1 = d.window()
+    solve = None
+    if args.solve:
+        b = E.make_point_source(g, 0, (n // 2, n // 2, n // 2))
+        t0 = time.perf_counter()
+        _, res = d.solve(b, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+        ts = max_over_ranks(ws, time.perf_counter() - t0)
+        solve = {"status": res.status, "iterations": res.iterations, "relres": res.relres,
+                 "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5)}
+    d.close()
+    cfg = workload_config(n)
+    cfg["parallelism"] = f"z-slab x{ws} (levels <= 64^3 agglomerated)"
+    return {
+        "metric": metric_name(), "value": round(value, 4), "unit": "V-cycles/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "complex128 (f64)", "data": "synthetic (BASELINE configs[2] media recipe)",
+        "config": cfg,
+        "e2e": {"value": round(e_steps / (e2e_ms / 1e3), 4), "unit": "V-cycles/s",
+                "h2d_bytes_per_step": 16 * N // ws, "d2h_bytes_per_step": 16 * N // ws},
+        "halo_bytes_per_step_rank0": int(halo), "slab_rank0": [z0, z1, w0, w1],
+        "gmres_time_to_1e-6": solve, "setup_s": round(setup_s, 2), "clocks": clocks,
+        "gpu_launches": None,
+    }
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
@@ -415,14 +485,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--n", type=int, default=N_CELLS)
+    ap.add_argument("--cells", dest="n", type=int, default=N_CELLS)
     ap.add_argument("--solve", type=int, default=1)
     ap.add_argument("--max-it", type=int, default=600)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs",
+                    help="N > 1: z-slab decomposition (strong) or independent replicas (weak)")
     args = ap.parse_args()
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         line = run_reference(args, ws, rank)
+    elif ws > 1 and args.mode == "slabs":
+        line = run_b200_slabs(args, ws, rank, local)
     else:
         line = run_b200(args, ws, rank, local)
     if rank == 0 and line is not None:

@@ -143,6 +143,9 @@ int ehmg_dist_create(const char* job, int rank, int nranks, int device, int ndim
 int ehmg_dist_destroy(ehmg_dist d);
 int ehmg_dist_window(ehmg_dist d, int* z0, int* z1, int* w0, int* w1);
 int ehmg_dist_precondition(ehmg_dist d, const double* r, double* z);
+/* bench helper: CUDA-event ms of `count` applications on the resident window */
+int ehmg_dist_time_precondition(ehmg_dist d, const double* r, int count, double* ms);
+int64_t ehmg_dist_exchanged_bytes(ehmg_dist d);
 
 /* Per-launch CUDA-event profiling of the cycle kernels (bench roofline).
  * report: one "kernel level count total_ms" line per (kernel, level). */

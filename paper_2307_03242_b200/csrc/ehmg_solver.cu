@@ -1162,6 +1162,35 @@ int ehmg_dist_precondition(ehmg_dist d, const double* r, double* z) {
   });
 }
 
+// CUDA-event time of `count` distributed preconditioner applications on the
+// resident level-0 window (exchanges and barriers included).
+int ehmg_dist_time_precondition(ehmg_dist d, const double* r, int count, double* ms) {
+  return guard([&] {
+    ehmg_slab_mg_s& mg = *d->mg;
+    const int q = d->comm.rank;
+    std::vector<cplx*> B(mg.P_(), nullptr), X(mg.P_(), nullptr);
+    B[q] = mg.bw[0]->p;
+    X[q] = mg.xw[0]->p;
+    d->load_window(r, B[q]);
+    CK(cudaStreamSynchronize(mg.s));
+    d->comm.barrier();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, mg.s));
+    for (int i = 0; i < count; ++i) mg.precondition_windows(B, X);
+    CK(cudaEventRecord(b, mg.s));
+    CK(cudaEventSynchronize(b));
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, a, b));
+    *ms = f;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+int64_t ehmg_dist_exchanged_bytes(ehmg_dist d) { return d ? d->mg->exchanged_bytes : -1; }
+
 int ehmg_dist_solve(ehmg_dist d, const double* b, double* x, const ehmg_krylov_options* opt,
                     ehmg_krylov_result* res, double* history, int history_cap) {
   return guard([&] {

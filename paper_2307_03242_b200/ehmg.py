@@ -119,6 +119,9 @@ def lib():
         L.ehmg_dist_destroy.argtypes = [vp]
         L.ehmg_dist_window.argtypes = [vp, ip, ip, ip, ip]
         L.ehmg_dist_precondition.argtypes = [vp, vp, vp]
+        L.ehmg_dist_time_precondition.argtypes = [vp, vp, C.c_int, dp]
+        L.ehmg_dist_exchanged_bytes.argtypes = [vp]
+        L.ehmg_dist_exchanged_bytes.restype = i64
         L.ehmg_dist_solve.argtypes = [vp, vp, vp, C.POINTER(_KOpts), C.POINTER(_KRes), vp,
                                       C.c_int]
         L.ehmg_profile_enable.argtypes = [C.c_int]
@@ -706,6 +709,16 @@ class DistributedSlabSolver:
         z = np.zeros(self.n, np.complex128)
         _check(lib().ehmg_dist_precondition(self._h, r.ctypes.data, z.ctypes.data))
         return z
+
+    def time_precondition(self, r, count: int) -> float:
+        """CUDA-event ms of `count` applications on the resident window."""
+        r = np.ascontiguousarray(r, np.complex128)
+        ms = C.c_double(0)
+        _check(lib().ehmg_dist_time_precondition(self._h, r.ctypes.data, count, C.byref(ms)))
+        return ms.value
+
+    def exchanged_bytes(self) -> int:
+        return int(lib().ehmg_dist_exchanged_bytes(self._h))
 
     def solve(self, b, opt: "KrylovOptions" = None):
         opt = opt or KrylovOptions()
