@@ -732,6 +732,94 @@ __global__ void __launch_bounds__(kThreads) k_reduce(int mode, int64_t n, const 
   }
 }
 
+// Pipelined modified Gram-Schmidt pass (krylov.hpp:115-119 fused across two
+// MGS steps): optionally w += a*xa with a = *ap (the previous projection),
+// then accumulate |w|^2 (want_norm) and <y, w> (y != null) over the updated w.
+// Per element the arithmetic equals the separate axpy-then-dot passes; the
+// reduction tree is the deterministic one of k_reduce. Results: out_norm[0],
+// out_dot[0..1]; coef[0..1] = -<y,w> for the next pass.
+__global__ void __launch_bounds__(kThreads) k_mgs(int64_t n, const double* __restrict__ ap,
+                                                  const cplx* __restrict__ xa, cplx* __restrict__ w,
+                                                  const cplx* __restrict__ y, int want_norm,
+                                                  double* __restrict__ partial, unsigned* __restrict__ counter,
+                                                  double* __restrict__ out_norm, double* __restrict__ out_dot,
+                                                  double* __restrict__ coef) {
+  const cplx a = xa ? mk(ap[0], ap[1]) : mk(0, 0);
+  double sn = 0, sr = 0, si = 0;
+  GRID_STRIDE(i, n) {
+    cplx v = w[i];
+    if (xa) {
+      v += a * xa[i];
+      w[i] = v;
+    }
+    if (want_norm) sn += v.x * v.x + v.y * v.y;
+    if (y) {
+      const cplx q = y[i];
+      sr += q.x * v.x + q.y * v.y;
+      si += q.x * v.y - q.y * v.x;
+    }
+  }
+  __shared__ double sh[3][kThreads / 32];
+  __shared__ bool last;
+  sn = warp_sum(sn);
+  sr = warp_sum(sr);
+  si = warp_sum(si);
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x / 32] = sn;
+    sh[1][threadIdx.x / 32] = sr;
+    sh[2][threadIdx.x / 32] = si;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0, t1 = 0, t2 = 0;
+    for (int q = 0; q < kThreads / 32; ++q) {
+      t0 += sh[0][q];
+      t1 += sh[1][q];
+      t2 += sh[2][q];
+    }
+    partial[3 * blockIdx.x] = t0;
+    partial[3 * blockIdx.x + 1] = t1;
+    partial[3 * blockIdx.x + 2] = t2;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* pp = (const volatile double*)partial;
+    double t0 = 0, t1 = 0, t2 = 0;
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      t0 += pp[3 * q];
+      t1 += pp[3 * q + 1];
+      t2 += pp[3 * q + 2];
+    }
+    if (out_norm) out_norm[0] = t0;
+    if (out_dot) {
+      out_dot[0] = t1;
+      out_dot[1] = t2;
+    }
+    if (coef) {
+      coef[0] = -t1;
+      coef[1] = -t2;
+    }
+    *counter = 0;
+  }
+}
+
+// x += sum_i c_i Z_i (krylov.hpp:176), accumulated in the reference's order.
+struct MultiAxpy {
+  int m;
+  double c[2 * 16];
+  const cplx* z[16];
+};
+__global__ void __launch_bounds__(kThreads) k_multi_axpy(int64_t n, MultiAxpy A, cplx* __restrict__ x) {
+  GRID_STRIDE(i, n) {
+    cplx v = x[i];
+    for (int q = 0; q < A.m; ++q) v += mk(A.c[2 * q], A.c[2 * q + 1]) * A.z[q][i];
+    x[i] = v;
+  }
+}
+
 // y += a x with a = (ar, ai) or, when ap != nullptr, a = *ap (device).
 __global__ void __launch_bounds__(kThreads) k_axpy(int64_t n, double ar, double ai, const double* __restrict__ ap,
                                                    const cplx* __restrict__ x, cplx* __restrict__ y) {

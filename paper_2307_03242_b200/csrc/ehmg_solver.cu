@@ -336,9 +336,11 @@ struct Blas {
   DBuf<double2> partial;
   DBuf<unsigned> counter;
   DBuf<double> scal;  // [0..1] last result, [2..3] coef, [4..] hessenberg column
+  DBuf<double> partial3;
   void init(cudaStream_t s_, int ncol) {
     s = s_;
     partial.alloc(kRedBlocks);
+    partial3.alloc(3 * kRedBlocks);
     counter.alloc(1);
     counter.zero(s);
     scal.alloc(8 + 2 * (ncol + 2));
@@ -473,12 +475,26 @@ struct Fgmres {
       while (j < m && res.iterations < opt.max_iterations) {
         M(V[j]->p, Z[j]->p);
         A(Z[j]->p, w.p);
-        blas.reduce(1, n, w.p, nullptr, blas.wpre(), nullptr, nullptr);
-        for (int i = 0; i <= j; ++i) {
-          blas.reduce(0, n, V[i]->p, w.p, blas.hcol(i), blas.coef(), nullptr);
-          blas.axpy(n, mk(0, 0), blas.coef(), V[i]->p, w.p);
+        if (blas.owned.empty()) {
+          // pipelined MGS: pass i applies the projection on V[i-1] and takes <V[i], w>
+          double* cf[2] = {blas.coef(), blas.res()};
+          for (int i = 0; i <= j + 1; ++i) {
+            k_mgs<<<kRedBlocks, kThreads, 0, s>>>(n, i > 0 ? cf[(i - 1) & 1] : nullptr,
+                                                  i > 0 ? V[i - 1]->p : nullptr, w.p,
+                                                  i <= j ? V[i]->p : nullptr, i == 0 || i == j + 1,
+                                                  blas.partial3.p, blas.counter.p,
+                                                  i == 0 ? blas.wpre() : (i == j + 1 ? blas.wn() : nullptr),
+                                                  i <= j ? blas.hcol(i) : nullptr, i <= j ? cf[i & 1] : nullptr);
+            CK(cudaGetLastError());
+          }
+        } else {
+          blas.reduce(1, n, w.p, nullptr, blas.wpre(), nullptr, nullptr);
+          for (int i = 0; i <= j; ++i) {
+            blas.reduce(0, n, V[i]->p, w.p, blas.hcol(i), blas.coef(), nullptr);
+            blas.axpy(n, mk(0, 0), blas.coef(), V[i]->p, w.p);
+          }
+          blas.reduce(1, n, w.p, nullptr, blas.wn(), nullptr, nullptr);
         }
-        blas.reduce(1, n, w.p, nullptr, blas.wn(), nullptr, nullptr);
         CK(cudaMemcpyAsync(hbuf.data(), blas.scal.p, sizeof(double) * (8 + 2 * (j + 1)),
                            cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -540,7 +556,19 @@ struct Fgmres {
         }
         y[i] = cdiv(v, HH(i, i));
       }
-      for (int i = 0; i < j; ++i) blas.axpy(n, y[i], nullptr, Z[i]->p, x);
+      if (j <= 16) {
+        MultiAxpy ma;
+        ma.m = j;
+        for (int i = 0; i < j; ++i) {
+          ma.c[2 * i] = y[i].x;
+          ma.c[2 * i + 1] = y[i].y;
+          ma.z[i] = Z[i]->p;
+        }
+        k_multi_axpy<<<grid_for(n, 148 * 16), kThreads, 0, s>>>(n, ma, x);
+        CK(cudaGetLastError());
+      } else {
+        for (int i = 0; i < j; ++i) blas.axpy(n, y[i], nullptr, Z[i]->p, x);
+      }
       A(x, w.p);
       blas.sub(n, b, w.p, r.p);
       beta = blas.norm_host(n, r.p);
