@@ -179,20 +179,20 @@ struct ehmg_slab_mg_s {
     }
   }
 
-  void sweep_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X) {
+  void sweep_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool xzero = false) {
     for (int color = 0; color < 2; ++color) {
       for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& sl = *L[l][q];
-        sl.sm.colour_phase(sl.sg.g, P, sl.media.ref(), B[q], X[q], opt.damping, color, s);
+        sl.sm.colour_phase(sl.sg.g, P, sl.media.ref(), B[q], X[q], opt.damping, color, s, xzero && color == 0);
       }
       exchange(l, X);
     }
   }
 
   // multigrid.hpp:217 cycle_at on the distributed levels (B ghosts valid)
-  void cycle(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X) {
+  void cycle(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool xzero = false) {
     const int La = plan.La, nl = plan.nl;
-    for (int q = 0; q < opt.nu1; ++q) sweep_all(l, B, X);
+    for (int q = 0; q < opt.nu1; ++q) sweep_all(l, B, X, xzero && q == 0);
     for (int q = q_lo; q < q_hi; ++q) {
       SlabLevel& sl = *L[l][q];
       launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], sl.r.p, s);
@@ -210,7 +210,7 @@ struct ehmg_slab_mg_s {
         EC[q] = c.ec.p;
       }
       exchange(l + 1, BC);
-      for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC);
+      for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC, r == 0);
       for (int q = q_lo; q < q_hi; ++q)
         launch_transfer(L[l][q]->sg.g, L[l + 1][q]->sg.g, false, L[l + 1][q]->ec.p, X[q], true, s);
     } else {
@@ -233,7 +233,7 @@ struct ehmg_slab_mg_s {
       sync_barrier();  // the full coarse rhs is assembled on every rank
       CK(cudaMemsetAsync(erep.p, 0, sizeof(cplx) * gc.ndofs, s));
       CK(cudaStreamSynchronize(s));
-      for (int r = 0; r < repeat; ++r) rep->cycle_at(0, brep.p, erep.p);
+      for (int r = 0; r < repeat; ++r) rep->cycle_at(0, brep.p, erep.p, r == 0);
       CK(cudaStreamSynchronize(rep->s));
       for (int q = q_lo; q < q_hi; ++q) launch_transfer(L[l][q]->sg.g, gc, false, erep.p, X[q], true, s);
     }
@@ -245,7 +245,7 @@ struct ehmg_slab_mg_s {
     exchange(0, B);
     for (int q = q_lo; q < q_hi; ++q)
       CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
-    cycle(0, B, X);
+    cycle(0, B, X, true);
   }
 
   // global array <-> level-0 windows of the local slabs
@@ -282,7 +282,7 @@ struct ehmg_slab_mg_s {
     scatter(r, B);
     for (int q = q_lo; q < q_hi; ++q)
       CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
-    cycle(0, B, X);
+    cycle(0, B, X, true);
     gather(X, z);
     CK(cudaStreamSynchronize(s));
   }

@@ -304,8 +304,10 @@ struct Smoother {
     else k_vanka_expand<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, out);
     CK(cudaGetLastError());
   }
+  // xzero: x is zero on entry, so the first colour's residual is b itself
+  // (b - H*0 == b exactly) and its operator apply is skipped.
   void sweep(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
-             int order, cudaStream_t s) {
+             int order, cudaStream_t s, bool xzero = false) {
     const Cell* m = mr.packed;
     if (order == 0) {
       if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
@@ -313,19 +315,20 @@ struct Smoother {
       CK(cudaGetLastError());
       return;
     }
-    for (int color = 0; color < 2; ++color) colour_phase(g, P, mr, b, x, w, color, s);
+    for (int color = 0; color < 2; ++color) colour_phase(g, P, mr, b, x, w, color, s, xzero && color == 0);
   }
   // One red-black colour (global parity `color`; windows shift the local parity).
   void colour_phase(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
-                    int color, cudaStream_t s) {
+                    int color, cudaStream_t s, bool xzero = false) {
     const int64_t nt = colour_threads(g);
     const int lc = color ^ (g.zoff & 1);
-    launch_residual(g, P, mr, x, b, res.p, s);
+    const cplx* r = xzero ? b : res.p;
+    if (!xzero) launch_residual(g, P, mr, x, b, res.p, s);
     Prof pf("vanka_update", s);
     if (g.nd == 3)
-      k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, res.p, lc, w, x);
+      k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, r, lc, w, x);
     else
-      k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, res.p, lc, w, x);
+      k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, r, lc, w, x);
     CK(cudaGetLastError());
   }
 };
@@ -640,15 +643,16 @@ struct ehmg_mg_s {
     if (s) cudaStreamDestroy(s);
   }
 
-  void cycle_at(int l, const cplx* b, cplx* x);
+  // xzero: x is known to be zero on entry (precondition, coarse corrections)
+  void cycle_at(int l, const cplx* b, cplx* x, bool xzero = false);
   void precondition(const cplx* r, cplx* z) {
     CK(cudaMemsetAsync(z, 0, sizeof(cplx) * L[0]->g.ndofs, s));
-    cycle_at(0, r, z);
+    cycle_at(0, r, z, true);
   }
 };
 
 // multigrid.hpp:217 cycle_at
-void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
+void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x, bool xzero) {
   const int nl = (int)L.size();
   g_level = l;
   if (l + 1 == nl) {
@@ -659,7 +663,8 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
   }
   Level& lev = *L[l];
   Level& nxt = *L[l + 1];
-  for (int q = 0; q < opt.nu1; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s);
+  for (int q = 0; q < opt.nu1; ++q)
+    lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s, xzero && q == 0);
   launch_residual(lev.g, lev.P, lev.media.ref(), x, b, lev.r.p, s);
   launch_transfer(lev.g, nxt.g, true, lev.r.p, nxt.bc.p, false, s);
   CK(cudaMemsetAsync(nxt.ec.p, 0, sizeof(cplx) * nxt.g.ndofs, s));
@@ -667,15 +672,15 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
   switch (opt.cycle) {
     case 0:
     case 1:
-      cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      cycle_at(l + 1, nxt.bc.p, nxt.ec.p, true);
       break;
     case 2:
-      cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      cycle_at(l + 1, nxt.bc.p, nxt.ec.p, true);
       if (!next_coarsest) cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
       break;
     default:
       if (next_coarsest) {
-        cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+        cycle_at(l + 1, nxt.bc.p, nxt.ec.p, true);
       } else {
         ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol,
                                0.99, 2};
@@ -686,7 +691,7 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x) {
         };
         Fgmres::Fn M = [&](const cplx* in, cplx* out) {
           CK(cudaMemsetAsync(out, 0, sizeof(cplx) * nxt.g.ndofs, s));
-          cycle_at(l + 1, in, out);
+          cycle_at(l + 1, in, out, true);
         };
         nxt.inner.run(A, M, nxt.bc.p, nxt.ec.p, ko, hist);
       }

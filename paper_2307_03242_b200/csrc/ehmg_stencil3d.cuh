@@ -119,6 +119,7 @@ __device__ __forceinline__ double s3_inv(int c) {  // 1/c for c in {0,1,2}
 }
 
 // ----------------------------------------------------------------- kernel
+// 11 warps = 3 per SM sub-partition: 16K registers / 96 threads caps this at 168
 __global__ void __launch_bounds__(S3_THREADS, 1)
     k_stencil3d(const __grid_constant__ S3Maps maps, const S3Params P, const cplx* __restrict__ b,
                 cplx* __restrict__ y) {
