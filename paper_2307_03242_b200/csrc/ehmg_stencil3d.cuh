@@ -4,8 +4,8 @@
 // operator (operator.hpp:389-421), all four components in one launch.
 //
 // Design (B200, complex128, HBM-bound):
-//  * 2.5D tiling. A CTA owns a 32x8 tile of the (i,j) index plane plus a
-//    one-cell flux halo (34x10 = 340 positions, one thread each, 11 warps)
+//  * 2.5D tiling. A CTA owns a 33x8 tile of the (i,j) index plane plus a
+//    one-cell flux halo (35x10 = 350 positions, one thread each, 11 warps)
 //    and marches a z-chunk (persistent CTAs stride over tile x chunk items).
 //  * TMA. u0,u1,u2 (planes z, z+1), p (z-1, z) and the SoA cell media
 //    (z-1..z+1) sit in shared-memory rings filled by cp.async.bulk.tensor
@@ -35,12 +35,20 @@
 
 namespace ehmg {
 
-constexpr int S3_TX = 32, S3_TY = 8;
+// 33 columns: the n0+1 u0 faces of a power-of-two level (257, 129, 65, 33)
+// split into whole tiles with no one-column remainder tile.
+constexpr int S3_TX = 33, S3_TY = 8;
 constexpr int S3_UX = S3_TX + 4, S3_UY = S3_TY + 4, S3_UN = S3_UX * S3_UY;  // origin (i0-2, j0-2)
+constexpr int S3_US = (S3_UN + 15) / 16 * 16;  // ring-slot stride: TMA destinations stay 128-byte aligned
+// media boxes: TMA inner box extents and start offsets are 16-byte multiples,
+// so the float64 media planes start at an even column and use an even pitch
+// (UX + 1 columns: one spare column on the left or the right of the tile)
+constexpr int S3_MX = (S3_UX + 1) / 2 * 2, S3_MN = S3_MX * S3_UY, S3_MS = (S3_MN + 15) / 16 * 16;
+static_assert(S3_MX >= S3_UX + 1, "media pitch needs the spare column");
 constexpr int S3_FX = S3_TX + 2, S3_FY = S3_TY + 2, S3_FN = S3_FX * S3_FY;  // origin (i0-1, j0-1)
 constexpr int S3_THREADS = ((S3_FN + 31) / 32) * 32;                         // 352
 constexpr int S3_ZCHUNK = 32;
-constexpr unsigned S3_CBYTES = S3_UN * 16, S3_DBYTES = S3_UN * 8;  // one complex / double box
+constexpr unsigned S3_CBYTES = S3_UN * 16, S3_DBYTES = S3_MN * 8;  // one complex / double box
 
 struct S3Params {
   Geo g;
@@ -56,9 +64,9 @@ struct S3Maps {
 };
 
 struct __align__(128) S3Smem {
-  cplx u[3][3][S3_UN];  // [plane % 3][component]
-  cplx p[3][S3_UN];     // [plane % 3]
-  double mu[4][S3_UN], rho[4][S3_UN], gam[4][S3_UN], ilm[4][S3_UN];  // [plane % 4]
+  cplx u[3][3][S3_US];  // [plane % 3][component]
+  cplx p[3][S3_US];     // [plane % 3]
+  double mu[4][S3_MS], rho[4][S3_MS], gam[4][S3_MS], ilm[4][S3_MS];  // [plane % 4], pitch S3_MX
   cplx f[6][S3_FN];     // z-family fluxes at plane z: F00 F11 F01 F10 F20 F21
   cplx di[3][S3_FN];    // in-plane difference fields: d22 (cell z), d02, d12 (edge z+1)
   cplx q[2][3][S3_FN];  // mass products md*u [plane & 1][component]
@@ -106,10 +114,11 @@ __device__ __forceinline__ void s3_issue(S3Smem& S, const S3Maps& M, int i0, int
   }
   for (int q = 0; q < nm; ++q) {
     const int sl = zm[q] & 3;
-    s3_tma(S.mu[sl], &M.mu, i0 - 2, cy, zm[q], bar);
-    s3_tma(S.rho[sl], &M.rho, i0 - 2, cy, zm[q], bar);
-    s3_tma(S.gam[sl], &M.gam, i0 - 2, cy, zm[q], bar);
-    s3_tma(S.ilm[sl], &M.ilm, i0 - 2, cy, zm[q], bar);
+    const int mx = (i0 - 2) & ~1;
+    s3_tma(S.mu[sl], &M.mu, mx, cy, zm[q], bar);
+    s3_tma(S.rho[sl], &M.rho, mx, cy, zm[q], bar);
+    s3_tma(S.gam[sl], &M.gam, mx, cy, zm[q], bar);
+    s3_tma(S.ilm[sl], &M.ilm, mx, cy, zm[q], bar);
   }
   for (int q = 0; q < np; ++q) s3_tma(S.p[s3_mod3(zp[q])], &M.p, cx, cy, zp[q], bar);
 }
@@ -152,6 +161,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
     const int zend = (chunk + 1 == P.nchunks) ? n2 + 1 : (int)(((int64_t)(chunk + 1) * n2) / P.nchunks);
 
     // ---- per-item constants of this thread's position
+    // media boxes start at an even column (16-byte aligned TMA start): i0-2 or i0-3
+    const int um = (fx + 1 + (i0 & 1)) + S3_MX * (fy + 1);  // own media-local index
     const int xg = i0 - 1 + fx, yg = j0 - 1 + fy;
     const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
     const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
@@ -221,8 +232,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
         // Every shared-memory value this position needs is loaded once into
         // registers (grouped per component to bound register pressure).
         const double al = P.alpha, w2 = P.omega2;
-        const double mc00 = MUc[ui], mc_l = MUc[ui - 1], mc_b = MUc[ui - S3_UX], mc_lb = MUc[ui - 1 - S3_UX];
-        const double mm00 = MUm[ui], mm_l = MUm[ui - 1], mm_b = MUm[ui - S3_UX];
+        const double mc00 = MUc[um], mc_l = MUc[um - 1], mc_b = MUc[um - S3_MX], mc_lb = MUc[um - 1 - S3_MX];
+        const double mm00 = MUm[um], mm_l = MUm[um - 1], mm_b = MUm[um - S3_MX];
         // mu on the edges (operator.hpp:108 order: first axis outer, second inner)
         const double mu01 = (mc_lb + mc_l + mc_b + mc00) * mu01s;
         const double mu02 = (mm_l + mc_l + mm00 + mc00) * (ix * izc);
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
         const double* RHp = S.rho[(z + 1) & 3];
         const double* GAc = S.gam[z & 3];
         const double* GAp = S.gam[(z + 1) & 3];
-        const double rp00 = RHp[ui], gp00 = GAp[ui];
+        const double rp00 = RHp[um], gp00 = GAp[um];
         auto md = [&](double sr, double sg, double ic) {
           const double rho_f = sr * ic, gam_f = sg * ic + al;
           return mk(w2 * rho_f, -w2 * gam_f * rho_f);
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
           r01m = r01c;
           r01c = rn1;
           S.di[1][t] = v00 - u00;  // d02 at edge (q, z+1)
-          S.q[qb][0][t] = (zin && q0ok) ? md(RHp[ui - 1] + rp00, GAp[ui - 1] + gp00, ix) * v00 : mk(0, 0);
+          S.q[qb][0][t] = (zin && q0ok) ? md(RHp[um - 1] + rp00, GAp[um - 1] + gp00, ix) * v00 : mk(0, 0);
         }
         // ---- component 1: F11 (cell, +y pair, in-plane x), F10 (edge01, -x pair, in-plane y)
         {
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
           r10c = rn1;
           S.di[2][t] = v00 - u00;  // d12 at edge (q, z+1)
           S.q[qb][1][t] =
-              (zin && q1ok) ? md(RHp[ui - S3_UX] + rp00, GAp[ui - S3_UX] + gp00, iy) * v00 : mk(0, 0);
+              (zin && q1ok) ? md(RHp[um - S3_MX] + rp00, GAp[um - S3_MX] + gp00, iy) * v00 : mk(0, 0);
         }
         // ---- component 2: F20 (edge02, -x pair, in-plane y), F21 (edge12, -y pair, in-plane x)
         {
@@ -297,7 +308,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
           r21c = rn1;
           S.di[0][t] = v00 - u00;  // d22 at cell (q, z)
           S.q[qb][2][t] = (zg + 1 >= 0 && zg + 1 <= n2g && q2ok)
-                              ? md(RHc[ui] + rp00, GAc[ui] + gp00, izp) * v00
+                              ? md(RHc[um] + rp00, GAc[um] + gp00, izp) * v00
                               : mk(0, 0);
         }
       }
@@ -319,10 +330,10 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
           return a + c + 2.0 * m_;
         };
         const cplx d22 = (beta * S.di[0][t] + w * filt(S.di[0])) * c22;
-        const cplx f22 = MUc[ui] * d22;  // zero-filled mu masks cells outside the box
-        const double mu02p = (MUc[ui - 1] + MUp[ui - 1] + MUc[ui] + MUp[ui]) * (ix * izp);
+        const cplx f22 = MUc[um] * d22;  // zero-filled mu masks cells outside the box
+        const double mu02p = (MUc[um - 1] + MUp[um - 1] + MUc[um] + MUp[um]) * (ix * izp);
         const cplx f02p = mu02p * ((beta * S.di[1][t] + w * filt(S.di[1])) * c02);
-        const double mu12p = (MUc[ui - S3_UX] + MUp[ui - S3_UX] + MUc[ui] + MUp[ui]) * (iy * izp);
+        const double mu12p = (MUc[um - S3_MX] + MUp[um - S3_MX] + MUc[um] + MUp[um]) * (iy * izp);
         const cplx f12p = mu12p * ((beta * S.di[2][t] + w * filt(S.di[2])) * c12);
         const cplx(*Q)[S3_FN] = S.q[z & 1];
         const cplx qc0 = Q[0][t], qc1 = Q[1][t], qc2 = Q[2][t];
@@ -370,7 +381,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             cplx out = d00;
             out += d11;
             out += d22;
-            out += S.ilm[z & 3][ui] * pc;
+            out += S.ilm[z & 3][um] * pc;
             y[o3 + s2 * z] = b ? bb3 - out : out;
           }
         }
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
   }
 }
 
-inline S3Params make_s3params(const Geo& g, const OpPar& P) {
+inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148) {
   S3Params s;
   s.g = g;
   s.beta = P.beta;
@@ -419,14 +430,23 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P) {
   }
   s.ntiles_x = (g.n[0] + 1 + S3_TX - 1) / S3_TX;
   s.ntiles_y = (g.n[1] + 1 + S3_TY - 1) / S3_TY;
-  // z-chunks: ~32 planes on big levels; on small levels split further (down to
-  // 4 planes per chunk) until there are >= 2 items per SM to keep the chip busy.
+  // z-chunks: minimise (rounds of persistent CTAs) x (planes per chunk + 2
+  // warm-up planes) over chunk counts with >= 4 planes per chunk, so that
+  // the tile x chunk items fill whole waves of the 148 SMs.
   const int tiles = s.ntiles_x * s.ntiles_y;
-  int nch = (g.n[2] + S3_ZCHUNK / 2) / S3_ZCHUNK;
-  const int want = (2 * 148 + tiles - 1) / tiles;
-  const int cap = g.n[2] / 4 > 0 ? g.n[2] / 4 : 1;
-  if (nch < want) nch = want < cap ? want : cap;
-  s.nchunks = nch < 1 ? 1 : nch;
+  const int n2 = g.n[2];
+  int best = 1;
+  double best_cost = 1e300;
+  for (int nch = 1; nch <= (n2 / 4 > 0 ? n2 / 4 : 1); ++nch) {
+    const int64_t items = (int64_t)tiles * nch;
+    const int64_t rounds = (items + nsm - 1) / nsm;
+    const double cost = (double)rounds * ((n2 + nch - 1) / nch + 2);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = nch;
+    }
+  }
+  s.nchunks = best;
   return s;
 }
 
@@ -503,10 +523,10 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
       s3_encode(&e.M.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * S3_UX);
     s3_encode(&e.M.p, x + g.off[3], 2 * n0, n1, n2, 2 * S3_UX);
     const int64_t nc = g.ncells;
-    s3_encode(&e.M.mu, media_soa + 0 * nc, n0, n1, n2, S3_UX);
-    s3_encode(&e.M.rho, media_soa + 1 * nc, n0, n1, n2, S3_UX);
-    s3_encode(&e.M.gam, media_soa + 2 * nc, n0, n1, n2, S3_UX);
-    s3_encode(&e.M.ilm, media_soa + 3 * nc, n0, n1, n2, S3_UX);
+    s3_encode(&e.M.mu, media_soa + 0 * nc, n0, n1, n2, S3_MX);
+    s3_encode(&e.M.rho, media_soa + 1 * nc, n0, n1, n2, S3_MX);
+    s3_encode(&e.M.gam, media_soa + 2 * nc, n0, n1, n2, S3_MX);
+    s3_encode(&e.M.ilm, media_soa + 3 * nc, n0, n1, n2, S3_MX);
     if (cache.size() < 256) {
       cache.push_back(e);
       Mp = &cache.back().M;
@@ -517,7 +537,7 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
     }
   }
   const S3Maps M = *Mp;
-  const S3Params sp = make_s3params(g, P);
+  const S3Params sp = make_s3params(g, P, nsm);
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
   k_stencil3d<<<grid, S3_THREADS, smem, s>>>(M, sp, b, y);
