@@ -1,0 +1,66 @@
+"""A/B timing of the 3D operator apply across library builds.
+
+    python tools/ab_stencil.py LIB.so [LIB2.so ...] [--n 256] [--reps 20]
+
+Each library is loaded through ctypes, an operator is built at n^3 with the
+bench media, and `reps` applies on resident device buffers are timed with CUDA
+events on the operator's stream (development tool; not part of the product).
+"""
+import argparse
+import ctypes as C
+import math
+import sys
+
+import numpy as np
+import torch
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("libs", nargs="+")
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    n = a.n
+    nc = n ** 3
+    lam = np.full(nc, 2.0)
+    mu = np.ones(nc)
+    rho = np.ones(nc)
+    gam = np.full(nc, 0.01)
+    dims = (C.c_int * 3)(n, n, n)
+    dp = lambda v: v.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    for path in a.libs:
+        L = C.CDLL(path)
+        L.ehmg_op_n_dofs.restype = C.c_int64
+        L.ehmg_op_stream.restype = C.c_uint64
+        op = C.c_void_p()
+        rc = L.ehmg_op_create(3, dims, C.c_double(1.0 / n), dp(lam), dp(mu), dp(rho), dp(gam),
+                              C.c_double(2 / 3), C.c_double(2 * math.pi * n / 10), C.c_double(0.5),
+                              C.byref(op))
+        assert rc == 0, rc
+        N = L.ehmg_op_n_dofs(op)
+        torch.manual_seed(0)
+        x = torch.randn(N, dtype=torch.complex128, device="cuda")
+        y = torch.empty_like(x)
+        st = torch.cuda.ExternalStream(L.ehmg_op_stream(op))
+        L.ehmg_last_error.restype = C.c_char_p
+        for _ in range(3):
+            rc = L.ehmg_apply_mixed_operator(op, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1)
+            if rc:
+                print(path, "apply failed:", L.ehmg_last_error().decode())
+                break
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(a.reps):
+            L.ehmg_apply_mixed_operator(op, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        print(f"{path}: {ms:.4f} ms/apply  {N / ms / 1e6:.2f} GDOF/s  checksum {float(y.abs().sum()):.10e}")
+        L.ehmg_op_destroy(op)
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()
