@@ -79,6 +79,12 @@ int ehmg_coarsen_media(int ndim, const int* dims_fine, const double* fine, doubl
 int ehmg_attenuation_profile(int ndim, const int* dims, double gamma_phys, int layer_width,
                              double gamma_max, int absorb_top, double* out);
 
+/* experiments.hpp:78 layered_media: seeded horizontal layers (5..10 layers,
+ * per-layer vs, rho and lambda/mu ratio; same <random> engines and draw order
+ * as the reference). Outputs are cell-sized host arrays; gamma = gamma_phys. */
+int ehmg_layered_media(int ndim, const int* dims, double gamma_phys, uint64_t seed, double* lambda,
+                       double* mu, double* rho, double* gamma);
+
 /* ---- multigrid: multigrid.hpp:34 MgOptions, :75 Multigrid, :133 cycle,
  *      :136 precondition --------------------------------------------------
  * cycle: 0 two_grid, 1 v, 2 w, 3 k. coarse: the coarsest level is solved

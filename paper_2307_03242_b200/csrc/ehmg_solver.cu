@@ -15,7 +15,9 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <cmath>
+#include <random>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -975,6 +977,47 @@ int ehmg_coarsen_media(int nd, const int* dims_f, const double* fine, double* co
 }
 
 // media.hpp:95 (host-side media preparation; not on the per-cycle path)
+// experiments.hpp:78 layered_media: the same std::mt19937_64 stream and the
+// same <random> distributions, drawn in the reference's order, so one seed
+// gives the reference's layers bit for bit (same C++ standard library).
+int ehmg_layered_media(int nd, const int* dims, double gamma_phys, uint64_t seed, double* lambda,
+                       double* mu, double* rho, double* gamma) {
+  return guard([&] {
+    if (nd != 2 && nd != 3) throw Err(EHMG_EINVAL, "layered_media: ndim must be 2 or 3");
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    for (int a = 0; a < nd; ++a)
+      if (d[a] < 1) throw Err(EHMG_EINVAL, "layered_media: dims must be positive");
+    std::mt19937_64 rng(seed);
+    const int depth_n = d[nd - 1];
+    const int nl = std::min(std::uniform_int_distribution<int>(5, 10)(rng), depth_n);
+    std::vector<int> tops{0};
+    std::uniform_int_distribution<int> depth(1, depth_n - 1);
+    while ((int)tops.size() < nl) {
+      const int t = depth(rng);
+      if (std::find(tops.begin(), tops.end(), t) == tops.end()) tops.push_back(t);
+    }
+    std::sort(tops.begin(), tops.end());
+    std::uniform_real_distribution<double> vs(0.5, 2.0), dens(1.5, 3.0), ratio(2.0, 20.0);
+    std::vector<double> lr, ll, lm;
+    for (int l = 0; l < nl; ++l) {
+      const double v = vs(rng), r = dens(rng), q = ratio(rng);
+      const double m = r * v * v;
+      lr.push_back(r);
+      ll.push_back(q * m);
+      lm.push_back(m);
+    }
+    const int64_t plane = nd == 3 ? (int64_t)d[0] * d[1] : d[0];
+    for (int64_t i = 0; i < plane * depth_n; ++i) {
+      const int z = (int)(i / plane);
+      const int j = (int)(std::upper_bound(tops.begin(), tops.end(), z) - tops.begin()) - 1;
+      rho[i] = lr[j];
+      lambda[i] = ll[j];
+      mu[i] = lm[j];
+      gamma[i] = gamma_phys;
+    }
+  });
+}
+
 int ehmg_attenuation_profile(int nd, const int* dims, double gamma_phys, int L, double gamma_max,
                              int absorb_top, double* out) {
   return guard([&] {

@@ -85,6 +85,7 @@ def lib():
         L.ehmg_restrict_field.argtypes = [C.c_int, ip, vp, vp, C.c_int]
         L.ehmg_prolong_field.argtypes = [C.c_int, ip, vp, vp, C.c_int]
         L.ehmg_coarsen_media.argtypes = [C.c_int, ip, vp, vp]
+        L.ehmg_layered_media.argtypes = [C.c_int, ip, C.c_double, C.c_uint64, vp, vp, vp, vp]
         L.ehmg_attenuation_profile.argtypes = [C.c_int, ip, C.c_double, C.c_int, C.c_double,
                                                C.c_int, vp]
         L.ehmg_multigrid_create.argtypes = [C.c_int, ip, C.c_double, vp, vp, vp, vp, C.c_double,
@@ -786,6 +787,19 @@ def linear_media(g: StaggeredGrid, gamma_phys: float) -> MediaModel:
     return MediaModel(4 + 16 * tt, 1 + 14 * tt, 2 + tt, np.full(n, gamma_phys))
 
 
+def layered_media(g: StaggeredGrid, gamma_phys: float, seed: int) -> MediaModel:
+    """experiments.hpp:78 -- seeded horizontal layers along the last axis
+    (index 0 at the top): 5..10 layers, per-layer shear velocity in [0.5, 2],
+    density in [1.5, 3] and lambda/mu in [2, 20]. Drawn by the library with
+    the reference's std::mt19937_64 stream and <random> distributions."""
+    n = g.n_cells()
+    lam, mu, rho, gam = (np.empty(n, np.float64) for _ in range(4))
+    dims = (C.c_int * 3)(*(list(g.dims) + [1] * (3 - g.ndim)))
+    _check(lib().ehmg_layered_media(g.ndim, dims, float(gamma_phys), int(seed) & (2**64 - 1),
+                                    lam.ctypes.data, mu.ctypes.data, rho.ctypes.data, gam.ctypes.data))
+    return MediaModel(lam, mu, rho, gam)
+
+
 def min_interior_vs(g: StaggeredGrid, m: MediaModel, sponge: SpongeConfig) -> float:
     """experiments.hpp:116"""
     vs = m.vs().reshape(g.dims[::-1])
@@ -816,9 +830,10 @@ def default_solve_damping(g_s: float, levels: int) -> float:
     return 0.25
 
 
-def run_solve(cfg: dict) -> dict:
-    """experiments.hpp:258 run_solve_dim (media: homogeneous / linear or an
-    explicit MediaModel under cfg['media']). Returns the summary dict."""
+def run_solve(cfg: dict, seed: int = 1) -> dict:
+    """experiments.hpp:258 run_solve_dim (media: homogeneous / linear /
+    layered(seed) or an explicit MediaModel under cfg['media']); `seed` is the
+    CLI's --seed (tools/ehmg.cpp:22, default 1). Returns the summary dict."""
     import time
     dims = tuple(cfg.get("dims", (512, 128)))
     g = StaggeredGrid(dims, cfg.get("spacing", 1.0 / dims[-1]))
@@ -834,6 +849,8 @@ def run_solve(cfg: dict) -> dict:
                                            cfg.get("rho", 1.0), gamma_phys)
         elif problem == "linear":
             media = linear_media(g, gamma_phys)
+        elif problem == "layered":
+            media = layered_media(g, gamma_phys, seed)
         else:
             raise ValueError(f"config: unknown problem kind '{problem}'")
     media.gamma = build_attenuation_profile(g, gamma_phys, sponge)

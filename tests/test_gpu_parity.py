@@ -163,6 +163,33 @@ def test_fgmres_iterations_vs_oracle_2d():
     assert np.linalg.norm(r) / np.linalg.norm(b) == pytest.approx(res.relres, rel=1e-6)
 
 
+@pytest.mark.parametrize("dims", [(96, 64), (24, 20, 32)])
+def test_fgmres_layered_media_vs_oracle(dims):
+    """The reference's seeded layered model (experiments.hpp:78, problem
+    'layered'): FGMRES iteration count within +-1 of the oracle."""
+    g = E.StaggeredGrid(dims, 1.0 / dims[-1])
+    L = 8 if len(dims) == 2 else 4
+    sp = E.SpongeConfig(L)
+    med = E.layered_media(g, 0.01, 3)
+    med.gamma = E.build_attenuation_profile(g, 0.01, sp)
+    omega = E.omega_from_gs(g, med, 10.0, sp)
+    src = tuple(d // 2 for d in dims[:-1]) + (2,)
+    b = E.make_point_source(g, len(dims), src)
+    opt = E.MgOptions(n_levels=3, cycle="v", nu1=2, nu2=2, damping=0.35, vanka_mode="full",
+                      sweep="red_black")
+    mg = E.Multigrid(g, med, E.OperatorParams(2 / 3, omega, 0.5), opt)
+    D0 = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.0))
+    x = np.zeros(g.n_dofs(), complex)
+    res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=300))
+    om = O.MG(dims, g.h, O.Media(med.lambda_, med.mu, med.rho, med.gamma), 2 / 3, omega, 0.5,
+              n_levels=3, cycle="v", nu1=2, nu2=2, damping=0.35)
+    xr, info = om.solve(O.Op(dims, g.h, O.Media(med.lambda_, med.mu, med.rho, med.gamma), 2 / 3, omega,
+                             0.0), b, restart=10, max_iterations=300)
+    assert res.status == info["status"]
+    assert abs(res.iterations - info["iterations"]) <= 1
+    assert rel(x, xr) < 1e-5
+
+
 def test_full_size_properties_3d():
     """At the bench size (256^3 cells): linearity of the apply and of one
     V-cycle, and the residual identity r = b - A x, on device buffers."""
