@@ -31,6 +31,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # workload: BASELINE.json configs[2]
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+# kernel from one `ncu --set full` capture of the same residual at 256^3
+# (distinct b and x; profiles/round1/ncu_stencil3d_t33.txt).
+NCU_TRAFFIC = {"residual@L0": 3004467000 + 1062199000,
+               "source": "profiles/round1/ncu_stencil3d_t33.txt (ncu --set full, 256^3 residual)"}
 N_CELLS = 256
 LEVELS = 5
 BETA = 2.0 / 3.0
@@ -376,7 +381,8 @@ def run_b200(args, ws, rank, local):
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": {"bound": "hbm", "kernel": f"{kname}@L{klev}", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None, "alg_bytes_per_launch": nbytes,
+                     "traffic": NCU_TRAFFIC.get(f"{kname}@L{klev}") if n == N_CELLS else None,
+                     "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "clocks": clocks,
     }

@@ -29,10 +29,11 @@ def main():
     N = g.n_dofs()
     r = torch.randn(N, dtype=torch.complex128, device="cuda")
     y = torch.empty_like(r)
+    bvec = torch.randn(N, dtype=torch.complex128, device="cuda")  # distinct b: no L2 reuse of x
     if a.what == "apply":
         D = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.5))
         for _ in range(a.reps):
-            E.residual(D, r, r, y)
+            E.residual(D, bvec, r, y)
     else:
         opt = E.MgOptions(n_levels=5 if n >= 64 else 3, cycle="v", nu1=2, nu2=2, damping=0.25,
                           vanka_mode="full", sweep="red_black")
