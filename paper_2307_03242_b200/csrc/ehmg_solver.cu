@@ -19,6 +19,7 @@
 #include <cmath>
 #include <random>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -640,16 +641,74 @@ struct ehmg_mg_s {
   DBuf<cplx> ainv;  // row-major inverse of the coarsest operator
   int64_t nco = 0;
   DBuf<cplx> hx, hy;
+  // CUDA graphs of whole preconditioner applications, one per (r, z) pair:
+  // a V(2,2) cycle is ~75 launches, many of them short on the coarse levels.
+  struct GraphEntry {
+    const cplx* r;
+    cplx* z;
+    int uses;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
   ~ehmg_mg_s() {
+    for (auto& e : graphs)
+      if (e.exec) cudaGraphExecDestroy(e.exec);
     L.clear();
     if (s) cudaStreamDestroy(s);
   }
 
   // xzero: x is known to be zero on entry (precondition, coarse corrections)
   void cycle_at(int l, const cplx* b, cplx* x, bool xzero = false);
-  void precondition(const cplx* r, cplx* z) {
+  void precondition_direct(const cplx* r, cplx* z) {
     CK(cudaMemsetAsync(z, 0, sizeof(cplx) * L[0]->g.ndofs, s));
     cycle_at(0, r, z, true);
+  }
+  static bool graphs_enabled() {
+    static int on = -1;
+    if (on < 0) {
+      const char* e = getenv("EHMG_GRAPHS");
+      on = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return on == 1;
+  }
+  // The K-cycle's inner Krylov makes host decisions (not capturable); the
+  // per-launch profiler records events between kernels. Both run direct.
+  void precondition(const cplx* r, cplx* z) {
+    if (g_prof || opt.cycle == 3 || !graphs_enabled()) {
+      precondition_direct(r, z);
+      return;
+    }
+    GraphEntry* e = nullptr;
+    for (auto& q : graphs)
+      if (q.r == r && q.z == z) e = &q;
+    if (!e) {
+      if (graphs.size() >= 32) {
+        if (graphs.front().exec) cudaGraphExecDestroy(graphs.front().exec);
+        graphs.erase(graphs.begin());
+      }
+      graphs.push_back({r, z, 0, nullptr});
+      e = &graphs.back();
+    }
+    if (++e->uses == 1) {  // first use runs direct (lazy per-kernel setup happens outside capture)
+      precondition_direct(r, z);
+      return;
+    }
+    if (!e->exec) {
+      cudaGraph_t gph;
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        precondition_direct(r, z);
+      } catch (...) {
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(s, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        throw;
+      }
+      CK(cudaStreamEndCapture(s, &gph));
+      CK(cudaGraphInstantiate(&e->exec, gph, 0));
+      CK(cudaGraphDestroy(gph));
+    }
+    CK(cudaGraphLaunch(e->exec, s));
   }
 };
 

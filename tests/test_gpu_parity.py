@@ -115,6 +115,10 @@ def test_vcycle_vs_oracle(dims, nl):
     zr = O.MG(dims, h, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.3, n_levels=nl, cycle="v",
               nu1=2, nu2=2, damping=0.35).precondition(b)
     assert rel(z, zr) < CYCLE_TOL
+    # second call captures the cycle into a CUDA graph, third replays it: both
+    # must reproduce the direct launch sequence bit for bit
+    for _ in range(2):
+        assert np.array_equal(mg.precondition(b), z)
 
 
 def test_kcycle_and_wcycle_vs_oracle():
@@ -133,6 +137,8 @@ def test_kcycle_and_wcycle_vs_oracle():
         zr = O.MG(dims, h, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.3, n_levels=3, cycle=cyc,
                   damping=0.55).precondition(b)
         assert rel(z, zr) < (CYCLE_TOL if cyc == "w" else 1e-8)
+        for _ in range(2):  # graph capture / replay (W) and the direct K path
+            assert np.array_equal(mg.precondition(b), z)
 
 
 def test_fgmres_iterations_vs_oracle_2d():
