@@ -58,7 +58,14 @@ def workload_config(n):
             "cycle": "V(2,2) full red-black Vanka", "levels": LEVELS,
             "coarsest": f"{n >> (LEVELS - 1)}^3 exact (LU-derived inverse in HBM)",
             "damping": DAMPING, "source": "unit point source, x-component, centre",
-            "krylov": "FGMRES(10), rtol 1e-6", "l2": "inputs (1.08 GB/field) larger than L2"}
+            "krylov": "FGMRES(10), rtol 1e-6",
+            "l2": (f"inputs ({field_gb(n):.2f} GB/field) larger than the 126 MB L2" if field_gb(n) > 0.126
+                   else f"inputs ({field_gb(n):.3f} GB/field) fit in L2: no flush between steps")}
+
+
+def field_gb(n):
+    """one complex128 field on n^3 cells (u0, u1, u2 faces + p)"""
+    return 16 * (3 * n * n * (n + 1) + n ** 3) / 1e9
 
 
 # ------------------------------------------------------------- clocks
@@ -432,6 +439,12 @@ def run_b200_slabs(args, ws, rank, local):
     ms_max = max_over_ranks(ws, ms)
     value = args.steps / (ms_max / 1e3)
     barrier(ws)
+    # per-launch profile of one application on this rank -> launches per step
+    E.profile_enable(True)
+    d.time_precondition(r, 1)
+    launches_per_step = sum(c for (_, _, c, _) in E.profile_report())
+    E.profile_enable(False)
+    barrier(ws)
     e_steps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
     for _ in range(e_steps):
@@ -459,7 +472,7 @@ def run_b200_slabs(args, ws, rank, local):
                 "h2d_bytes_per_step": 16 * N // ws, "d2h_bytes_per_step": 16 * N // ws},
         "halo_bytes_per_step_rank0": int(halo), "slab_rank0": [z0, z1, w0, w1],
         "gmres_time_to_1e-6": solve, "setup_s": round(setup_s, 2), "clocks": clocks,
-        "gpu_launches": None,
+        "gpu_launches": int(launches_per_step * args.steps),
     }
 
 

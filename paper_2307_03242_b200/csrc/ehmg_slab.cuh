@@ -122,70 +122,132 @@ struct ehmg_slab_mg_s {
   std::vector<std::unique_ptr<DBuf<cplx>>> bw, xw;         // level-0 windows of local slabs
   int64_t exchanged_bytes = 0;
 
+  // Overlap of the smoothing ghost exchanges with the stencil rows that do not
+  // read ghost planes: pushes/pulls run on sx, the interior rows on s.
+  cudaStream_t sx = nullptr;
+  cudaEvent_t ev_upd = nullptr, ev_x = nullptr;
+  std::vector<char> pend;  // per level: the smoothed iterate's ghosts are stale
+
   ~ehmg_slab_mg_s() {
     for (void* p : mapped) cudaIpcCloseMemHandle(p);
     L.clear();
     rep.reset();
+    if (ev_upd) cudaEventDestroy(ev_upd);
+    if (ev_x) cudaEventDestroy(ev_x);
+    if (sx) cudaStreamDestroy(sx);
     if (s) cudaStreamDestroy(s);
   }
 
   int P_() const { return plan.nslabs; }
   bool local(int q) const { return q >= q_lo && q < q_hi; }
 
-  void sync_barrier() {
-    CK(cudaStreamSynchronize(s));
+  void sync_barrier(cudaStream_t st) {
+    CK(cudaStreamSynchronize(st));
     if (comm) comm->barrier();
   }
-  void copy(cplx* dst, const cplx* src, int64_t n) {
+  void sync_barrier() { sync_barrier(s); }
+  void copy(cplx* dst, const cplx* src, int64_t n, cudaStream_t st) {
     if (n <= 0) return;
-    CK(cudaMemcpyAsync(dst, src, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(dst, src, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st));
     exchanged_bytes += (int64_t)sizeof(cplx) * n;
   }
+  void copy(cplx* dst, const cplx* src, int64_t n) { copy(dst, src, n, s); }
   // global planes [a, b) of component k between a window array and an inbox block
-  void to_inbox(cplx* inbox, const SlabGeo& dst, bool above, const cplx* v, const SlabGeo& src, int k) {
+  void to_inbox(cplx* inbox, const SlabGeo& dst, bool above, const cplx* v, const SlabGeo& src, int k,
+                cudaStream_t st) {
     int a, b;
     dst.ghost(k, above, a, b);
     const int64_t ps = slab_plane(src.g, k);
-    copy(inbox + dst.inbox_off(k, above), v + src.g.off[k] + (a - src.g.zoff) * ps, ps * (b - a));
+    copy(inbox + dst.inbox_off(k, above), v + src.g.off[k] + (a - src.g.zoff) * ps, ps * (b - a), st);
   }
-  void from_inbox(cplx* v, const SlabGeo& dst, bool above, const cplx* inbox, int k) {
+  void from_inbox(cplx* v, const SlabGeo& dst, bool above, const cplx* inbox, int k, cudaStream_t st) {
     int a, b;
     dst.ghost(k, above, a, b);
     const int64_t ps = slab_plane(dst.g, k);
-    copy(v + dst.g.off[k] + (a - dst.g.zoff) * ps, inbox + dst.inbox_off(k, above), ps * (b - a));
+    copy(v + dst.g.off[k] + (a - dst.g.zoff) * ps, inbox + dst.inbox_off(k, above), ps * (b - a), st);
   }
 
-  // ghost exchange of one field per local slab (V indexed by slab)
-  void exchange(int l, const std::vector<cplx*>& V) {
-    sync_barrier();  // neighbours finished updating owned planes and reading inboxes
+  // ghost exchange of one field per local slab (V indexed by slab), copies on st
+  void exchange(int l, const std::vector<cplx*>& V, cudaStream_t st) {
+    sync_barrier(st);  // neighbours finished updating owned planes and reading inboxes
     for (int q = q_lo; q < q_hi; ++q) {
       const SlabLevel& me = *L[l][q];
       if (q + 1 < P_()) {
         const SlabLevel& up = *L[l][q + 1];
-        for (int k = 0; k < 4; ++k) to_inbox(up.peer_lo, up.sg, false, V[q], me.sg, k);
+        for (int k = 0; k < 4; ++k) to_inbox(up.peer_lo, up.sg, false, V[q], me.sg, k, st);
       }
       if (q > 0) {
         const SlabLevel& dn = *L[l][q - 1];
-        for (int k = 0; k < 4; ++k) to_inbox(dn.peer_hi, dn.sg, true, V[q], me.sg, k);
+        for (int k = 0; k < 4; ++k) to_inbox(dn.peer_hi, dn.sg, true, V[q], me.sg, k, st);
       }
     }
-    sync_barrier();  // all pushes landed
+    sync_barrier(st);  // all pushes landed
     for (int q = q_lo; q < q_hi; ++q) {
       SlabLevel& me = *L[l][q];
       for (int k = 0; k < 4; ++k) {
-        if (q > 0) from_inbox(V[q], me.sg, false, me.in_lo.p, k);
-        if (q + 1 < P_()) from_inbox(V[q], me.sg, true, me.in_hi.p, k);
+        if (q > 0) from_inbox(V[q], me.sg, false, me.in_lo.p, k, st);
+        if (q + 1 < P_()) from_inbox(V[q], me.sg, true, me.in_hi.p, k, st);
       }
     }
+  }
+  void exchange(int l, const std::vector<cplx*>& V) { exchange(l, V, s); }
+
+  // Output planes of slab q (window-local, [a, b)) whose rows read no ghost
+  // plane: rows at plane z read planes z-1..z+1 of every component.
+  void interior_rows(int q, const SlabGeo& sg, int& a, int& b) const {
+    const int nz = sg.g.n[2];
+    a = q > 0 ? (sg.Z0 - sg.W0()) + 1 : 0;
+    b = q + 1 < P_() ? (sg.Z1 - sg.W0()) - 1 : nz + 1;
+    if (b < a) b = a;
+  }
+  // r = b - H x on every local slab. When x's ghosts are stale (an update
+  // since the last exchange) the exchange runs on sx while s computes the
+  // interior rows; the rows next to the ghost planes follow the exchange.
+  void residual_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool for_restrict) {
+    auto out = [&](int q) { SlabLevel& sl = *L[l][q]; return for_restrict ? sl.r.p : sl.sm.res.p; };
+    if (!pend[l]) {
+      for (int q = q_lo; q < q_hi; ++q) {
+        SlabLevel& sl = *L[l][q];
+        launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], out(q), s);
+      }
+      return;
+    }
+    CK(cudaEventRecord(ev_upd, s));  // the update the pushes must see
+    CK(cudaStreamWaitEvent(sx, ev_upd, 0));
+    for (int q = q_lo; q < q_hi; ++q) {
+      SlabLevel& sl = *L[l][q];
+      int a, b;
+      interior_rows(q, sl.sg, a, b);
+      if (b > a) launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], out(q), s, a, b);
+    }
+    exchange(l, X, sx);
+    CK(cudaEventRecord(ev_x, sx));
+    CK(cudaStreamWaitEvent(s, ev_x, 0));
+    for (int q = q_lo; q < q_hi; ++q) {
+      SlabLevel& sl = *L[l][q];
+      int a, b;
+      interior_rows(q, sl.sg, a, b);
+      if (a > 0) launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], out(q), s, 0, a);
+      if (b < sl.sg.g.n[2] + 1) launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], out(q), s, b, -1);
+    }
+    pend[l] = 0;
+  }
+  // refresh stale ghosts (before transfers read them)
+  void settle(int l, const std::vector<cplx*>& X) {
+    if (!pend[l]) return;
+    exchange(l, X);
+    pend[l] = 0;
   }
 
   void sweep_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool xzero = false) {
     for (int color = 0; color < 2; ++color) {
+      const bool first_zero = xzero && color == 0;  // residual is b itself
+      if (!first_zero) residual_all(l, B, X, false);
       for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& sl = *L[l][q];
-        sl.sm.colour_phase(sl.sg.g, P, sl.media.ref(), B[q], X[q], opt.damping, color, s, xzero && color == 0);
+        sl.sm.update(sl.sg.g, first_zero ? B[q] : sl.sm.res.p, X[q], opt.damping, color, s);
       }
-      exchange(l, X);
+      pend[l] = 1;
     }
   }
 
@@ -193,10 +255,7 @@ struct ehmg_slab_mg_s {
   void cycle(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool xzero = false) {
     const int La = plan.La, nl = plan.nl;
     for (int q = 0; q < opt.nu1; ++q) sweep_all(l, B, X, xzero && q == 0);
-    for (int q = q_lo; q < q_hi; ++q) {
-      SlabLevel& sl = *L[l][q];
-      launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], sl.r.p, s);
-    }
+    residual_all(l, B, X, true);
     const bool next_coarsest = (l + 2 == nl);
     const int repeat = (opt.cycle == 2 && !next_coarsest) ? 2 : 1;
     if (l + 1 < La) {
@@ -238,6 +297,7 @@ struct ehmg_slab_mg_s {
       for (int q = q_lo; q < q_hi; ++q) launch_transfer(L[l][q]->sg.g, gc, false, erep.p, X[q], true, s);
     }
     for (int q = 0; q < opt.nu2; ++q) sweep_all(l, B, X);
+    settle(l, X);
   }
 
   // z = M r on the level-0 windows of the local slabs (ghosts of B refreshed here)
@@ -311,6 +371,9 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   const int La = sm->plan.La, nl = opt.n_levels;
   CK(cudaGetDevice(&sm->dev));
   CK(cudaStreamCreateWithFlags(&sm->s, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sm->sx, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&sm->ev_upd, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&sm->ev_x, cudaEventDisableTiming));
   cudaStream_t s = sm->s;
   // global media per level [0, La] (every rank holds them; setup only)
   std::vector<std::unique_ptr<DevMedia>> gm;
@@ -321,6 +384,7 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
     else gm[l - 1]->coarsen_into(sm->G[l - 1], *gm[l], sm->G[l], s);
   }
   sm->L.resize(La);
+  sm->pend.assign(La, 0);
   for (int l = 0; l < La; ++l) {
     for (int q = 0; q < nslabs; ++q) {
       auto sl = std::make_unique<SlabLevel>();

@@ -214,12 +214,14 @@ struct DevMedia {
 
 // ----------------------------------------------------------- level kernels
 // r = b - A x (b != null) or y = A x.
+// Rows of output planes [z_lo, z_hi) only (TMA path; the generic kernels
+// always write every row, a correct superset).
 static void launch_residual(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* x,
-                            const cplx* b, cplx* y, cudaStream_t s) {
+                            const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
   Prof pf(b ? "residual" : "apply", s);
   const Cell* m = mr.packed;
   if (g.nd == 3 && stencil3d_supported(g)) {
-    launch_stencil3d(g, P, mr.soa, x, b, y, s);
+    launch_stencil3d(g, P, mr.soa, x, b, y, s, z_lo, z_hi);
   } else if (g.nd == 3) {
     k_apply_generic<3><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
   } else {
@@ -323,10 +325,14 @@ struct Smoother {
   // One red-black colour (global parity `color`; windows shift the local parity).
   void colour_phase(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
                     int color, cudaStream_t s, bool xzero = false) {
-    const int64_t nt = colour_threads(g);
-    const int lc = color ^ (g.zoff & 1);
     const cplx* r = xzero ? b : res.p;
     if (!xzero) launch_residual(g, P, mr, x, b, res.p, s);
+    update(g, r, x, w, color, s);
+  }
+  // Vanka update of one colour from a precomputed residual r.
+  void update(const Geo& g, const cplx* r, cplx* x, double w, int color, cudaStream_t s) {
+    const int64_t nt = colour_threads(g);
+    const int lc = color ^ (g.zoff & 1);
     Prof pf("vanka_update", s);
     if (g.nd == 3)
       k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, r, lc, w, x);

@@ -57,6 +57,7 @@ struct S3Params {
   double wn;                      // (1-beta)/6
   double inv_msum[7];             // 1/(beta + k*wn), k valid mass neighbours
   int nchunks, ntiles_x, ntiles_y;
+  int z_lo, z_hi;  // output planes [z_lo, z_hi); z_hi = n2 + 1 includes the top u2 faces
 };
 
 struct S3Maps {
@@ -157,8 +158,9 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
     const int tile = item % (P.ntiles_x * P.ntiles_y);
     const int chunk = item / (P.ntiles_x * P.ntiles_y);
     const int i0 = (tile % P.ntiles_x) * S3_TX, j0 = (tile / P.ntiles_x) * S3_TY;
-    const int zb = (int)(((int64_t)chunk * n2) / P.nchunks);
-    const int zend = (chunk + 1 == P.nchunks) ? n2 + 1 : (int)(((int64_t)(chunk + 1) * n2) / P.nchunks);
+    const int zspan = P.z_hi - P.z_lo;
+    const int zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
+    const int zend = P.z_lo + (int)(((int64_t)(chunk + 1) * zspan) / P.nchunks);
 
     // ---- per-item constants of this thread's position
     // media boxes start at an even column (16-byte aligned TMA start): i0-2 or i0-3
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
   }
 }
 
-inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148) {
+inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z_lo = 0, int z_hi = -1) {
   S3Params s;
   s.g = g;
   s.beta = P.beta;
@@ -434,7 +436,9 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148) {
   // warm-up planes) over chunk counts with >= 4 planes per chunk, so that
   // the tile x chunk items fill whole waves of the 148 SMs.
   const int tiles = s.ntiles_x * s.ntiles_y;
-  const int n2 = g.n[2];
+  s.z_lo = z_lo;
+  s.z_hi = z_hi < 0 ? g.n[2] + 1 : z_hi;
+  const int n2 = s.z_hi - s.z_lo;  // planes to emit
   int best = 1;
   double best_cost = 1e300;
   for (int nch = 1; nch <= (n2 / 4 > 0 ? n2 / 4 : 1); ++nch) {
@@ -486,8 +490,9 @@ inline bool stencil3d_supported(const Geo& g) {
 }
 
 // media_soa: 4 consecutive cell arrays {mu, rho, gamma, 1/(lambda+mu)}.
+// Output planes [z_lo, z_hi) (default: all, including the top u2 faces).
 inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
-                             const cplx* b, cplx* y, cudaStream_t s) {
+                             const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
   static int nsm = 0;
   const size_t smem = sizeof(S3Smem);
   if (!nsm) {
@@ -537,7 +542,8 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
     }
   }
   const S3Maps M = *Mp;
-  const S3Params sp = make_s3params(g, P, nsm);
+  const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi);
+  if (sp.z_hi <= sp.z_lo) return;
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
   k_stencil3d<<<grid, S3_THREADS, smem, s>>>(M, sp, b, y);
