@@ -99,6 +99,10 @@ typedef struct {
   int sweep;
   int k_inner_iterations;
   double k_inner_rtol;
+  /* 0: complex128 hierarchy; 1: complex64 hierarchy behind complex128
+   * precondition()/cycle() calls (experiments.hpp:241 MixedPrecondition,
+   * config "precision": "mixed"; V/W/two-grid cycles, red-black sweeps) */
+  int precision;
 } ehmg_mg_options;
 
 int ehmg_multigrid_create(int ndim, const int* dims, double h, const double* lambda,

@@ -295,6 +295,7 @@ def ref():
                                          C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _cp, _cp,
                                          C.POINTER(C.c_int), C.POINTER(C.c_int),
                                          C.POINTER(C.c_double), _dp, C.c_int, C.POINTER(C.c_int)]
+        L.ref_solve_mixed.argtypes = L.ref_solve.argtypes
         _ref = L
     return _ref
 
@@ -357,12 +358,15 @@ def ref_mg_cycles(dims, h, media, beta, omega, alpha, b, x, ncycles=1, n_levels=
 
 def ref_solve(dims, h, media, beta, omega, alpha, b, n_levels=2, cycle="v", nu1=1, nu2=1,
               damping=0.75, vanka="full", sweep="red_black", restart=5, max_iterations=600,
-              rtol=1e-6):
+              rtol=1e-6, precision="double"):
+    """The reference's solve (experiments.hpp:313); precision "mixed" runs the
+    reference float hierarchy behind a double FGMRES (MixedPrecondition)."""
     x = np.zeros(n_dofs(dims), np.complex128)
     it, st, nh = C.c_int(0), C.c_int(0), C.c_int(0)
     rr = C.c_double(0)
     hist = np.zeros(max_iterations + 64, np.float64)
-    _chk(ref().ref_solve(len(dims), _dims(dims), h, *media.arrays(), beta, omega, alpha,
+    fn = ref().ref_solve_mixed if precision == "mixed" else ref().ref_solve
+    _chk(fn(len(dims), _dims(dims), h, *media.arrays(), beta, omega, alpha,
                          n_levels, CYCLES[cycle], nu1, nu2, damping, 0 if vanka == "full" else 1,
                          1 if sweep == "red_black" else 0, restart, max_iterations, rtol,
                          np.ascontiguousarray(b, np.complex128), x, C.byref(it), C.byref(st),

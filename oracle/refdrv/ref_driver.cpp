@@ -35,6 +35,7 @@
 #include "ehmg/krylov.hpp"
 #include "ehmg/operator.hpp"
 #include "ehmg/transfer.hpp"
+#include "ehmg/multigrid.hpp"  // convert_field (multigrid.hpp:311); Multigrid itself is not instantiated
 #include "ehmg/vanka.hpp"
 #undef private
 
@@ -77,7 +78,9 @@ struct Media {
 };
 
 // ---- exact coarsest solve (dense LU on reference unit-probe rows) -------
-struct DenseLU {
+template <class CT>
+struct DenseLUT {
+  using Cd = CT;
   std::int64_t n = 0;
   std::vector<Cd> a;  // column-major
   std::vector<std::int64_t> piv;
@@ -85,7 +88,7 @@ struct DenseLU {
     piv.resize(size_t(n));
     for (std::int64_t k = 0; k < n; ++k) {
       std::int64_t p = k;
-      double best = std::abs(a[size_t(k + k * n)]);
+      auto best = std::abs(a[size_t(k + k * n)]);
       for (std::int64_t i = k + 1; i < n; ++i)
         if (std::abs(a[size_t(i + k * n)]) > best) best = std::abs(a[size_t(i + k * n)]), p = i;
       piv[size_t(k)] = p;
@@ -111,18 +114,23 @@ struct DenseLU {
   }
 };
 
-template <int Dim> DenseLU dense_lu(const OpData<double, Dim>& D) {
+using DenseLU = DenseLUT<Cd>;
+
+// Real = float: the LU of the float operator in float arithmetic, as the
+// reference's Multigrid<float> factors its float matrix (multigrid.hpp:97).
+template <class Real, int Dim> DenseLUT<std::complex<Real>> dense_lu(const OpData<Real, Dim>& D) {
+  using Cd = std::complex<Real>;
   std::array<std::int64_t, Dim + 2> off{};
   for (int c = 0; c <= Dim; ++c)
     off[size_t(c) + 1] = off[size_t(c)] + (c < Dim ? D.faceb[size_t(c)].size() : D.cellb.size());
-  DenseLU L;
+  DenseLUT<Cd> L;
   L.n = off[Dim + 1];
   L.a.assign(size_t(L.n * L.n), Cd(0));
   for (int cc = 0; cc <= Dim; ++cc) {
     const Box<Dim>& cb = cc < Dim ? D.faceb[size_t(cc)] : D.cellb;
     for_each(cb, [&](const Idx<Dim>& ci) {
       std::int64_t col = off[size_t(cc)] + cb.lin(ci);
-      UnitAcc<double, Dim> acc{D, cc, ci};
+      UnitAcc<Real, Dim> acc{D, cc, ci};
       for (int rc = 0; rc <= Dim; ++rc) {
         const Box<Dim>& rb = rc < Dim ? D.faceb[size_t(rc)] : D.cellb;
         std::array<int, 3> lo{-2, -2, Dim == 3 ? -2 : 0}, hi{2, 2, Dim == 3 ? 2 : 0};
@@ -145,35 +153,36 @@ template <int Dim> DenseLU dense_lu(const OpData<double, Dim>& D) {
 }
 
 // ---- restated cycle around the reference components --------------------
-template <int Dim> struct RefMG {
-  using F = FieldVector<double, Dim>;
+template <class Real, int Dim> struct RefMGT {
+  using F = FieldVector<Real, Dim>;
+  using Cd = std::complex<Real>;
   struct Lev {
     StaggeredGrid<Dim> g;
-    OpData<double, Dim> D;
-    VankaSmoother<double, Dim> sm;
+    OpData<Real, Dim> D;
+    VankaSmoother<Real, Dim> sm;
     F r, t, bc, ec;
   };
   std::vector<std::unique_ptr<Lev>> L;
-  DenseLU lu;
+  DenseLUT<Cd> lu;
   int cycle, nu1, nu2;
   double w;
   VankaMode mode;
   SweepOrder order;
 
-  RefMG(StaggeredGrid<Dim> g, MediaModel<Dim> m, OperatorParams par, int nl, int cyc, int n1,
+  RefMGT(StaggeredGrid<Dim> g, MediaModel<Dim> m, OperatorParams par, int nl, int cyc, int n1,
         int n2, double w_, int vmode, int sweep)
       : cycle(cyc), nu1(n1), nu2(n2), w(w_), mode(vmode ? VankaMode::economic : VankaMode::full),
         order(sweep ? SweepOrder::red_black : SweepOrder::lexicographic) {
     for (int l = 0; l < nl; ++l) {
       auto lv = std::make_unique<Lev>(
-          Lev{g, make_opdata<double>(g, m, par), VankaSmoother<double, Dim>(mode), F(g), F(g), F(g), F(g)});
+          Lev{g, make_opdata<Real>(g, m, par), VankaSmoother<Real, Dim>(mode), F(g), F(g), F(g), F(g)});
       L.push_back(std::move(lv));
       if (l + 1 < nl) {
         m = coarsen_media(g, m);
         g = coarsen_grid(g);
       }
     }
-    lu = dense_lu(L.back()->D);
+    lu = dense_lu<Real, Dim>(L.back()->D);
   }
   void cyc(int l, const F& b, F& x) {
     const int nl = int(L.size());
@@ -201,6 +210,7 @@ template <int Dim> struct RefMG {
     for (int s = 0; s < nu2; ++s) lev.sm.sweep(lev.D, b, x, w, order);
   }
 };
+template <int Dim> using RefMG = RefMGT<double, Dim>;
 
 template <int Dim>
 int apply_t(const int* dims, double h, Media M, double beta, double omega, double alpha,
@@ -276,10 +286,18 @@ template <int Dim>
 int solve_t(const int* dims, double h, Media M, double beta, double omega, double alpha, int nl,
             int cyc, int nu1, int nu2, double w, int vmode, int sweep, int restart, int max_it,
             double rtol, const Cd* b, Cd* x, int* iters, int* status, double* relres,
-            double* hist, int hist_cap, int* n_hist) {
+            double* hist, int hist_cap, int* n_hist, int mixed = 0) {
   StaggeredGrid<Dim> g(to_idx<Dim>(dims), h);
   auto media = media_of<Dim>(g, M.lam, M.mu, M.rho, M.gam);
-  RefMG<Dim> mg(g, media, {beta, omega, alpha, false}, nl, cyc, nu1, nu2, w, vmode, sweep);
+  std::unique_ptr<RefMG<Dim>> mgd;
+  std::unique_ptr<RefMGT<float, Dim>> mgf;
+  if (mixed)
+    mgf = std::make_unique<RefMGT<float, Dim>>(g, media, OperatorParams{beta, omega, alpha, false}, nl, cyc, nu1,
+                                               nu2, w, vmode, sweep);
+  else
+    mgd = std::make_unique<RefMG<Dim>>(g, media, OperatorParams{beta, omega, alpha, false}, nl, cyc, nu1, nu2,
+                                       w, vmode, sweep);
+  FieldVector<float, Dim> rf(g), zf(g);
   auto D0 = make_opdata<double, Dim>(g, media, {beta, omega, 0.0, false});
   using F = FieldVector<double, Dim>;
   F B(g), X(g);
@@ -290,9 +308,17 @@ int solve_t(const int* dims, double h, Media M, double beta, double omega, doubl
   ko.max_iterations = max_it;
   ko.rtol = rtol;
   auto A = [&](const F& in, F& out) { apply_mixed_operator(D0, in, out); };
+  // experiments.hpp:241 MixedPrecondition for mixed
   auto Mp = [&](const F& r, F& z) {
-    z.set_zero();
-    mg.cyc(0, r, z);
+    if (mixed) {
+      convert_field(r, rf);
+      zf.set_zero();
+      mgf->cyc(0, rf, zf);
+      convert_field(zf, z);
+    } else {
+      z.set_zero();
+      mgd->cyc(0, r, z);
+    }
   };
   KrylovResult res = fgmres(A, Mp, B, X, ko);
   store(X, x);
@@ -393,6 +419,19 @@ int ref_solve(int ndim, const int* dims, double h, const double* lam, const doub
   return guard([&] {
     return ndim == 2 ? solve_t<2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist)
                      : solve_t<3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist);
+  });
+}
+
+// FGMRES in double around a complex64 hierarchy (precision "mixed")
+int ref_solve_mixed(int ndim, const int* dims, double h, const double* lam, const double* mu,
+                    const double* rho, const double* gam, double beta, double omega, double alpha, int nl,
+                    int cyc, int nu1, int nu2, double w, int vmode, int sweep, int restart, int max_it,
+                    double rtol, const Cd* b, Cd* x, int* iters, int* status, double* relres,
+                    double* hist, int hist_cap, int* n_hist) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    return ndim == 2 ? solve_t<2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist, 1)
+                     : solve_t<3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist, 1);
   });
 }
 

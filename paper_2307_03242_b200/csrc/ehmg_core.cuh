@@ -45,6 +45,44 @@ EH_HD cplx cdiv(cplx a, cplx b) {
   return mk((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
 }
 
+// complex64 fields of the single-precision hierarchy (experiments.hpp:241
+// MixedPrecondition): same operations on float2.
+typedef float2 cplxf;
+EH_HD cplxf mkf(float r, float i) { return make_float2(r, i); }
+EH_HD cplxf operator+(cplxf a, cplxf b) { return mkf(a.x + b.x, a.y + b.y); }
+EH_HD cplxf operator-(cplxf a, cplxf b) { return mkf(a.x - b.x, a.y - b.y); }
+EH_HD cplxf operator-(cplxf a) { return mkf(-a.x, -a.y); }
+EH_HD cplxf operator*(float s, cplxf a) { return mkf(s * a.x, s * a.y); }
+EH_HD cplxf operator*(cplxf a, float s) { return mkf(a.x * s, a.y * s); }
+EH_HD cplxf operator*(cplxf a, cplxf b) { return mkf(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+EH_HD cplxf& operator+=(cplxf& a, cplxf b) {
+  a.x += b.x;
+  a.y += b.y;
+  return a;
+}
+EH_HD cplxf& operator-=(cplxf& a, cplxf b) {
+  a.x -= b.x;
+  a.y -= b.y;
+  return a;
+}
+
+// Field element traits: V = cplx (complex128) or cplxf (complex64).
+template <class V> struct VT;
+template <> struct VT<cplx> {
+  typedef double R;
+  EH_HD static cplx mk(double r, double i) { return make_double2(r, i); }
+};
+template <> struct VT<cplxf> {
+  typedef float R;
+  EH_HD static cplxf mk(float r, float i) { return make_float2(r, i); }
+};
+// widen to complex128 / narrow from complex128 (identity for cplx)
+EH_HD cplx wide(cplx a) { return a; }
+EH_HD cplx wide(cplxf a) { return make_double2((double)a.x, (double)a.y); }
+template <class V> EH_HD V narrow(cplx a);
+template <> EH_HD cplx narrow<cplx>(cplx a) { return a; }
+template <> EH_HD cplxf narrow<cplxf>(cplx a) { return make_float2((float)a.x, (float)a.y); }
+
 // --------------------------------------------------------------- geometry
 // One level of the staggered grid (grid.hpp:64). 2D grids carry n[2] = 1.
 // A z-slab window of a global grid stores cell planes [zoff, zoff + n[2])
@@ -140,15 +178,19 @@ EH_HD void sh(const int* i, int axis, int d, int* o) {
 }
 
 // ---------------------------------------------------------------- accessors
-struct FieldAcc {
-  const cplx* x;
+// Reads a resident field of element type V, widened to complex128 (the
+// generic rows always evaluate in double).
+template <class V>
+struct FieldAccT {
+  const V* x;
   EH_HD cplx u(const Geo& g, int k, const int* f) const {
-    return g.face_ok(k, f) ? x[g.off[k] + g.flin(k, f)] : mk(0, 0);
+    return g.face_ok(k, f) ? wide(x[g.off[k] + g.flin(k, f)]) : mk(0, 0);
   }
   EH_HD cplx p(const Geo& g, const int* c) const {
-    return g.cell_ok(c) ? x[g.off[g.nd] + g.clin(c)] : mk(0, 0);
+    return g.cell_ok(c) ? wide(x[g.off[g.nd] + g.clin(c)]) : mk(0, 0);
   }
 };
+typedef FieldAccT<cplx> FieldAcc;
 
 struct UnitAcc {  // operator.hpp:212 UnitAcc
   int comp;

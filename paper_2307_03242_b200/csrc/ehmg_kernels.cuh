@@ -21,17 +21,18 @@ inline int grid_for(int64_t n, int cap = 148 * 16) {
 
 // --------------------------------------------------------------- operator
 // y = A x (b == nullptr) or y = b - A x. One thread per DOF, generic rows.
-template <int ND>
+// V = cplx or cplxf storage; rows evaluate in double.
+template <int ND, class V = cplx>
 __global__ void __launch_bounds__(kThreads) k_apply_generic(Geo g, OpPar P, const Cell* __restrict__ m,
-                                                            const cplx* __restrict__ x,
-                                                            const cplx* __restrict__ b,
-                                                            cplx* __restrict__ y) {
-  FieldAcc A{x};
+                                                            const V* __restrict__ x,
+                                                            const V* __restrict__ b,
+                                                            V* __restrict__ y) {
+  FieldAccT<V> A{x};
   GRID_STRIDE(r, g.ndofs) {
     int i[3];
     int comp = g.unlin(r, i);
     cplx v = row_any<ND>(g, m, P, comp, i, A);
-    y[r] = b ? b[r] - v : v;
+    y[r] = narrow<V>(b ? wide(b[r]) - v : v);
   }
 }
 
@@ -296,21 +297,22 @@ __global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict_
 // for the state at the start of the colour (vanka.hpp:205); every cell of
 // `color` solves its local system from r and adds w * correction to the DOFs
 // it owns. Cells of one colour share no DOFs, so the in-place writes commute.
-template <int ND>
-__global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int full, const cplx* __restrict__ soa,
-                                                           const cplx* __restrict__ r, int color, double w,
-                                                           cplx* __restrict__ x) {
+// T = cplx or cplxf storage (cache, residual, iterate); arithmetic in double.
+template <int ND, class T = cplx>
+__global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
+                                                           const T* __restrict__ r, int color, double w,
+                                                           T* __restrict__ x) {
   const int nu = full ? 4 : 2, cs = ND * nu + 1;
   const int64_t nt = colour_threads(g);
   GRID_STRIDE(t, nt) {
     int c[3];
     if (!colour_cell(g, t, color, c)) continue;
-    const cplx* q = soa + (int64_t)color * cs * nt + t;
-    auto Q = [&](int e) { return q[(int64_t)e * nt]; };
+    const T* q = soa + (int64_t)color * cs * nt + t;
+    auto Q = [&](int e) { return wide(q[(int64_t)e * nt]); };
     const int64_t pi = g.off[ND] + g.clin(c);
     int64_t fi[ND][2];
     cplx rr[ND][2];
-    cplx dpa = r[pi];
+    cplx dpa = wide(r[pi]);
     const cplx b0 = mk(V.ih, 0), b1 = mk(-V.ih, 0);
     auto loadU = [&](int k, cplx* U) {
       if (full) {
@@ -325,8 +327,8 @@ __global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int f
       sh(c, k, 1, f1);
       fi[k][0] = g.off[k] + g.flin(k, c);
       fi[k][1] = g.off[k] + g.flin(k, f1);
-      rr[k][0] = r[fi[k][0]];
-      rr[k][1] = r[fi[k][1]];
+      rr[k][0] = wide(r[fi[k][0]]);
+      rr[k][1] = wide(r[fi[k][1]]);
       cplx U[4];
       loadU(k, U);
       const double c0 = vk_c0<ND>(V, g, k, c);
@@ -348,10 +350,10 @@ __global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int f
         du0 = U[0] * rr[k][0] - g0 * dp;
         du1 = U[3] * rr[k][1] - g1 * dp;
       }
-      x[fi[k][0]] += w * du0;
-      x[fi[k][1]] += w * du1;
+      x[fi[k][0]] = narrow<T>(wide(x[fi[k][0]]) + w * du0);
+      x[fi[k][1]] = narrow<T>(wide(x[fi[k][1]]) + w * du1);
     }
-    x[pi] += w * dp;
+    x[pi] = narrow<T>(wide(x[pi]) + w * dp);
   }
 }
 
@@ -455,10 +457,10 @@ EH_HD Taps prolong_taps(int f, int n_fine, bool face) {
 // One thread per destination DOF; the tensor product is contracted axis 0
 // innermost, the association the reference's axis-by-axis sweep produces
 // (transfer.hpp:164).
-template <int ND>
+template <int ND, class V = cplx>
 __global__ void __launch_bounds__(kThreads) k_transfer(Geo gf, Geo gc, int restricting,
-                                                       const cplx* __restrict__ in,
-                                                       cplx* __restrict__ out, int accumulate) {
+                                                       const V* __restrict__ in,
+                                                       V* __restrict__ out, int accumulate) {
   const Geo& gto = restricting ? gc : gf;
   const Geo& gfrom = restricting ? gf : gc;
   GRID_STRIDE(r, gto.ndofs) {
@@ -485,12 +487,12 @@ __global__ void __launch_bounds__(kThreads) k_transfer(Geo gf, Geo gc, int restr
       for (int q1 = 0; q1 < t[1].cnt; ++q1) {
         cplx s0 = mk(0, 0);
         const int64_t rowb = base + (int64_t)d0 * (t[1].idx[q1] + (int64_t)d1 * t[2].idx[q2]);
-        for (int q0 = 0; q0 < t[0].cnt; ++q0) s0 += t[0].w[q0] * in[rowb + t[0].idx[q0]];
+        for (int q0 = 0; q0 < t[0].cnt; ++q0) s0 += t[0].w[q0] * wide(in[rowb + t[0].idx[q0]]);
         s1 += t[1].w[q1] * s0;
       }
       s2 += t[2].w[q2] * s1;
     }
-    out[r] = accumulate ? out[r] + s2 : s2;
+    out[r] = narrow<V>(accumulate ? wide(out[r]) + s2 : s2);
   }
 }
 
@@ -500,9 +502,9 @@ __global__ void __launch_bounds__(kThreads) k_transfer(Geo gf, Geo gc, int restr
 // division). Same tap rules and contraction order as k_transfer. Both grids
 // may be z-slab windows: taps along z follow the global grid, reads outside
 // the fine/coarse window storage contribute zero (garbage ghost region).
-template <int C>
-__global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const cplx* __restrict__ xf,
-                                                   cplx* __restrict__ xc) {
+template <int C, class V = cplx>
+__global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const V* __restrict__ xf,
+                                                   V* __restrict__ xc) {
   const int o0 = blockIdx.x * 32 + threadIdx.x, o1 = blockIdx.y * 8 + threadIdx.y, o2 = blockIdx.z;
   const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1);
   if (o0 >= D0 || o1 >= D1) return;
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const cplx* _
   const Taps t0 = restrict_taps(o0, F0, C == 0);
   const Taps t1 = restrict_taps(o1, F1, C == 1);
   const Taps t2 = restrict_taps(o2 + gc.zoff, gf.gn2 + (C == 2), C == 2);
-  const cplx* base = xf + gf.off[C];
+  const V* base = xf + gf.off[C];
   cplx s2 = mk(0, 0);
 #pragma unroll
   for (int q2 = 0; q2 < 3; ++q2) {
@@ -521,24 +523,24 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const cplx* _
 #pragma unroll
       for (int q1 = 0; q1 < 3; ++q1) {
         if (q1 >= t1.cnt) break;
-        const cplx* row = base + (int64_t)F0 * (t1.idx[q1] + (int64_t)F1 * z);
+        const V* row = base + (int64_t)F0 * (t1.idx[q1] + (int64_t)F1 * z);
         cplx s0 = mk(0, 0);
 #pragma unroll
         for (int q0 = 0; q0 < 3; ++q0) {
           if (q0 >= t0.cnt) break;
-          s0 += t0.w[q0] * row[t0.idx[q0]];
+          s0 += t0.w[q0] * wide(row[t0.idx[q0]]);
         }
         s1 += t1.w[q1] * s0;
       }
     }
     s2 += t2.w[q2] * s1;
   }
-  xc[gc.off[C] + o0 + (int64_t)D0 * (o1 + (int64_t)D1 * o2)] = s2;
+  xc[gc.off[C] + o0 + (int64_t)D0 * (o1 + (int64_t)D1 * o2)] = narrow<V>(s2);
 }
 
-template <int C>
-__global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const cplx* __restrict__ xc,
-                                                  cplx* __restrict__ xf, int accumulate) {
+template <int C, class V = cplx>
+__global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const V* __restrict__ xc,
+                                                  V* __restrict__ xf, int accumulate) {
   const int f0 = blockIdx.x * 32 + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y, f2 = blockIdx.z;
   const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
   if (f0 >= F0 || f1 >= F1) return;
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const cplx* __
   const Taps t0 = prolong_taps(f0, F0, C == 0);
   const Taps t1 = prolong_taps(f1, F1, C == 1);
   const Taps t2 = prolong_taps(f2 + gf.zoff, gf.gn2 + (C == 2), C == 2);
-  const cplx* base = xc + gc.off[C];
+  const V* base = xc + gc.off[C];
   cplx s2 = mk(0, 0);
 #pragma unroll
   for (int q2 = 0; q2 < 2; ++q2) {
@@ -557,20 +559,20 @@ __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const cplx* __
 #pragma unroll
       for (int q1 = 0; q1 < 2; ++q1) {
         if (q1 >= t1.cnt) break;
-        const cplx* row = base + (int64_t)D0 * (t1.idx[q1] + (int64_t)D1 * z);
+        const V* row = base + (int64_t)D0 * (t1.idx[q1] + (int64_t)D1 * z);
         cplx s0 = mk(0, 0);
 #pragma unroll
         for (int q0 = 0; q0 < 2; ++q0) {
           if (q0 >= t0.cnt) break;
-          s0 += t0.w[q0] * row[t0.idx[q0]];
+          s0 += t0.w[q0] * wide(row[t0.idx[q0]]);
         }
         s1 += t1.w[q1] * s0;
       }
     }
     s2 += t2.w[q2] * s1;
   }
-  cplx* o = xf + gf.off[C] + f0 + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
-  *o = accumulate ? *o + s2 : s2;
+  V* o = xf + gf.off[C] + f0 + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
+  *o = narrow<V>(accumulate ? wide(*o) + s2 : s2);
 }
 
 // ------------------------------------------------------------------ media
@@ -635,15 +637,18 @@ __global__ void k_coarse_matrix(Geo g, OpPar P, const Cell* __restrict__ m, cplx
 }
 
 // x = Ainv b with Ainv row-major: one warp per row, coalesced along the row.
-__global__ void __launch_bounds__(kThreads) k_gemv_rows(int64_t N, const cplx* __restrict__ A,
-                                                        const cplx* __restrict__ b, cplx* __restrict__ x) {
+// A and the vectors stored as V (complex64 for the single-precision
+// hierarchy: half the bytes of the bandwidth-bound inverse); sums in double.
+template <class V = cplx>
+__global__ void __launch_bounds__(kThreads) k_gemv_rows(int64_t N, const V* __restrict__ A,
+                                                        const V* __restrict__ b, V* __restrict__ x) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; row < N; row += warps) {
-    const cplx* a = A + row * N;
+    const V* a = A + row * N;
     double sr = 0, si = 0;
     for (int64_t j = lane; j < N; j += 32) {
-      cplx av = a[j], bv = __ldg(&b[j]);
+      const cplx av = wide(a[j]), bv = wide(__ldg(&b[j]));
       sr = fma(av.x, bv.x, fma(-av.y, bv.y, sr));
       si = fma(av.x, bv.y, fma(av.y, bv.x, si));
     }
@@ -651,8 +656,14 @@ __global__ void __launch_bounds__(kThreads) k_gemv_rows(int64_t N, const cplx* _
       sr += __shfl_xor_sync(0xffffffffu, sr, s);
       si += __shfl_xor_sync(0xffffffffu, si, s);
     }
-    if (lane == 0) x[row] = mk(sr, si);
+    if (lane == 0) x[row] = narrow<V>(mk(sr, si));
   }
+}
+
+// complex128 <-> complex64 copies (experiments.hpp:243 convert_field)
+template <class D, class S>
+__global__ void __launch_bounds__(kThreads) k_convert(int64_t n, const S* __restrict__ src, D* __restrict__ dst) {
+  GRID_STRIDE(i, n) dst[i] = narrow<D>(wide(src[i]));
 }
 
 __global__ void k_identity(int64_t N, cplx* __restrict__ B) {

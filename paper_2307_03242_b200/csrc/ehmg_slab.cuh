@@ -354,6 +354,7 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   if (g0.nd != 3) throw Err(EHMG_EINVAL, "slab: z-slab decomposition is 3D only");
   if (opt.cycle == 3) throw Err(EHMG_EINVAL, "slab: K-cycles need a distributed inner Krylov (not supported)");
   if (opt.sweep != 1) throw Err(EHMG_EINVAL, "slab: only red-black sweeps decompose");
+  if (opt.precision != 0) throw Err(EHMG_EINVAL, "slab: mixed precision is single-GPU only");
   if (!stencil3d_supported(g0)) throw Err(EHMG_EINVAL, "slab: needs an even x extent (TMA stencil)");
   auto sm = std::make_unique<ehmg_slab_mg_s>();
   sm->opt = opt;

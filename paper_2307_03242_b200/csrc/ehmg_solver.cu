@@ -148,7 +148,12 @@ static void validate_media(int64_t n, const double* lam, const double* mu, const
 struct MediaRef {
   const Cell* packed;
   const double* soa;
+  const float* soaf;  // float copy of soa (single-precision hierarchy), or null
 };
+
+__global__ void k_d2f(int64_t n, const double* __restrict__ in, float* __restrict__ out) {
+  GRID_STRIDE(i, n) out[i] = (float)in[i];
+}
 
 __global__ void k_media_soa(int64_t n, const Cell* __restrict__ in, double* __restrict__ out) {
   GRID_STRIDE(i, n) {
@@ -165,7 +170,14 @@ struct DevMedia {
   DBuf<double> raw[4];
   DBuf<Cell> packed;
   DBuf<double> soa;
-  MediaRef ref() const { return MediaRef{packed.p, soa.p}; }
+  DBuf<float> soaf;
+  MediaRef ref() const { return MediaRef{packed.p, soa.p, soaf.p}; }
+  // float SoA for the complex64 stencil (the double SoA is released)
+  void make_float(int64_t n, cudaStream_t s) {
+    soaf.alloc(4 * n);
+    k_d2f<<<grid_for(4 * n), kThreads, 0, s>>>(4 * n, soa.p, soaf.p);
+    CK(cudaGetLastError());
+  }
   void upload(int64_t n, const double* const* f, cudaStream_t s) {
     for (int q = 0; q < 4; ++q) {
       raw[q].alloc(n);
@@ -229,9 +241,25 @@ static void launch_residual(const Geo& g, const OpPar& P, const MediaRef& mr, co
   }
   CK(cudaGetLastError());
 }
+// complex64 fields: the 3D stencil computes in float; the generic rows
+// evaluate in double and store complex64.
+static void launch_residual(const Geo& g, const OpPar& P, const MediaRef& mr, const cplxf* x,
+                            const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  Prof pf(b ? "residual" : "apply", s);
+  const Cell* m = mr.packed;
+  if (g.nd == 3 && g.n[0] % 2 == 0 && mr.soaf) {
+    launch_stencil3d(g, P, mr.soaf, x, b, y, s, z_lo, z_hi);
+  } else if (g.nd == 3) {
+    k_apply_generic<3, cplxf><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
+  } else {
+    k_apply_generic<2, cplxf><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
+  }
+  CK(cudaGetLastError());
+}
 
-static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, const cplx* in,
-                            cplx* out, bool accumulate, cudaStream_t s) {
+template <class V>
+static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, const V* in, V* out,
+                            bool accumulate, cudaStream_t s) {
   const Geo& gto = restricting ? gc : gf;
   Prof pf(restricting ? "restrict" : "prolong_add", s);
   if (gf.nd == 3) {
@@ -240,20 +268,20 @@ static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, cons
       const int d0 = gto.n[0] + (c == 0), d1 = gto.n[1] + (c == 1), d2 = gto.n[2] + (c == 2);
       const dim3 grd((d0 + 31) / 32, (d1 + 7) / 8, c < 3 ? d2 : gto.n[2]);
       if (restricting) {
-        if (c == 0) k_restrict3<0><<<grd, blk, 0, s>>>(gf, gc, in, out);
-        else if (c == 1) k_restrict3<1><<<grd, blk, 0, s>>>(gf, gc, in, out);
-        else if (c == 2) k_restrict3<2><<<grd, blk, 0, s>>>(gf, gc, in, out);
-        else k_restrict3<3><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        if (c == 0) k_restrict3<0, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        else if (c == 1) k_restrict3<1, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        else if (c == 2) k_restrict3<2, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
+        else k_restrict3<3, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
       } else {
-        if (c == 0) k_prolong3<0><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
-        else if (c == 1) k_prolong3<1><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
-        else if (c == 2) k_prolong3<2><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
-        else k_prolong3<3><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        if (c == 0) k_prolong3<0, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        else if (c == 1) k_prolong3<1, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        else if (c == 2) k_prolong3<2, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        else k_prolong3<3, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
       }
     }
   } else {
-    k_transfer<2><<<grid_for(gto.ndofs, 148 * 64), kThreads, 0, s>>>(gf, gc, restricting, in, out,
-                                                                     accumulate);
+    k_transfer<2, V><<<grid_for(gto.ndofs, 148 * 64), kThreads, 0, s>>>(gf, gc, restricting, in, out,
+                                                                        accumulate);
   }
   CK(cudaGetLastError());
 }
@@ -271,6 +299,21 @@ struct Smoother {
   int full = 1, stride = 0;  // stride: reference (vanka.hpp:35) entries per cell
   VkPar vk;
   DBuf<cplx> soa, res;
+  DBuf<cplxf> soaf, resf;  // complex64 cache / residual (single-precision hierarchy)
+  // switch this smoother to complex64 storage (the double cache is released)
+  void make_float(const Geo& g, cudaStream_t s) {
+    soaf.alloc(soa.n);
+    k_convert<cplxf, cplx><<<grid_for(soa.n, 148 * 64), kThreads, 0, s>>>(soa.n, soa.p, soaf.p);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    soa.release();
+    res.release();
+    resf.alloc(g.ndofs);
+  }
+  const cplx* cache(const cplx*) const { return soa.p; }
+  const cplxf* cache(const cplxf*) const { return soaf.p; }
+  cplx* resbuf(const cplx*) { return res.p; }
+  cplxf* resbuf(const cplxf*) { return resf.p; }
   // Cache for the cells of `gg` (global grid, global packed media m), or of
   // its z-window [z0, z1) when z1 >= 0; sweeps then run on the window geometry.
   void build(const Geo& gg, const OpPar& P, const Cell* m, int full_, cudaStream_t s, int z0 = 0,
@@ -311,33 +354,42 @@ struct Smoother {
   }
   // xzero: x is zero on entry, so the first colour's residual is b itself
   // (b - H*0 == b exactly) and its operator apply is skipped.
-  void sweep(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
-             int order, cudaStream_t s, bool xzero = false) {
+  template <class V>
+  void sweep(const Geo& g, const OpPar& P, const MediaRef& mr, const V* b, V* x, double w, int order,
+             cudaStream_t s, bool xzero = false) {
     const Cell* m = mr.packed;
     if (order == 0) {
-      if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
-      else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
-      CK(cudaGetLastError());
-      return;
+      if constexpr (sizeof(V) == sizeof(cplx)) {
+        if (g.nd == 3) k_vanka_lex<3><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
+        else k_vanka_lex<2><<<1, 1, 0, s>>>(g, P, vk, m, full, soa.p, b, x, w);
+        CK(cudaGetLastError());
+        return;
+      } else {
+        throw Err(EHMG_EINVAL, "mixed precision: lexicographic Vanka sweeps are not supported");
+      }
     }
     for (int color = 0; color < 2; ++color) colour_phase(g, P, mr, b, x, w, color, s, xzero && color == 0);
   }
   // One red-black colour (global parity `color`; windows shift the local parity).
-  void colour_phase(const Geo& g, const OpPar& P, const MediaRef& mr, const cplx* b, cplx* x, double w,
-                    int color, cudaStream_t s, bool xzero = false) {
-    const cplx* r = xzero ? b : res.p;
-    if (!xzero) launch_residual(g, P, mr, x, b, res.p, s);
+  template <class V>
+  void colour_phase(const Geo& g, const OpPar& P, const MediaRef& mr, const V* b, V* x, double w, int color,
+                    cudaStream_t s, bool xzero = false) {
+    V* rb = resbuf(b);
+    const V* r = xzero ? b : rb;
+    if (!xzero) launch_residual(g, P, mr, x, b, rb, s);
     update(g, r, x, w, color, s);
   }
   // Vanka update of one colour from a precomputed residual r.
-  void update(const Geo& g, const cplx* r, cplx* x, double w, int color, cudaStream_t s) {
+  template <class V>
+  void update(const Geo& g, const V* r, V* x, double w, int color, cudaStream_t s) {
     const int64_t nt = colour_threads(g);
     const int lc = color ^ (g.zoff & 1);
+    const V* cq = cache(r);
     Prof pf("vanka_update", s);
     if (g.nd == 3)
-      k_vanka_update<3><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, r, lc, w, x);
+      k_vanka_update<3, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x);
     else
-      k_vanka_update<2><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, soa.p, r, lc, w, x);
+      k_vanka_update<2, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x);
     CK(cudaGetLastError());
   }
 };
@@ -636,7 +688,20 @@ struct Level {
   DevMedia media;
   Smoother sm;
   DBuf<cplx> r, bc, ec;
-  Fgmres inner;  // K-cycle acceleration on this level
+  DBuf<cplxf> rf, bcf, ecf;  // complex64 level vectors (single-precision hierarchy)
+  Fgmres inner;              // K-cycle acceleration on this level
+};
+// level vectors by element type
+template <class V> struct LB;
+template <> struct LB<cplx> {
+  static cplx* r(Level& L) { return L.r.p; }
+  static cplx* bc(Level& L) { return L.bc.p; }
+  static cplx* ec(Level& L) { return L.ec.p; }
+};
+template <> struct LB<cplxf> {
+  static cplxf* r(Level& L) { return L.rf.p; }
+  static cplxf* bc(Level& L) { return L.bcf.p; }
+  static cplxf* ec(Level& L) { return L.ecf.p; }
 };
 
 struct ehmg_mg_s {
@@ -647,6 +712,12 @@ struct ehmg_mg_s {
   DBuf<cplx> ainv;  // row-major inverse of the coarsest operator
   int64_t nco = 0;
   DBuf<cplx> hx, hy;
+  // precision 1: the hierarchy holds complex64 fields, caches and coarsest
+  // inverse (experiments.hpp:241 MixedPrecondition); r and z stay complex128.
+  int prec = 0;
+  DBuf<cplxf> ainvf, rin, zout;
+  const cplx* coarse_inv(const cplx*) const { return ainv.p; }
+  const cplxf* coarse_inv(const cplxf*) const { return ainvf.p; }
   // CUDA graphs of whole preconditioner applications, one per (r, z) pair:
   // a V(2,2) cycle is ~75 launches, many of them short on the coarse levels.
   struct GraphEntry {
@@ -664,10 +735,23 @@ struct ehmg_mg_s {
   }
 
   // xzero: x is known to be zero on entry (precondition, coarse corrections)
-  void cycle_at(int l, const cplx* b, cplx* x, bool xzero = false);
+  template <class V>
+  void cycle_t(int l, const V* b, V* x, bool xzero);
+  void cycle_at(int l, const cplx* b, cplx* x, bool xzero = false) { cycle_t<cplx>(l, b, x, xzero); }
   void precondition_direct(const cplx* r, cplx* z) {
-    CK(cudaMemsetAsync(z, 0, sizeof(cplx) * L[0]->g.ndofs, s));
-    cycle_at(0, r, z, true);
+    const int64_t n = L[0]->g.ndofs;
+    if (prec == 0) {
+      CK(cudaMemsetAsync(z, 0, sizeof(cplx) * n, s));
+      cycle_at(0, r, z, true);
+      return;
+    }
+    // multigrid.hpp:310 convert_field in, float cycle, convert out
+    k_convert<cplxf, cplx><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, r, rin.p);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(zout.p, 0, sizeof(cplxf) * n, s));
+    cycle_t<cplxf>(0, rin.p, zout.p, true);
+    k_convert<cplx, cplxf><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, zout.p, z);
+    CK(cudaGetLastError());
   }
   static bool graphs_enabled() {
     static int on = -1;
@@ -719,12 +803,13 @@ struct ehmg_mg_s {
 };
 
 // multigrid.hpp:217 cycle_at
-void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x, bool xzero) {
+template <class V>
+void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
   const int nl = (int)L.size();
   g_level = l;
   if (l + 1 == nl) {
     Prof pf("coarse_solve", s);
-    k_gemv_rows<<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, ainv.p, b, x);
+    k_gemv_rows<V><<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x);
     CK(cudaGetLastError());
     return;
   }
@@ -732,22 +817,27 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x, bool xzero) {
   Level& nxt = *L[l + 1];
   for (int q = 0; q < opt.nu1; ++q)
     lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s, xzero && q == 0);
-  launch_residual(lev.g, lev.P, lev.media.ref(), x, b, lev.r.p, s);
-  launch_transfer(lev.g, nxt.g, true, lev.r.p, nxt.bc.p, false, s);
-  CK(cudaMemsetAsync(nxt.ec.p, 0, sizeof(cplx) * nxt.g.ndofs, s));
+  V* const lr = LB<V>::r(lev);
+  V* const nbc = LB<V>::bc(nxt);
+  V* const nec = LB<V>::ec(nxt);
+  launch_residual(lev.g, lev.P, lev.media.ref(), x, b, lr, s);
+  launch_transfer(lev.g, nxt.g, true, (const V*)lr, nbc, false, s);
+  CK(cudaMemsetAsync(nec, 0, sizeof(V) * nxt.g.ndofs, s));
   const bool next_coarsest = (l + 2 == nl);
   switch (opt.cycle) {
     case 0:
     case 1:
-      cycle_at(l + 1, nxt.bc.p, nxt.ec.p, true);
+      cycle_t<V>(l + 1, nbc, nec, true);
       break;
     case 2:
-      cycle_at(l + 1, nxt.bc.p, nxt.ec.p, true);
-      if (!next_coarsest) cycle_at(l + 1, nxt.bc.p, nxt.ec.p);
+      cycle_t<V>(l + 1, nbc, nec, true);
+      if (!next_coarsest) cycle_t<V>(l + 1, nbc, nec, false);
       break;
     default:
       if (next_coarsest) {
-        cycle_at(l + 1, nxt.bc.p, nxt.ec.p, true);
+        cycle_t<V>(l + 1, nbc, nec, true);
+      } else if constexpr (sizeof(V) != sizeof(cplx)) {
+        throw Err(EHMG_EINVAL, "mixed precision: K-cycles are not supported");
       } else {
         ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol,
                                0.99, 2};
@@ -765,7 +855,7 @@ void ehmg_mg_s::cycle_at(int l, const cplx* b, cplx* x, bool xzero) {
       break;
   }
   g_level = l;
-  launch_transfer(lev.g, nxt.g, false, nxt.ec.p, x, true, s);
+  launch_transfer(lev.g, nxt.g, false, (const V*)nec, x, true, s);
   for (int q = 0; q < opt.nu2; ++q) lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s);
 }
 
@@ -855,6 +945,12 @@ static std::unique_ptr<ehmg_mg_s> build_mg(const Geo& g, const double* const* ho
   CK(cudaGetDevice(&mg->dev));
   CK(cudaStreamCreateWithFlags(&mg->s, cudaStreamNonBlocking));
   cudaStream_t s = mg->s;
+  const bool mixed = opt.precision == 1;
+  if (opt.precision != 0 && opt.precision != 1) throw Err(EHMG_EINVAL, "multigrid: precision must be 0 or 1");
+  if (mixed && opt.cycle == 3) throw Err(EHMG_EINVAL, "mixed precision: K-cycles are not supported");
+  if (mixed && opt.sweep == 0)
+    throw Err(EHMG_EINVAL, "mixed precision: lexicographic Vanka sweeps are not supported");
+  mg->prec = mixed ? 1 : 0;
   for (int l = 0; l < nlevels; ++l) {
     auto lev = std::make_unique<Level>();
     lev->g = l == 0 ? g : coarse_geo(mg->L[l - 1]->g);
@@ -868,18 +964,43 @@ static std::unique_ptr<ehmg_mg_s> build_mg(const Geo& g, const double* const* ho
     const bool coarsest = (l + 1 == nlevels);
     if (!coarsest) {
       lev->sm.build(lev->g, P, lev->media.packed.p, opt.vanka_mode == 0 ? 1 : 0, s);
-      lev->r.alloc(lev->g.ndofs);
+      if (mixed) {
+        lev->sm.make_float(lev->g, s);
+        lev->rf.alloc(lev->g.ndofs);
+      } else {
+        lev->r.alloc(lev->g.ndofs);
+      }
     }
     if (l > 0) {
-      lev->bc.alloc(lev->g.ndofs);
-      lev->ec.alloc(lev->g.ndofs);
+      if (mixed) {
+        lev->bcf.alloc(lev->g.ndofs);
+        lev->ecf.alloc(lev->g.ndofs);
+      } else {
+        lev->bc.alloc(lev->g.ndofs);
+        lev->ec.alloc(lev->g.ndofs);
+      }
     }
     mg->L.push_back(std::move(lev));
   }
   for (auto& lev : mg->L) lev->media.drop_raw();
+  if (mixed)
+    for (auto& lev : mg->L) {
+      lev->media.make_float(lev->g.ncells, s);
+      lev->media.soa.release();
+    }
   Level& cl = *mg->L.back();
   mg->nco = cl.g.ndofs;
   build_coarse_inverse(cl.g, P, cl.media.packed.p, mg->ainv, s);
+  if (mixed) {
+    const int64_t nn = mg->nco * mg->nco;
+    mg->ainvf.alloc(nn);
+    k_convert<cplxf, cplx><<<grid_for(nn, 148 * 64), kThreads, 0, s>>>(nn, mg->ainv.p, mg->ainvf.p);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    mg->ainv.release();
+    mg->rin.alloc(g.ndofs);
+    mg->zout.alloc(g.ndofs);
+  }
   CK(cudaStreamSynchronize(s));
   return mg;
 }
@@ -1386,7 +1507,17 @@ int ehmg_multigrid_cycle(ehmg_mg mg, const double* b, double* x, int where) {
       CK(cudaMemcpyAsync(mg->hx.p, x, sizeof(cplx) * n, cudaMemcpyHostToDevice, mg->s));
       dx = mg->hx.p;
     }
-    mg->cycle_at(0, db, dx);
+    if (mg->prec == 0) {
+      mg->cycle_at(0, db, dx);
+    } else {
+      cudaStream_t s = mg->s;
+      k_convert<cplxf, cplx><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, db, mg->rin.p);
+      k_convert<cplxf, cplx><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, dx, mg->zout.p);
+      CK(cudaGetLastError());
+      mg->cycle_t<cplxf>(0, mg->rin.p, mg->zout.p, false);
+      k_convert<cplx, cplxf><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, mg->zout.p, dx);
+      CK(cudaGetLastError());
+    }
     from_dev(x, dx, n, where, mg->s);
   });
 }

@@ -58,21 +58,33 @@ struct S3Params {
   double inv_msum[7];             // 1/(beta + k*wn), k valid mass neighbours
   int nchunks, ntiles_x, ntiles_y;
   int z_lo, z_hi;  // output planes [z_lo, z_hi); z_hi = n2 + 1 includes the top u2 faces
+  float inv_wsum_f[16], inv_msum_f[7];  // the same tables accumulated in float (complex64 kernel)
+};
+
+// Source arrays of the complex64 kernel (loaded with cp.async: complex64
+// rows of n0+1 faces are not 16-byte multiples, which tensor maps require).
+struct S3Src {
+  const cplxf* u[3];
+  const cplxf* p;
+  const float *mu, *rho, *gam, *ilm;
 };
 
 struct S3Maps {
   CUtensorMap u[3], p, mu, rho, gam, ilm;
 };
 
-struct __align__(128) S3Smem {
-  cplx u[3][3][S3_US];  // [plane % 3][component]
-  cplx p[3][S3_US];     // [plane % 3]
-  double mu[4][S3_MS], rho[4][S3_MS], gam[4][S3_MS], ilm[4][S3_MS];  // [plane % 4], pitch S3_MX
-  cplx f[6][S3_FN];     // z-family fluxes at plane z: F00 F11 F01 F10 F20 F21
-  cplx di[3][S3_FN];    // in-plane difference fields: d22 (cell z), d02, d12 (edge z+1)
-  cplx q[2][3][S3_FN];  // mass products md*u [plane & 1][component]
+template <class V>
+struct __align__(128) S3SmemT {
+  typedef typename VT<V>::R R;
+  V u[3][3][S3_US];  // [plane % 3][component]
+  V p[3][S3_US];     // [plane % 3]
+  R mu[4][S3_MS], rho[4][S3_MS], gam[4][S3_MS], ilm[4][S3_MS];  // [plane % 4], pitch S3_MX
+  V f[6][S3_FN];     // z-family fluxes at plane z: F00 F11 F01 F10 F20 F21
+  V di[3][S3_FN];    // in-plane difference fields: d22 (cell z), d02, d12 (edge z+1)
+  V q[2][3][S3_FN];  // mass products md*u [plane & 1][component]
   unsigned long long bar[2];
 };
+typedef S3SmemT<cplx> S3Smem;
 
 __device__ __forceinline__ unsigned s3_saddr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -124,28 +136,95 @@ __device__ __forceinline__ void s3_issue(S3Smem& S, const S3Maps& M, int i0, int
   for (int q = 0; q < np; ++q) s3_tma(S.p[s3_mod3(zp[q])], &M.p, cx, cy, zp[q], bar);
 }
 
-__device__ __forceinline__ double s3_inv(int c) {  // 1/c for c in {0,1,2}
-  return c == 2 ? 0.5 : (c == 1 ? 1.0 : 0.0);
+template <class R>
+__device__ __forceinline__ R s3_inv(int c) {  // 1/c for c in {0,1,2}
+  return c == 2 ? R(0.5) : (c == 1 ? R(1) : R(0));
+}
+template <class R> __device__ __forceinline__ R s3_iw(const S3Params& P, int i);
+template <> __device__ __forceinline__ double s3_iw<double>(const S3Params& P, int i) { return P.inv_wsum[i]; }
+template <> __device__ __forceinline__ float s3_iw<float>(const S3Params& P, int i) { return P.inv_wsum_f[i]; }
+template <class R> __device__ __forceinline__ R s3_im(const S3Params& P, int i);
+template <> __device__ __forceinline__ double s3_im<double>(const S3Params& P, int i) { return P.inv_msum[i]; }
+template <> __device__ __forceinline__ float s3_im<float>(const S3Params& P, int i) { return P.inv_msum_f[i]; }
+
+// complex64 loads: every thread copies its share of each box with cp.async
+// (zero outside the array, like the tensor maps' out-of-bounds fill).
+__device__ __forceinline__ void s3_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s3_saddr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void s3_cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s3_saddr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void s3_cp_commit_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void s3_cplane(cplxf* dst, const cplxf* base, int d0, int d1, int d2, int x0, int y0,
+                                          int z) {
+  const bool zin = z >= 0 && z < d2;
+  for (int e = threadIdx.x; e < S3_UN; e += blockDim.x) {
+    const int r = e / S3_UX, j = e - r * S3_UX, x = x0 + j, y = y0 + r;
+    if (zin && x >= 0 && x < d0 && y >= 0 && y < d1)
+      s3_cp8(&dst[e], base + ((int64_t)z * d1 + y) * d0 + x);
+    else
+      dst[e] = mkf(0.f, 0.f);
+  }
+}
+__device__ __forceinline__ void s3_mplane(float* dst, const float* base, int d0, int d1, int d2, int x0, int y0,
+                                          int z) {
+  const bool zin = z >= 0 && z < d2;
+  for (int e = threadIdx.x; e < S3_MN; e += blockDim.x) {
+    const int r = e / S3_MX, j = e - r * S3_MX, x = x0 + j, y = y0 + r;
+    if (zin && x >= 0 && x < d0 && y >= 0 && y < d1)
+      s3_cp4(&dst[e], base + ((int64_t)z * d1 + y) * d0 + x);
+    else
+      dst[e] = 0.f;
+  }
+}
+__device__ __forceinline__ void s3_issue_ca(S3SmemT<cplxf>& S, const S3Src& M, const Geo& g, int i0, int j0,
+                                            const int* zu, int nu, const int* zm, int nm, const int* zp, int np) {
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int cx = i0 - 2, cy = j0 - 2, mx = (i0 - 2) & ~1;
+  for (int q = 0; q < nu; ++q) {
+    const int sl = s3_mod3(zu[q]);
+    s3_cplane(S.u[sl][0], M.u[0], n0 + 1, n1, n2, cx, cy, zu[q]);
+    s3_cplane(S.u[sl][1], M.u[1], n0, n1 + 1, n2, cx, cy, zu[q]);
+    s3_cplane(S.u[sl][2], M.u[2], n0, n1, n2 + 1, cx, cy, zu[q]);
+  }
+  for (int q = 0; q < nm; ++q) {
+    const int sl = zm[q] & 3;
+    s3_mplane(S.mu[sl], M.mu, n0, n1, n2, mx, cy, zm[q]);
+    s3_mplane(S.rho[sl], M.rho, n0, n1, n2, mx, cy, zm[q]);
+    s3_mplane(S.gam[sl], M.gam, n0, n1, n2, mx, cy, zm[q]);
+    s3_mplane(S.ilm[sl], M.ilm, n0, n1, n2, mx, cy, zm[q]);
+  }
+  for (int q = 0; q < np; ++q) s3_cplane(S.p[s3_mod3(zp[q])], M.p, n0, n1, n2, cx, cy, zp[q]);
 }
 
 // ----------------------------------------------------------------- kernel
 // 11 warps = 3 per SM sub-partition: 16K registers / 96 threads caps this at 168
+// V = C: complex128, planes by TMA. V = cplxf: complex64 arithmetic (the
+// single-precision hierarchy), planes by cp.async from `src`.
+template <class V>
 __global__ void __launch_bounds__(S3_THREADS, 1)
-    k_stencil3d(const __grid_constant__ S3Maps maps, const S3Params P, const cplx* __restrict__ b,
-                cplx* __restrict__ y) {
+    k_stencil3d(const __grid_constant__ S3Maps maps, const __grid_constant__ S3Src src, const S3Params P,
+                const V* __restrict__ b, V* __restrict__ y) {
+  typedef V C;
+  typedef typename VT<V>::R R;
+  constexpr bool kTma = sizeof(R) == 8;
+  const C zc = VT<V>::mk(0, 0);
   extern __shared__ __align__(1024) unsigned char s3_raw[];
-  S3Smem& S = *reinterpret_cast<S3Smem*>(s3_raw);
+  S3SmemT<V>& S = *reinterpret_cast<S3SmemT<V>*>(s3_raw);
   const Geo& g = P.g;
   const int t = threadIdx.x;
   const bool act = t < S3_FN;
   const int fx = act ? t % S3_FX : 1, fy = act ? t / S3_FX : 1;
   const int ui = (fx + 1) + S3_UX * (fy + 1);  // own U-local index
   const bool interior = act && fx >= 1 && fx <= S3_TX && fy >= 1 && fy <= S3_TY;
-  const double beta = P.beta, w = P.w, ih = g.inv_h, wn = P.wn;
+  const R beta = (R)P.beta, w = (R)P.w, ih = (R)g.inv_h, wn = (R)P.wn;
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];  // local storage extents
   const int zoff = g.zoff, n2g = g.gn2;               // global z semantics (slab windows)
 
-  if (t == 0) {
+  if (kTma && t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -168,14 +247,14 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
     const int xg = i0 - 1 + fx, yg = j0 - 1 + fy;
     const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
     const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
-    const double ix = s3_inv(lx + hx1), iy = s3_inv(ly + hy1);
+    const R ix = s3_inv<R>(lx + hx1), iy = s3_inv<R>(ly + hy1);
     const int fl00 = ly | (hy0 << 1), fl11 = (lx << 2) | (hx0 << 3);
     const int fl01 = (lx << 2) | (hx1 << 3), fl10 = (ly << 2) | (hy1 << 3);
     const int fl20 = ly | (hy0 << 1), fl21 = lx | (hx0 << 1);
-    const double c22 = P.inv_wsum[lx | (hx0 << 1) | (ly << 2) | (hy0 << 3)] * ih;
-    const double c02 = P.inv_wsum[ly | (hy0 << 1) | (lx << 2) | (hx1 << 3)] * ih;
-    const double c12 = P.inv_wsum[lx | (hx0 << 1) | (ly << 2) | (hy1 << 3)] * ih;
-    const double mu01s = ix * iy;
+    const R c22 = s3_iw<R>(P, lx | (hx0 << 1) | (ly << 2) | (hy0 << 3)) * ih;
+    const R c02 = s3_iw<R>(P, ly | (hy0 << 1) | (lx << 2) | (hx1 << 3)) * ih;
+    const R c12 = s3_iw<R>(P, lx | (hx0 << 1) | (ly << 2) | (hy1 << 3)) * ih;
+    const R mu01s = ix * iy;
     const int mc0 = (lx + (xg + 1 < n0 + 1)) + (ly + hy0), mc1 = (lx + hx0) + (ly + (yg + 1 < n1 + 1)),
               mc2 = (lx + hx0) + (ly + hy0);
     const bool v0 = interior && xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
@@ -190,173 +269,186 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
     const int64_t o3 = g.off[3] + xg + (int64_t)n0 * yg;
 
     // ---- prologue load group for the first (warm-up) step z = zb-2
-    if (t == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    {
       const int zu[2] = {zb - 2, zb - 1}, zm[3] = {zb - 3, zb - 2, zb - 1}, zp[2] = {zb - 3, zb - 2};
-      s3_issue(S, maps, i0, j0, zu, 2, zm, 3, zp, 2, &S.bar[seq & 1]);
+      if constexpr (kTma) {
+        if (t == 0) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          s3_issue(S, maps, i0, j0, zu, 2, zm, 3, zp, 2, &S.bar[seq & 1]);
+        }
+      } else {
+        s3_issue_ca(S, src, g, i0, j0, zu, 2, zm, 3, zp, 2);
+      }
     }
 
-    cplx r00m = mk(0, 0), r00c = mk(0, 0), r11m = mk(0, 0), r11c = mk(0, 0);
-    cplx r01m = mk(0, 0), r01c = mk(0, 0), r10m = mk(0, 0), r10c = mk(0, 0);
-    cplx r20m = mk(0, 0), r20c = mk(0, 0), r21m = mk(0, 0), r21c = mk(0, 0);
-    cplx f02c = mk(0, 0), f12c = mk(0, 0), f22m = mk(0, 0);
-    cplx qm0 = mk(0, 0), qm1 = mk(0, 0), qm2 = mk(0, 0);
+    C r00m = zc, r00c = zc, r11m = zc, r11c = zc;
+    C r01m = zc, r01c = zc, r10m = zc, r10c = zc;
+    C r20m = zc, r20c = zc, r21m = zc, r21c = zc;
+    C f02c = zc, f12c = zc, f22m = zc;
+    C qm0 = zc, qm1 = zc, qm2 = zc;
     int su0 = s3_mod3(zb - 2), pm = s3_mod3(zb - 3);  // ring slots of u plane z, p plane z-1
 
     for (int z = zb - 2; z < zend; ++z) {
-      s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+      if constexpr (kTma) s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+      else s3_cp_commit_wait();
       ++seq;
       __syncthreads();  // all of step z-1 done: its slots may be refilled
-      if (t == 0) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      {
         const int zu[1] = {z + 2}, zm[1] = {z + 2}, zp[1] = {z + 1};
-        s3_issue(S, maps, i0, j0, zu, 1, zm, 1, zp, 1, &S.bar[seq & 1]);
+        if constexpr (kTma) {
+          if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            s3_issue(S, maps, i0, j0, zu, 1, zm, 1, zp, 1, &S.bar[seq & 1]);
+          }
+        } else {
+          s3_issue_ca(S, src, g, i0, j0, zu, 1, zm, 1, zp, 1);
+        }
       }
       const int su1 = su0 == 2 ? 0 : su0 + 1;
       const int pc_ = pm == 2 ? 0 : pm + 1;
-      const cplx* U0 = S.u[su0][0];
-      const cplx* U1 = S.u[su0][1];
-      const cplx* U2 = S.u[su0][2];
-      const cplx* V0 = S.u[su1][0];
-      const cplx* V1 = S.u[su1][1];
-      const cplx* V2 = S.u[su1][2];
-      const double* MUm = S.mu[(z - 1) & 3];
-      const double* MUc = S.mu[z & 3];
-      const double* MUp = S.mu[(z + 1) & 3];
+      const C* U0 = S.u[su0][0];
+      const C* U1 = S.u[su0][1];
+      const C* U2 = S.u[su0][2];
+      const C* V0 = S.u[su1][0];
+      const C* V1 = S.u[su1][1];
+      const C* V2 = S.u[su1][2];
+      const R* MUm = S.mu[(z - 1) & 3];
+      const R* MUc = S.mu[z & 3];
+      const R* MUp = S.mu[(z + 1) & 3];
       // uniform z quantities (global plane index zg decides the boundary rules)
       const int zg = z + zoff;
       const int lz = zg >= 1, hz0 = zg + 1 < n2g, hz1 = zg + 1 < n2g + 1;
-      const double izc = s3_inv(lz + (zg < n2g)), izp = s3_inv((zg + 1 >= 1) + (zg + 1 < n2g));
+      const R izc = s3_inv<R>(lz + (zg < n2g)), izp = s3_inv<R>((zg + 1 >= 1) + (zg + 1 < n2g));
       const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
-      cplx d00 = mk(0, 0), d11 = mk(0, 0);
+      C d00 = zc, d11 = zc;
 
       if (act) {
         // Every shared-memory value this position needs is loaded once into
         // registers (grouped per component to bound register pressure).
-        const double al = P.alpha, w2 = P.omega2;
-        const double mc00 = MUc[um], mc_l = MUc[um - 1], mc_b = MUc[um - S3_MX], mc_lb = MUc[um - 1 - S3_MX];
-        const double mm00 = MUm[um], mm_l = MUm[um - 1], mm_b = MUm[um - S3_MX];
+        const R al = (R)P.alpha, w2 = (R)P.omega2;
+        const R mc00 = MUc[um], mc_l = MUc[um - 1], mc_b = MUc[um - S3_MX], mc_lb = MUc[um - 1 - S3_MX];
+        const R mm00 = MUm[um], mm_l = MUm[um - 1], mm_b = MUm[um - S3_MX];
         // mu on the edges (operator.hpp:108 order: first axis outer, second inner)
-        const double mu01 = (mc_lb + mc_l + mc_b + mc00) * mu01s;
-        const double mu02 = (mm_l + mc_l + mm00 + mc00) * (ix * izc);
-        const double mu12 = (mm_b + mc_b + mm00 + mc00) * (iy * izc);
-        const double* RHc = S.rho[z & 3];
-        const double* RHp = S.rho[(z + 1) & 3];
-        const double* GAc = S.gam[z & 3];
-        const double* GAp = S.gam[(z + 1) & 3];
-        const double rp00 = RHp[um], gp00 = GAp[um];
-        auto md = [&](double sr, double sg, double ic) {
-          const double rho_f = sr * ic, gam_f = sg * ic + al;
-          return mk(w2 * rho_f, -w2 * gam_f * rho_f);
+        const R mu01 = (mc_lb + mc_l + mc_b + mc00) * mu01s;
+        const R mu02 = (mm_l + mc_l + mm00 + mc00) * (ix * izc);
+        const R mu12 = (mm_b + mc_b + mm00 + mc00) * (iy * izc);
+        const R* RHc = S.rho[z & 3];
+        const R* RHp = S.rho[(z + 1) & 3];
+        const R* GAc = S.gam[z & 3];
+        const R* GAp = S.gam[(z + 1) & 3];
+        const R rp00 = RHp[um], gp00 = GAp[um];
+        auto md = [&](R sr, R sg, R ic) {
+          const R rho_f = sr * ic, gam_f = sg * ic + al;
+          return VT<V>::mk(w2 * rho_f, -w2 * gam_f * rho_f);
         };
         const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
         const int qb = (z + 1) & 1;
         // ---- component 0: F00 (cell, +x pair, in-plane y), F01 (edge01, -y pair, in-plane x)
         {
-          const cplx vmm = V0[ui - S3_UX - 1], vm0 = V0[ui - S3_UX], vmp = V0[ui - S3_UX + 1];
-          const cplx v0m = V0[ui - 1], v00 = V0[ui], v0p = V0[ui + 1];
-          const cplx vp0 = V0[ui + S3_UX], vpp = V0[ui + S3_UX + 1];
-          const cplx u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - S3_UX];
-          const cplx rn0 = (vmp - vm0) + (vpp - vp0) + 2.0 * (v0p - v00);
-          const cplx sz0 = r00m + rn0 + 2.0 * r00c;
-          d00 = (beta * (u0p - u00) + w * sz0) * (P.inv_wsum[fl00 | zA] * ih);
+          const C vmm = V0[ui - S3_UX - 1], vm0 = V0[ui - S3_UX], vmp = V0[ui - S3_UX + 1];
+          const C v0m = V0[ui - 1], v00 = V0[ui], v0p = V0[ui + 1];
+          const C vp0 = V0[ui + S3_UX], vpp = V0[ui + S3_UX + 1];
+          const C u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - S3_UX];
+          const C rn0 = (vmp - vm0) + (vpp - vp0) + R(2) * (v0p - v00);
+          const C sz0 = r00m + rn0 + R(2) * r00c;
+          d00 = (beta * (u0p - u00) + w * sz0) * (s3_iw<R>(P, fl00 | zA) * ih);
           S.f[0][t] = mc00 * d00;
           r00m = r00c;
           r00c = rn0;
-          const cplx rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
-          const cplx sz1 = r01m + rn1 + 2.0 * r01c;
-          S.f[2][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[zB | fl01] * ih));
+          const C rn1 = (v0m - vmm) + (v0p - vmp) + R(2) * (v00 - vm0);
+          const C sz1 = r01m + rn1 + R(2) * r01c;
+          S.f[2][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (s3_iw<R>(P, zB | fl01) * ih));
           r01m = r01c;
           r01c = rn1;
           S.di[1][t] = v00 - u00;  // d02 at edge (q, z+1)
-          S.q[qb][0][t] = (zin && q0ok) ? md(RHp[um - 1] + rp00, GAp[um - 1] + gp00, ix) * v00 : mk(0, 0);
+          S.q[qb][0][t] = (zin && q0ok) ? md(RHp[um - 1] + rp00, GAp[um - 1] + gp00, ix) * v00 : zc;
         }
         // ---- component 1: F11 (cell, +y pair, in-plane x), F10 (edge01, -x pair, in-plane y)
         {
-          const cplx vmm = V1[ui - S3_UX - 1], vm0 = V1[ui - S3_UX];
-          const cplx v0m = V1[ui - 1], v00 = V1[ui], v0p = V1[ui + 1];
-          const cplx vpm = V1[ui + S3_UX - 1], vp0 = V1[ui + S3_UX], vpp = V1[ui + S3_UX + 1];
-          const cplx u00 = U1[ui], up0 = U1[ui + S3_UX], u0m = U1[ui - 1];
-          const cplx rn0 = (vpm - v0m) + (vpp - v0p) + 2.0 * (vp0 - v00);
-          const cplx sz0 = r11m + rn0 + 2.0 * r11c;
-          d11 = (beta * (up0 - u00) + w * sz0) * (P.inv_wsum[zB | fl11] * ih);
+          const C vmm = V1[ui - S3_UX - 1], vm0 = V1[ui - S3_UX];
+          const C v0m = V1[ui - 1], v00 = V1[ui], v0p = V1[ui + 1];
+          const C vpm = V1[ui + S3_UX - 1], vp0 = V1[ui + S3_UX], vpp = V1[ui + S3_UX + 1];
+          const C u00 = U1[ui], up0 = U1[ui + S3_UX], u0m = U1[ui - 1];
+          const C rn0 = (vpm - v0m) + (vpp - v0p) + R(2) * (vp0 - v00);
+          const C sz0 = r11m + rn0 + R(2) * r11c;
+          d11 = (beta * (up0 - u00) + w * sz0) * (s3_iw<R>(P, zB | fl11) * ih);
           S.f[1][t] = mc00 * d11;
           r11m = r11c;
           r11c = rn0;
-          const cplx rn1 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
-          const cplx sz1 = r10m + rn1 + 2.0 * r10c;
-          S.f[3][t] = mu01 * ((beta * (u00 - u0m) + w * sz1) * (P.inv_wsum[zB | fl10] * ih));
+          const C rn1 = (vm0 - vmm) + (vp0 - vpm) + R(2) * (v00 - v0m);
+          const C sz1 = r10m + rn1 + R(2) * r10c;
+          S.f[3][t] = mu01 * ((beta * (u00 - u0m) + w * sz1) * (s3_iw<R>(P, zB | fl10) * ih));
           r10m = r10c;
           r10c = rn1;
           S.di[2][t] = v00 - u00;  // d12 at edge (q, z+1)
           S.q[qb][1][t] =
-              (zin && q1ok) ? md(RHp[um - S3_MX] + rp00, GAp[um - S3_MX] + gp00, iy) * v00 : mk(0, 0);
+              (zin && q1ok) ? md(RHp[um - S3_MX] + rp00, GAp[um - S3_MX] + gp00, iy) * v00 : zc;
         }
         // ---- component 2: F20 (edge02, -x pair, in-plane y), F21 (edge12, -y pair, in-plane x)
         {
-          const cplx vmm = V2[ui - S3_UX - 1], vm0 = V2[ui - S3_UX], vmp = V2[ui - S3_UX + 1];
-          const cplx v0m = V2[ui - 1], v00 = V2[ui], v0p = V2[ui + 1];
-          const cplx vpm = V2[ui + S3_UX - 1], vp0 = V2[ui + S3_UX];
-          const cplx u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - S3_UX];
-          const cplx rn0 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
-          const cplx sz0 = r20m + rn0 + 2.0 * r20c;
-          S.f[4][t] = mu02 * ((beta * (u00 - u0m) + w * sz0) * (P.inv_wsum[fl20 | zC] * ih));
+          const C vmm = V2[ui - S3_UX - 1], vm0 = V2[ui - S3_UX], vmp = V2[ui - S3_UX + 1];
+          const C v0m = V2[ui - 1], v00 = V2[ui], v0p = V2[ui + 1];
+          const C vpm = V2[ui + S3_UX - 1], vp0 = V2[ui + S3_UX];
+          const C u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - S3_UX];
+          const C rn0 = (vm0 - vmm) + (vp0 - vpm) + R(2) * (v00 - v0m);
+          const C sz0 = r20m + rn0 + R(2) * r20c;
+          S.f[4][t] = mu02 * ((beta * (u00 - u0m) + w * sz0) * (s3_iw<R>(P, fl20 | zC) * ih));
           r20m = r20c;
           r20c = rn0;
-          const cplx rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
-          const cplx sz1 = r21m + rn1 + 2.0 * r21c;
-          S.f[5][t] = mu12 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[fl21 | zC] * ih));
+          const C rn1 = (v0m - vmm) + (v0p - vmp) + R(2) * (v00 - vm0);
+          const C sz1 = r21m + rn1 + R(2) * r21c;
+          S.f[5][t] = mu12 * ((beta * (u00 - um0) + w * sz1) * (s3_iw<R>(P, fl21 | zC) * ih));
           r21m = r21c;
           r21c = rn1;
           S.di[0][t] = v00 - u00;  // d22 at cell (q, z)
           S.q[qb][2][t] = (zg + 1 >= 0 && zg + 1 <= n2g && q2ok)
                               ? md(RHc[um] + rp00, GAc[um] + gp00, izp) * v00
-                              : mk(0, 0);
+                              : zc;
         }
       }
       __syncthreads();
 
       if (interior) {
         // residual mode: fetch b for this plane's rows early (latency overlap)
-        cplx bb0 = mk(0, 0), bb1 = mk(0, 0), bb2 = mk(0, 0), bb3 = mk(0, 0);
+        C bb0 = zc, bb1 = zc, bb2 = zc, bb3 = zc;
         if (b && z >= zb) {
           if (v0 && z < n2) bb0 = __ldg(&b[o0 + s0 * z]);
           if (v1 && z < n2) bb1 = __ldg(&b[o1 + s1 * z]);
           if (v2) bb2 = __ldg(&b[o2 + s2 * z]);
           if (v2 && z < n2) bb3 = __ldg(&b[o3 + s2 * z]);
         }
-        auto filt = [&](const cplx* D) {
-          const cplx a = D[t - 1 - S3_FX] + D[t + 1 - S3_FX] + 2.0 * D[t - S3_FX];
-          const cplx c = D[t - 1 + S3_FX] + D[t + 1 + S3_FX] + 2.0 * D[t + S3_FX];
-          const cplx m_ = D[t - 1] + D[t + 1] + 2.0 * D[t];
-          return a + c + 2.0 * m_;
+        auto filt = [&](const C* D) {
+          const C a = D[t - 1 - S3_FX] + D[t + 1 - S3_FX] + R(2) * D[t - S3_FX];
+          const C c = D[t - 1 + S3_FX] + D[t + 1 + S3_FX] + R(2) * D[t + S3_FX];
+          const C m_ = D[t - 1] + D[t + 1] + R(2) * D[t];
+          return a + c + R(2) * m_;
         };
-        const cplx d22 = (beta * S.di[0][t] + w * filt(S.di[0])) * c22;
-        const cplx f22 = MUc[um] * d22;  // zero-filled mu masks cells outside the box
-        const double mu02p = (MUc[um - 1] + MUp[um - 1] + MUc[um] + MUp[um]) * (ix * izp);
-        const cplx f02p = mu02p * ((beta * S.di[1][t] + w * filt(S.di[1])) * c02);
-        const double mu12p = (MUc[um - S3_MX] + MUp[um - S3_MX] + MUc[um] + MUp[um]) * (iy * izp);
-        const cplx f12p = mu12p * ((beta * S.di[2][t] + w * filt(S.di[2])) * c12);
-        const cplx(*Q)[S3_FN] = S.q[z & 1];
-        const cplx qc0 = Q[0][t], qc1 = Q[1][t], qc2 = Q[2][t];
+        const C d22 = (beta * S.di[0][t] + w * filt(S.di[0])) * c22;
+        const C f22 = MUc[um] * d22;  // zero-filled mu masks cells outside the box
+        const R mu02p = (MUc[um - 1] + MUp[um - 1] + MUc[um] + MUp[um]) * (ix * izp);
+        const C f02p = mu02p * ((beta * S.di[1][t] + w * filt(S.di[1])) * c02);
+        const R mu12p = (MUc[um - S3_MX] + MUp[um - S3_MX] + MUc[um] + MUp[um]) * (iy * izp);
+        const C f12p = mu12p * ((beta * S.di[2][t] + w * filt(S.di[2])) * c12);
+        const C(*Q)[S3_FN] = S.q[z & 1];
+        const C qc0 = Q[0][t], qc1 = Q[1][t], qc2 = Q[2][t];
 
         if (z >= zb) {
-          const cplx(*QN)[S3_FN] = S.q[(z + 1) & 1];
-          const cplx* Pc = S.p[pc_];
-          const cplx pc = Pc[ui];
-          auto mass = [&](int k, cplx qc, cplx qm, int cnt) -> cplx {
-            cplx v = beta * qc;
+          const C(*QN)[S3_FN] = S.q[(z + 1) & 1];
+          const C* Pc = S.p[pc_];
+          const C pc = Pc[ui];
+          auto mass = [&](int k, C qc, C qm, int cnt) -> C {
+            C v = beta * qc;
             v += wn * Q[k][t - 1];
             v += wn * Q[k][t + 1];
             v += wn * Q[k][t - S3_FX];
             v += wn * Q[k][t + S3_FX];
             v += wn * qm;
             v += wn * QN[k][t];
-            return v * P.inv_msum[cnt];
+            return v * s3_im<R>(P, cnt);
           };
           const int czz = lz + hz0;
           if (v0 && z < n2) {  // u0 row (operator.hpp:389 / :409)
-            cplx out = (S.f[0][t - 1] - S.f[0][t]) * ih;
+            C out = (S.f[0][t - 1] - S.f[0][t]) * ih;
             out += (S.f[2][t] - S.f[2][t + S3_FX]) * ih;
             out += (f02c - f02p) * ih;
             out -= mass(0, qc0, qm0, mc0 + czz);
@@ -364,7 +456,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             y[o0 + s0 * z] = b ? bb0 - out : out;
           }
           if (v1 && z < n2) {  // u1 row
-            cplx out = (S.f[3][t] - S.f[3][t + 1]) * ih;
+            C out = (S.f[3][t] - S.f[3][t + 1]) * ih;
             out += (S.f[1][t - S3_FX] - S.f[1][t]) * ih;
             out += (f12c - f12p) * ih;
             out -= mass(1, qc1, qm1, mc1 + czz);
@@ -372,7 +464,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             y[o1 + s1 * z] = b ? bb1 - out : out;
           }
           if (v2) {  // u2 row (z <= n2)
-            cplx out = (S.f[4][t] - S.f[4][t + 1]) * ih;
+            C out = (S.f[4][t] - S.f[4][t + 1]) * ih;
             out += (S.f[5][t] - S.f[5][t + S3_FX]) * ih;
             out += (f22m - f22) * ih;
             out -= mass(2, qc2, qm2, mc2 + lz + hz1);
@@ -380,7 +472,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
             y[o2 + s2 * z] = b ? bb2 - out : out;
           }
           if (v2 && z < n2) {  // p row (operator.hpp:416)
-            cplx out = d00;
+            C out = d00;
             out += d11;
             out += d22;
             out += S.ilm[z & 3][um] * pc;
@@ -398,7 +490,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
       pm = pc_;
     }
     // drain the group issued by the last step before the next item reuses smem
-    s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+    if constexpr (kTma) s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+    else s3_cp_commit_wait();
     ++seq;
     __syncthreads();
   }
@@ -423,12 +516,25 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z
           wsum += w * (double)((s1 == 0 ? 2 : 1) * (s2 == 0 ? 2 : 1));
         }
     s.inv_wsum[f] = P.beta != 1.0 ? 1.0 / wsum : 1.0;
+    // operator.hpp:288 with Real = float
+    const float wf = (float)((1.0 - P.beta) / 16.0);
+    float wsf = (float)P.beta;
+    if (P.beta != 1.0)
+      for (int s1 = -1; s1 <= 1; ++s1)
+        for (int s2 = -1; s2 <= 1; ++s2) {
+          if ((s1 == -1 && !lo1) || (s1 == 1 && !hi1) || (s2 == -1 && !lo2) || (s2 == 1 && !hi2)) continue;
+          wsf += wf * (float)((s1 == 0 ? 2 : 1) * (s2 == 0 ? 2 : 1));
+        }
+    s.inv_wsum_f[f] = P.beta != 1.0 ? 1.0f / wsf : 1.0f;
   }
   s.wn = (1.0 - P.beta) / 6.0;
   for (int c = 0; c <= 6; ++c) {
     double wsum = P.beta;
     for (int q = 0; q < c; ++q) wsum += s.wn;
     s.inv_msum[c] = P.beta != 1.0 ? 1.0 / wsum : 1.0;
+    float wsf = (float)P.beta;
+    for (int q = 0; q < c; ++q) wsf += (float)s.wn;
+    s.inv_msum_f[c] = P.beta != 1.0 ? 1.0f / wsf : 1.0f;
   }
   s.ntiles_x = (g.n[0] + 1 + S3_TX - 1) / S3_TX;
   s.ntiles_y = (g.n[1] + 1 + S3_TY - 1) / S3_TY;
@@ -496,7 +602,9 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
   static int nsm = 0;
   const size_t smem = sizeof(S3Smem);
   if (!nsm) {
-    cudaFuncSetAttribute(k_stencil3d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stencil3d<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_stencil3d<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(S3SmemT<cplxf>));
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -546,7 +654,36 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
   if (sp.z_hi <= sp.z_lo) return;
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
-  k_stencil3d<<<grid, S3_THREADS, smem, s>>>(M, sp, b, y);
+  k_stencil3d<cplx><<<grid, S3_THREADS, smem, s>>>(M, S3Src{}, sp, b, y);
+}
+
+// complex64 variant (single-precision hierarchy): media_soa holds the four
+// float cell arrays; planes are loaded with cp.async, so no tensor maps.
+inline void launch_stencil3d(const Geo& g, const OpPar& P, const float* media_soa, const cplxf* x,
+                             const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  static int nsm = 0;
+  if (!nsm) {
+    cudaFuncSetAttribute(k_stencil3d<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S3Smem));
+    cudaFuncSetAttribute(k_stencil3d<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(S3SmemT<cplxf>));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int64_t nc = g.ncells;
+  S3Src src;
+  for (int k = 0; k < 3; ++k) src.u[k] = x + g.off[k];
+  src.p = x + g.off[3];
+  src.mu = media_soa;
+  src.rho = media_soa + nc;
+  src.gam = media_soa + 2 * nc;
+  src.ilm = media_soa + 3 * nc;
+  const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi);
+  if (sp.z_hi <= sp.z_lo) return;
+  const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
+  const int grid = items < nsm ? items : nsm;
+  k_stencil3d<cplxf><<<grid, S3_THREADS, sizeof(S3SmemT<cplxf>), s>>>(S3Maps{}, src, sp, b, y);
 }
 
 }  // namespace ehmg

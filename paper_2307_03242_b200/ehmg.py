@@ -44,7 +44,8 @@ _lib = None
 class _MgOpts(C.Structure):
     _fields_ = [("n_levels", C.c_int), ("cycle", C.c_int), ("nu1", C.c_int), ("nu2", C.c_int),
                 ("damping", C.c_double), ("vanka_mode", C.c_int), ("sweep", C.c_int),
-                ("k_inner_iterations", C.c_int), ("k_inner_rtol", C.c_double)]
+                ("k_inner_iterations", C.c_int), ("k_inner_rtol", C.c_double),
+                ("precision", C.c_int)]
 
 
 class _KOpts(C.Structure):
@@ -523,7 +524,12 @@ class Multigrid:
     """multigrid.hpp:70 -- shifted-Laplacian hierarchy resident in HBM."""
 
     def __init__(self, grid: StaggeredGrid, media: MediaModel, par: OperatorParams,
-                 opt: MgOptions):
+                 opt: MgOptions, precision: str = "double"):
+        """precision "mixed": complex64 hierarchy behind complex128
+        precondition()/cycle() (experiments.hpp:241 MixedPrecondition)."""
+        if precision not in ("double", "mixed"):
+            raise ValueError(f"config: unknown precision '{precision}'")
+        self.precision = precision
         if opt.cycle not in _CYCLES:
             raise ValueError(f"config: unknown cycle '{opt.cycle}'")
         if opt.coarse not in ("lu", "automatic"):
@@ -533,7 +539,7 @@ class Multigrid:
         self.grid, self.par, self.opt = grid, par, opt
         o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
                     0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
-                    opt.k_inner_iterations, opt.k_inner_rtol)
+                    opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0)
         arrs = media.arrays(grid)
         h = C.c_void_p()
         _check(lib().ehmg_multigrid_create(grid.ndim, _dims_arr(grid.dims), grid.h,
@@ -866,8 +872,11 @@ def run_solve(cfg: dict, seed: int = 1) -> dict:
     opt = MgOptions(n_levels=levels, cycle=cfg.get("cycle", "w"), nu1=cfg.get("nu1", 1),
                     nu2=cfg.get("nu2", 1), damping=w, vanka_mode=cfg.get("vanka", FULL),
                     sweep=cfg.get("order", RED_BLACK), coarse="lu")
+    precision = cfg.get("precision", "double")  # experiments.hpp:314
+    if precision not in ("double", "mixed"):
+        raise ValueError(f"config: unknown precision '{precision}'")
     D0 = make_opdata(g, media, OperatorParams(beta, omega, 0.0))
-    mg = Multigrid(g, media, OperatorParams(beta, omega, alpha), opt)
+    mg = Multigrid(g, media, OperatorParams(beta, omega, alpha), opt, precision=precision)
     comp = cfg.get("source_component", g.ndim)
     src = cfg.get("source_index", middle_of_top_row(g))
     b = make_point_source(g, comp, src)
@@ -877,5 +886,5 @@ def run_solve(cfg: dict, seed: int = 1) -> dict:
     res = fgmres(D0, mg, b, x, ko)
     secs = time.perf_counter() - t0
     return dict(grid="x".join(map(str, dims)), beta=beta, g_s=g_s, levels=levels, alpha=alpha,
-                w=w, omega=omega, iterations=res.iterations, final_relres=res.relres,
+                w=w, omega=omega, precision=precision, iterations=res.iterations, final_relres=res.relres,
                 wall_time_s=secs, status=res.status, history=res.history, solution=x)
