@@ -297,28 +297,32 @@ __global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict_
 // for the state at the start of the colour (vanka.hpp:205); every cell of
 // `color` solves its local system from r and adds w * correction to the DOFs
 // it owns. Cells of one colour share no DOFs, so the in-place writes commute.
-// T = cplx or cplxf storage (cache, residual, iterate); arithmetic in double.
+// T = cplx or cplxf: storage and arithmetic type (the single-precision
+// hierarchy updates in float, as the reference's VankaSmoother<float>).
 template <int ND, class T = cplx>
-__global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
+__global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 2 : 4) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
                                                            const T* __restrict__ r, int color, double w,
                                                            T* __restrict__ x) {
+  typedef typename VT<T>::R R;
   const int nu = full ? 4 : 2, cs = ND * nu + 1;
+  const T zero = VT<T>::mk(0, 0);
+  const R wr = (R)w;
   const int64_t nt = colour_threads(g);
   GRID_STRIDE(t, nt) {
     int c[3];
     if (!colour_cell(g, t, color, c)) continue;
     const T* q = soa + (int64_t)color * cs * nt + t;
-    auto Q = [&](int e) { return wide(q[(int64_t)e * nt]); };
+    auto Q = [&](int e) { return q[(int64_t)e * nt]; };
     const int64_t pi = g.off[ND] + g.clin(c);
     int64_t fi[ND][2];
-    cplx rr[ND][2];
-    cplx dpa = wide(r[pi]);
-    const cplx b0 = mk(V.ih, 0), b1 = mk(-V.ih, 0);
-    auto loadU = [&](int k, cplx* U) {
+    T rr[ND][2];
+    T dpa = r[pi];
+    const T b0 = VT<T>::mk((R)V.ih, 0), b1 = VT<T>::mk(-(R)V.ih, 0);
+    auto loadU = [&](int k, T* U) {
       if (full) {
         U[0] = Q(4 * k), U[1] = Q(4 * k + 1), U[2] = Q(4 * k + 2), U[3] = Q(4 * k + 3);
       } else {
-        U[0] = Q(2 * k), U[3] = Q(2 * k + 1), U[1] = U[2] = mk(0, 0);
+        U[0] = Q(2 * k), U[3] = Q(2 * k + 1), U[1] = U[2] = zero;
       }
     };
 #pragma unroll
@@ -327,22 +331,22 @@ __global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int f
       sh(c, k, 1, f1);
       fi[k][0] = g.off[k] + g.flin(k, c);
       fi[k][1] = g.off[k] + g.flin(k, f1);
-      rr[k][0] = wide(r[fi[k][0]]);
-      rr[k][1] = wide(r[fi[k][1]]);
-      cplx U[4];
+      rr[k][0] = r[fi[k][0]];
+      rr[k][1] = r[fi[k][1]];
+      T U[4];
       loadU(k, U);
-      const double c0 = vk_c0<ND>(V, g, k, c);
-      const cplx k0 = mk(c0, 0), k1 = mk(-c0, 0);
-      const cplx h0 = k0 * U[0] + k1 * U[2], h1 = k0 * U[1] + k1 * U[3];
+      const R c0 = (R)vk_c0<ND>(V, g, k, c);
+      const T k0 = VT<T>::mk(c0, 0), k1 = VT<T>::mk(-c0, 0);
+      const T h0 = k0 * U[0] + k1 * U[2], h1 = k0 * U[1] + k1 * U[3];
       dpa -= h0 * rr[k][0] + h1 * rr[k][1];
     }
-    const cplx dp = Q(cs - 1) * dpa;
+    const T dp = Q(cs - 1) * dpa;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      cplx U[4];
+      T U[4];
       loadU(k, U);  // second read hits L1
-      const cplx g0 = U[0] * b0 + U[1] * b1, g1 = U[2] * b0 + U[3] * b1;
-      cplx du0, du1;
+      const T g0 = U[0] * b0 + U[1] * b1, g1 = U[2] * b0 + U[3] * b1;
+      T du0, du1;
       if (full) {
         du0 = U[0] * rr[k][0] + U[1] * rr[k][1] - g0 * dp;
         du1 = U[2] * rr[k][0] + U[3] * rr[k][1] - g1 * dp;
@@ -350,10 +354,10 @@ __global__ void __launch_bounds__(kThreads) k_vanka_update(Geo g, VkPar V, int f
         du0 = U[0] * rr[k][0] - g0 * dp;
         du1 = U[3] * rr[k][1] - g1 * dp;
       }
-      x[fi[k][0]] = narrow<T>(wide(x[fi[k][0]]) + w * du0);
-      x[fi[k][1]] = narrow<T>(wide(x[fi[k][1]]) + w * du1);
+      x[fi[k][0]] += wr * du0;
+      x[fi[k][1]] += wr * du1;
     }
-    x[pi] = narrow<T>(wide(x[pi]) + w * dp);
+    x[pi] += wr * dp;
   }
 }
 

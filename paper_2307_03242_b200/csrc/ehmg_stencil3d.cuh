@@ -50,6 +50,19 @@ constexpr int S3_THREADS = ((S3_FN + 31) / 32) * 32;                         // 
 constexpr int S3_ZCHUNK = 32;
 constexpr unsigned S3_CBYTES = S3_UN * 16, S3_DBYTES = S3_MN * 8;  // one complex / double box
 
+// Tile height per element type: complex128 fits a 33x8 tile (11 warps at the
+// 168-register limit); complex64 halves the rings and the register file per
+// value, so a 33x16 tile (20 warps, 96 registers) runs with less halo work.
+template <class V> struct S3Cfg;
+template <> struct S3Cfg<cplx> {
+  static constexpr int TY = S3_TY, UY = S3_UY, UN = S3_UN, US = S3_US, MN = S3_MN, MS = S3_MS, FY = S3_FY,
+                       FN = S3_FN, THREADS = S3_THREADS;
+};
+template <> struct S3Cfg<cplxf> {
+  static constexpr int TY = 16, UY = TY + 4, UN = S3_UX * UY, US = (UN + 15) / 16 * 16, MN = S3_MX * UY,
+                       MS = (MN + 15) / 16 * 16, FY = TY + 2, FN = S3_FX * FY, THREADS = ((FN + 31) / 32) * 32;
+};
+
 struct S3Params {
   Geo g;
   double beta, omega2, alpha, w;  // w = (1-beta)/16
@@ -76,12 +89,13 @@ struct S3Maps {
 template <class V>
 struct __align__(128) S3SmemT {
   typedef typename VT<V>::R R;
-  V u[3][3][S3_US];  // [plane % 3][component]
-  V p[3][S3_US];     // [plane % 3]
-  R mu[4][S3_MS], rho[4][S3_MS], gam[4][S3_MS], ilm[4][S3_MS];  // [plane % 4], pitch S3_MX
-  V f[6][S3_FN];     // z-family fluxes at plane z: F00 F11 F01 F10 F20 F21
-  V di[3][S3_FN];    // in-plane difference fields: d22 (cell z), d02, d12 (edge z+1)
-  V q[2][3][S3_FN];  // mass products md*u [plane & 1][component]
+  typedef S3Cfg<V> K;
+  V u[3][3][K::US];  // [plane % 3][component]
+  V p[3][K::US];     // [plane % 3]
+  R mu[4][K::MS], rho[4][K::MS], gam[4][K::MS], ilm[4][K::MS];  // [plane % 4], pitch S3_MX
+  V f[6][K::FN];     // z-family fluxes at plane z: F00 F11 F01 F10 F20 F21
+  V di[3][K::FN];    // in-plane difference fields: d22 (cell z), d02, d12 (edge z+1)
+  V q[2][3][K::FN];  // mass products md*u [plane & 1][component]
   unsigned long long bar[2];
 };
 typedef S3SmemT<cplx> S3Smem;
@@ -161,7 +175,7 @@ __device__ __forceinline__ void s3_cp_commit_wait() {
 __device__ __forceinline__ void s3_cplane(cplxf* dst, const cplxf* base, int d0, int d1, int d2, int x0, int y0,
                                           int z) {
   const bool zin = z >= 0 && z < d2;
-  for (int e = threadIdx.x; e < S3_UN; e += blockDim.x) {
+  for (int e = threadIdx.x; e < S3Cfg<cplxf>::UN; e += blockDim.x) {
     const int r = e / S3_UX, j = e - r * S3_UX, x = x0 + j, y = y0 + r;
     if (zin && x >= 0 && x < d0 && y >= 0 && y < d1)
       s3_cp8(&dst[e], base + ((int64_t)z * d1 + y) * d0 + x);
@@ -172,7 +186,7 @@ __device__ __forceinline__ void s3_cplane(cplxf* dst, const cplxf* base, int d0,
 __device__ __forceinline__ void s3_mplane(float* dst, const float* base, int d0, int d1, int d2, int x0, int y0,
                                           int z) {
   const bool zin = z >= 0 && z < d2;
-  for (int e = threadIdx.x; e < S3_MN; e += blockDim.x) {
+  for (int e = threadIdx.x; e < S3Cfg<cplxf>::MN; e += blockDim.x) {
     const int r = e / S3_MX, j = e - r * S3_MX, x = x0 + j, y = y0 + r;
     if (zin && x >= 0 && x < d0 && y >= 0 && y < d1)
       s3_cp4(&dst[e], base + ((int64_t)z * d1 + y) * d0 + x);
@@ -205,10 +219,11 @@ __device__ __forceinline__ void s3_issue_ca(S3SmemT<cplxf>& S, const S3Src& M, c
 // V = C: complex128, planes by TMA. V = cplxf: complex64 arithmetic (the
 // single-precision hierarchy), planes by cp.async from `src`.
 template <class V>
-__global__ void __launch_bounds__(S3_THREADS, 1)
+__global__ void __launch_bounds__(S3Cfg<V>::THREADS, 1)
     k_stencil3d(const __grid_constant__ S3Maps maps, const __grid_constant__ S3Src src, const S3Params P,
                 const V* __restrict__ b, V* __restrict__ y) {
   typedef V C;
+  constexpr int S3_FN_ = S3Cfg<V>::FN, S3_TY_ = S3Cfg<V>::TY, S3_FY_ = S3Cfg<V>::FY;
   typedef typename VT<V>::R R;
   constexpr bool kTma = sizeof(R) == 8;
   const C zc = VT<V>::mk(0, 0);
@@ -216,10 +231,10 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
   S3SmemT<V>& S = *reinterpret_cast<S3SmemT<V>*>(s3_raw);
   const Geo& g = P.g;
   const int t = threadIdx.x;
-  const bool act = t < S3_FN;
+  const bool act = t < S3_FN_;
   const int fx = act ? t % S3_FX : 1, fy = act ? t / S3_FX : 1;
   const int ui = (fx + 1) + S3_UX * (fy + 1);  // own U-local index
-  const bool interior = act && fx >= 1 && fx <= S3_TX && fy >= 1 && fy <= S3_TY;
+  const bool interior = act && fx >= 1 && fx <= S3_TX && fy >= 1 && fy <= S3_TY_;
   const R beta = (R)P.beta, w = (R)P.w, ih = (R)g.inv_h, wn = (R)P.wn;
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];  // local storage extents
   const int zoff = g.zoff, n2g = g.gn2;               // global z semantics (slab windows)
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int tile = item % (P.ntiles_x * P.ntiles_y);
     const int chunk = item / (P.ntiles_x * P.ntiles_y);
-    const int i0 = (tile % P.ntiles_x) * S3_TX, j0 = (tile / P.ntiles_x) * S3_TY;
+    const int i0 = (tile % P.ntiles_x) * S3_TX, j0 = (tile / P.ntiles_x) * S3_TY_;
     const int zspan = P.z_hi - P.z_lo;
     const int zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
     const int zend = P.z_lo + (int)(((int64_t)(chunk + 1) * zspan) / P.nchunks);
@@ -429,11 +444,11 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
         const C f02p = mu02p * ((beta * S.di[1][t] + w * filt(S.di[1])) * c02);
         const R mu12p = (MUc[um - S3_MX] + MUp[um - S3_MX] + MUc[um] + MUp[um]) * (iy * izp);
         const C f12p = mu12p * ((beta * S.di[2][t] + w * filt(S.di[2])) * c12);
-        const C(*Q)[S3_FN] = S.q[z & 1];
+        const C(*Q)[S3_FN_] = S.q[z & 1];
         const C qc0 = Q[0][t], qc1 = Q[1][t], qc2 = Q[2][t];
 
         if (z >= zb) {
-          const C(*QN)[S3_FN] = S.q[(z + 1) & 1];
+          const C(*QN)[S3_FN_] = S.q[(z + 1) & 1];
           const C* Pc = S.p[pc_];
           const C pc = Pc[ui];
           auto mass = [&](int k, C qc, C qm, int cnt) -> C {
@@ -497,7 +512,8 @@ __global__ void __launch_bounds__(S3_THREADS, 1)
   }
 }
 
-inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z_lo = 0, int z_hi = -1) {
+inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z_lo = 0, int z_hi = -1,
+                               int ty = S3_TY) {
   S3Params s;
   s.g = g;
   s.beta = P.beta;
@@ -537,7 +553,7 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z
     s.inv_msum_f[c] = P.beta != 1.0 ? 1.0f / wsf : 1.0f;
   }
   s.ntiles_x = (g.n[0] + 1 + S3_TX - 1) / S3_TX;
-  s.ntiles_y = (g.n[1] + 1 + S3_TY - 1) / S3_TY;
+  s.ntiles_y = (g.n[1] + 1 + ty - 1) / ty;
   // z-chunks: minimise (rounds of persistent CTAs) x (planes per chunk + 2
   // warm-up planes) over chunk counts with >= 4 planes per chunk, so that
   // the tile x chunk items fill whole waves of the 148 SMs.
@@ -679,11 +695,11 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const float* media_so
   src.rho = media_soa + nc;
   src.gam = media_soa + 2 * nc;
   src.ilm = media_soa + 3 * nc;
-  const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi);
+  const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi, S3Cfg<cplxf>::TY);
   if (sp.z_hi <= sp.z_lo) return;
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
-  k_stencil3d<cplxf><<<grid, S3_THREADS, sizeof(S3SmemT<cplxf>), s>>>(S3Maps{}, src, sp, b, y);
+  k_stencil3d<cplxf><<<grid, S3Cfg<cplxf>::THREADS, sizeof(S3SmemT<cplxf>), s>>>(S3Maps{}, src, sp, b, y);
 }
 
 }  // namespace ehmg
