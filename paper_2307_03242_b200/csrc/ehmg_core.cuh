@@ -49,20 +49,59 @@ EH_HD cplx cdiv(cplx a, cplx b) {
 // MixedPrecondition): same operations on float2.
 typedef float2 cplxf;
 EH_HD cplxf mkf(float r, float i) { return make_float2(r, i); }
+#if defined(__CUDA_ARCH__)
+// Blackwell packed FP32 pairs (FADD2 / FMUL2 / FFMA2): one instruction per
+// complex64 add or real scale, two per complex product.
+__device__ __forceinline__ unsigned long long f2pk(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ cplxf f2up(unsigned long long r) {
+  cplxf o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ cplxf f2add(cplxf a, cplxf b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a.x, a.y)), "l"(f2pk(b.x, b.y)));
+  return f2up(r);
+}
+__device__ __forceinline__ cplxf f2sub(cplxf a, cplxf b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a.x, a.y)), "l"(f2pk(b.x, b.y)));
+  return f2up(r);
+}
+__device__ __forceinline__ cplxf f2scale(float s, cplxf a) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(s, s)), "l"(f2pk(a.x, a.y)));
+  return f2up(r);
+}
+__device__ __forceinline__ cplxf f2mul(cplxf a, cplxf b) {
+  unsigned long long t, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2pk(a.x, a.x)), "l"(f2pk(b.x, b.y)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pk(-a.y, a.y)), "l"(f2pk(b.y, b.x)), "l"(t));
+  return f2up(r);
+}
+EH_HD cplxf operator+(cplxf a, cplxf b) { return f2add(a, b); }
+EH_HD cplxf operator-(cplxf a, cplxf b) { return f2sub(a, b); }
+EH_HD cplxf operator*(float s, cplxf a) { return f2scale(s, a); }
+EH_HD cplxf operator*(cplxf a, float s) { return f2scale(s, a); }
+EH_HD cplxf operator*(cplxf a, cplxf b) { return f2mul(a, b); }
+#else
 EH_HD cplxf operator+(cplxf a, cplxf b) { return mkf(a.x + b.x, a.y + b.y); }
 EH_HD cplxf operator-(cplxf a, cplxf b) { return mkf(a.x - b.x, a.y - b.y); }
-EH_HD cplxf operator-(cplxf a) { return mkf(-a.x, -a.y); }
 EH_HD cplxf operator*(float s, cplxf a) { return mkf(s * a.x, s * a.y); }
 EH_HD cplxf operator*(cplxf a, float s) { return mkf(a.x * s, a.y * s); }
 EH_HD cplxf operator*(cplxf a, cplxf b) { return mkf(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+#endif
+EH_HD cplxf operator-(cplxf a) { return mkf(-a.x, -a.y); }
 EH_HD cplxf& operator+=(cplxf& a, cplxf b) {
-  a.x += b.x;
-  a.y += b.y;
+  a = a + b;
   return a;
 }
 EH_HD cplxf& operator-=(cplxf& a, cplxf b) {
-  a.x -= b.x;
-  a.y -= b.y;
+  a = a - b;
   return a;
 }
 
