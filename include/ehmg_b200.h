@@ -118,6 +118,26 @@ uint64_t ehmg_multigrid_stream(ehmg_mg mg);
 int ehmg_multigrid_time_precondition(ehmg_mg mg, const double* r_dev, double* z_dev, int count,
                                      double* ms);
 
+/* multigrid.hpp:56 MeasureOptions / :63 MeasureResult / :143
+ * measure_convergence_factor: stationary cycles from the reference's seeded
+ * random start; factor = geometric-mean residual reduction per cycle. */
+typedef struct {
+  int warmup;
+  double tol;
+  int max_cycles;
+  int growth_limit;
+} ehmg_measure_options;
+
+typedef struct {
+  double factor;
+  int cycles;
+  int diverged;
+  int n_history;
+} ehmg_measure_result;
+
+int ehmg_multigrid_measure_convergence(ehmg_mg mg, uint64_t seed, const ehmg_measure_options* mo,
+                                       ehmg_measure_result* res, double* history, int history_cap);
+
 /* ---- z-slab decomposed multigrid (north_star subsystem (6); no reference
  *      counterpart -- the reference is single-node CPU). Fine levels are split
  *      into z-slabs with 2 ghost planes exchanged after every field update;

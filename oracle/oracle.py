@@ -296,6 +296,10 @@ def ref():
                                          C.POINTER(C.c_int), C.POINTER(C.c_int),
                                          C.POINTER(C.c_double), _dp, C.c_int, C.POINTER(C.c_int)]
         L.ref_solve_mixed.argtypes = L.ref_solve.argtypes
+        L.ref_measure.argtypes = common + [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                           C.c_uint64, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                           _dp, C.c_int, C.POINTER(C.c_int)]
         _ref = L
     return _ref
 
@@ -373,3 +377,19 @@ def ref_solve(dims, h, media, beta, omega, alpha, b, n_levels=2, cycle="v", nu1=
                          C.byref(rr), hist, len(hist), C.byref(nh)))
     return x, dict(status=STATUS[st.value], iterations=it.value, relres=rr.value,
                    history=list(hist[:min(nh.value, len(hist))]))
+
+
+def ref_measure(dims, h, media, beta, omega, alpha, seed, n_levels=2, cycle="v", nu1=1, nu2=1,
+                damping=0.75, vanka="economic", sweep="lexicographic", warmup=5, tol=1e-9,
+                max_cycles=500, growth_limit=20, precision="double"):
+    """multigrid.hpp:143 measure_convergence_factor of the reference (restated
+    driver loop around the reference's cycle components)."""
+    f, cy, dv, nh = C.c_double(0), C.c_int(0), C.c_int(0), C.c_int(0)
+    hist = np.zeros(max_cycles + 8, np.float64)
+    _chk(ref().ref_measure(len(dims), _dims(dims), h, *media.arrays(), beta, omega, alpha, n_levels,
+                           CYCLES[cycle], nu1, nu2, damping, 0 if vanka == "full" else 1,
+                           1 if sweep == "red_black" else 0, seed, warmup, tol, max_cycles, growth_limit,
+                           1 if precision == "mixed" else 0, C.byref(f), C.byref(cy), C.byref(dv), hist,
+                           len(hist), C.byref(nh)))
+    return dict(factor=f.value, cycles=cy.value, diverged=bool(dv.value),
+                history=list(hist[:min(nh.value, len(hist))]))

@@ -331,6 +331,64 @@ int solve_t(const int* dims, double h, Media M, double beta, double omega, doubl
   return 0;
 }
 
+// multigrid.hpp:143 measure_convergence_factor restated around the
+// restated cycle (RefMGT::cyc) and the reference's apply/norm/scal.
+template <class Real, int Dim>
+int measure_t(const int* dims, double h, Media M, double beta, double omega, double alpha, int nl, int cyc,
+              int nu1, int nu2, double w, int vmode, int sweep, std::uint64_t seed, int warmup, double tol,
+              int max_cycles, int growth_limit, double* factor, int* cycles, int* diverged, double* hist,
+              int hist_cap, int* n_hist) {
+  StaggeredGrid<Dim> g(to_idx<Dim>(dims), h);
+  auto media = media_of<Dim>(g, M.lam, M.mu, M.rho, M.gam);
+  RefMGT<Real, Dim> mg(g, media, OperatorParams{beta, omega, alpha, false}, nl, cyc, nu1, nu2, w, vmode, sweep);
+  using C = std::complex<Real>;
+  auto& D = mg.L[0]->D;
+  auto x = make_field(D), zero = make_field(D), t = make_field(D);
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  for (auto& comp : x.comp)
+    for (auto& v : comp) v = C(Real(dist(rng)), Real(dist(rng)));
+  for (int i = 0; i < warmup; ++i) mg.cyc(0, zero, x);
+  auto rnorm = [&]() {
+    apply_mixed_operator(D, x, t);
+    return norm(t);
+  };
+  double r0 = rnorm();
+  *factor = 0.0;
+  *cycles = 0;
+  *diverged = 0;
+  *n_hist = 0;
+  if (r0 == 0.0) return 0;
+  scal(C(Real(1.0 / r0)), x);
+  std::vector<double> hs;
+  double prev = 1.0;
+  int growths = 0;
+  while (*cycles < max_cycles) {
+    mg.cyc(0, zero, x);
+    ++*cycles;
+    double rn = rnorm();
+    hs.push_back(rn);
+    if (rn > prev) {
+      if (++growths >= growth_limit) {
+        *diverged = 1;
+        break;
+      }
+    } else {
+      growths = 0;
+    }
+    prev = rn;
+    if (rn < tol) break;
+    if (!std::isfinite(rn) || rn > 1e12) {
+      *diverged = 1;
+      break;
+    }
+  }
+  *factor = std::pow(hs.empty() ? 1.0 : hs.back(), 1.0 / std::max(1, *cycles));
+  *n_hist = int(hs.size());
+  for (int i = 0; i < std::min(hist_cap, int(hs.size())); ++i) hist[i] = hs[size_t(i)];
+  return 0;
+}
+
 template <class F> int guard(F&& f) {
   try {
     return f();
@@ -419,6 +477,21 @@ int ref_solve(int ndim, const int* dims, double h, const double* lam, const doub
   return guard([&] {
     return ndim == 2 ? solve_t<2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist)
                      : solve_t<3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, restart, max_it, rtol, b, x, iters, status, relres, hist, hist_cap, n_hist);
+  });
+}
+
+int ref_measure(int ndim, const int* dims, double h, const double* lam, const double* mu, const double* rho,
+                const double* gam, double beta, double omega, double alpha, int nl, int cyc, int nu1, int nu2,
+                double w, int vmode, int sweep, std::uint64_t seed, int warmup, double tol, int max_cycles,
+                int growth_limit, int mixed, double* factor, int* cycles, int* diverged, double* hist,
+                int hist_cap, int* n_hist) {
+  Media M{lam, mu, rho, gam};
+  return guard([&] {
+    if (ndim == 2)
+      return mixed ? measure_t<float, 2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, seed, warmup, tol, max_cycles, growth_limit, factor, cycles, diverged, hist, hist_cap, n_hist)
+                   : measure_t<double, 2>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, seed, warmup, tol, max_cycles, growth_limit, factor, cycles, diverged, hist, hist_cap, n_hist);
+    return mixed ? measure_t<float, 3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, seed, warmup, tol, max_cycles, growth_limit, factor, cycles, diverged, hist, hist_cap, n_hist)
+                 : measure_t<double, 3>(dims, h, M, beta, omega, alpha, nl, cyc, nu1, nu2, w, vmode, sweep, seed, warmup, tol, max_cycles, growth_limit, factor, cycles, diverged, hist, hist_cap, n_hist);
   });
 }
 

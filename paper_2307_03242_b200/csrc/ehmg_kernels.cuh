@@ -670,6 +670,11 @@ __global__ void __launch_bounds__(kThreads) k_convert(int64_t n, const S* __rest
   GRID_STRIDE(i, n) dst[i] = narrow<D>(wide(src[i]));
 }
 
+template <class V>
+__global__ void __launch_bounds__(kThreads) k_scale_real(int64_t n, typename VT<V>::R s, V* __restrict__ x) {
+  GRID_STRIDE(i, n) x[i] = s * x[i];
+}
+
 __global__ void k_identity(int64_t N, cplx* __restrict__ B) {
   GRID_STRIDE(i, N * N) { B[i] = (i / N == i % N) ? mk(1, 0) : mk(0, 0); }
 }
@@ -689,17 +694,18 @@ __device__ __forceinline__ double warp_sum<double>(double v) {
 // to finish sums the partials in block order. mode 0: <x,y> (conj x),
 // mode 1: ||x||^2. Result (re, im) to out[0..1]; optional negated copy to
 // coef (the MGS axpy coefficient) and accumulation into hacc.
-__global__ void __launch_bounds__(kThreads) k_reduce(int mode, int64_t n, const cplx* __restrict__ x,
-                                                     const cplx* __restrict__ y, double2* __restrict__ partial,
+template <class V = cplx>
+__global__ void __launch_bounds__(kThreads) k_reduce(int mode, int64_t n, const V* __restrict__ x,
+                                                     const V* __restrict__ y, double2* __restrict__ partial,
                                                      unsigned* __restrict__ counter, double* __restrict__ out,
                                                      double* __restrict__ coef, double* __restrict__ hacc) {
   double sr = 0, si = 0;
   GRID_STRIDE(i, n) {
-    cplx a = x[i];
+    const cplx a = wide(x[i]);
     if (mode == 1) {
       sr += a.x * a.x + a.y * a.y;
     } else {
-      cplx bb = y[i];
+      const cplx bb = wide(y[i]);
       sr += a.x * bb.x + a.y * bb.y;
       si += a.x * bb.y - a.y * bb.x;
     }

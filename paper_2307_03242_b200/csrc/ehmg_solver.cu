@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <random>
 #include <cstdio>
 #include <cstdlib>
@@ -1007,6 +1008,76 @@ static std::unique_ptr<ehmg_mg_s> build_mg(const Geo& g, const double* const* ho
 
 #include "ehmg_slab.cuh"
 
+// multigrid.hpp:143 measure_convergence_factor: stationary cycles on the
+// homogeneous problem from a seeded random start (the reference's
+// std::mt19937_64 / uniform(-1, 1) draws, re and im per value in component
+// order), residual norm ||H x|| of the level-0 (shifted) operator.
+template <class V>
+static void measure_t(ehmg_mg_s& mg, uint64_t seed, const ehmg_measure_options& mo, ehmg_measure_result* res,
+                      double* history, int cap) {
+  typedef typename VT<V>::R Real;
+  typedef std::complex<Real> C;
+  Level& fl = *mg.L[0];
+  const int64_t n = fl.g.ndofs;
+  cudaStream_t s = mg.s;
+  std::vector<C> hx((size_t)n);
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  for (auto& v : hx) v = C(Real(dist(rng)), Real(dist(rng)));  // same expression as the reference
+  DBuf<V> x(n), zero(n), t(n);
+  DBuf<double2> partial(kRedBlocks);
+  DBuf<unsigned> counter(1);
+  DBuf<double> out(2);
+  counter.zero(s);
+  zero.zero(s);
+  CK(cudaMemcpyAsync(x.p, hx.data(), sizeof(V) * n, cudaMemcpyHostToDevice, s));
+  auto rnorm = [&]() {
+    launch_residual(fl.g, fl.P, fl.media.ref(), (const V*)x.p, (const V*)nullptr, t.p, s);
+    k_reduce<V><<<kRedBlocks, kThreads, 0, s>>>(1, n, t.p, nullptr, partial.p, counter.p, out.p, nullptr, nullptr);
+    CK(cudaGetLastError());
+    double h2[2];
+    CK(cudaMemcpyAsync(h2, out.p, sizeof(h2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return std::sqrt(h2[0]);
+  };
+  for (int i = 0; i < mo.warmup; ++i) mg.cycle_t<V>(0, zero.p, x.p, false);
+  const double r0 = rnorm();
+  res->factor = 0.0;
+  res->cycles = 0;
+  res->diverged = 0;
+  res->n_history = 0;
+  if (r0 == 0.0) return;
+  const Real sc = Real(1.0 / r0);
+  k_scale_real<V><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, sc, x.p);
+  CK(cudaGetLastError());
+  std::vector<double> hist;
+  double prev = 1.0;
+  int growths = 0;
+  while (res->cycles < mo.max_cycles) {
+    mg.cycle_t<V>(0, zero.p, x.p, false);
+    ++res->cycles;
+    const double rn = rnorm();
+    hist.push_back(rn);
+    if (rn > prev) {
+      if (++growths >= mo.growth_limit) {
+        res->diverged = 1;
+        break;
+      }
+    } else {
+      growths = 0;
+    }
+    prev = rn;
+    if (rn < mo.tol) break;
+    if (!std::isfinite(rn) || rn > 1e12) {
+      res->diverged = 1;
+      break;
+    }
+  }
+  res->factor = std::pow(hist.empty() ? 1.0 : hist.back(), 1.0 / std::max(1, res->cycles));
+  res->n_history = (int)hist.size();
+  for (int i = 0; i < std::min(cap, (int)hist.size()); ++i) history[i] = hist[(size_t)i];
+}
+
 // ------------------------------------------------------------------ C ABI
 extern "C" {
 
@@ -1530,6 +1601,15 @@ int ehmg_multigrid_precondition(ehmg_mg mg, const double* r, double* z, int wher
     cplx* dz = out_dev(z, mg->hx, n, where);
     mg->precondition(dr, dz);
     from_dev(z, dz, n, where, mg->s);
+  });
+}
+
+int ehmg_multigrid_measure_convergence(ehmg_mg mg, uint64_t seed, const ehmg_measure_options* mo,
+                                       ehmg_measure_result* res, double* history, int cap) {
+  return guard([&] {
+    if (!mo || !res) throw Err(EHMG_EINVAL, "measure: null options or result");
+    if (mg->prec == 0) measure_t<cplx>(*mg, seed, *mo, res, history, cap);
+    else measure_t<cplxf>(*mg, seed, *mo, res, history, cap);
   });
 }
 

@@ -48,6 +48,16 @@ class _MgOpts(C.Structure):
                 ("precision", C.c_int)]
 
 
+class _MOpts(C.Structure):
+    _fields_ = [("warmup", C.c_int), ("tol", C.c_double), ("max_cycles", C.c_int),
+                ("growth_limit", C.c_int)]
+
+
+class _MRes(C.Structure):
+    _fields_ = [("factor", C.c_double), ("cycles", C.c_int), ("diverged", C.c_int),
+                ("n_history", C.c_int)]
+
+
 class _KOpts(C.Structure):
     _fields_ = [("restart", C.c_int), ("max_iterations", C.c_int), ("rtol", C.c_double),
                 ("stall_factor", C.c_double), ("stall_cycles", C.c_int)]
@@ -87,6 +97,8 @@ def lib():
         L.ehmg_prolong_field.argtypes = [C.c_int, ip, vp, vp, C.c_int]
         L.ehmg_coarsen_media.argtypes = [C.c_int, ip, vp, vp]
         L.ehmg_layered_media.argtypes = [C.c_int, ip, C.c_double, C.c_uint64, vp, vp, vp, vp]
+        L.ehmg_multigrid_measure_convergence.argtypes = [vp, C.c_uint64, C.POINTER(_MOpts),
+                                                         C.POINTER(_MRes), vp, C.c_int]
         L.ehmg_attenuation_profile.argtypes = [C.c_int, ip, C.c_double, C.c_int, C.c_double,
                                                C.c_int, vp]
         L.ehmg_multigrid_create.argtypes = [C.c_int, ip, C.c_double, vp, vp, vp, vp, C.c_double,
@@ -520,6 +532,24 @@ class MgOptions:
     k_inner_rtol: float = 0.25
 
 
+@dataclasses.dataclass
+class MeasureOptions:
+    """multigrid.hpp:56"""
+    warmup: int = 5
+    tol: float = 1e-9
+    max_cycles: int = 500
+    growth_limit: int = 20
+
+
+@dataclasses.dataclass
+class MeasureResult:
+    """multigrid.hpp:63"""
+    factor: float
+    cycles: int
+    diverged: bool
+    history: list
+
+
 class Multigrid:
     """multigrid.hpp:70 -- shifted-Laplacian hierarchy resident in HBM."""
 
@@ -574,6 +604,18 @@ class Multigrid:
             raise ValueError("b and x must both be host arrays or both device tensors")
         _check(lib().ehmg_multigrid_cycle(self._h, pb, px, wx))
         return x
+
+    def measure_convergence_factor(self, seed: int, mo: MeasureOptions = None) -> MeasureResult:
+        """multigrid.hpp:143 -- stationary cycles on the homogeneous problem from
+        the reference's seeded random start; geometric-mean reduction factor."""
+        mo = mo or MeasureOptions()
+        o = _MOpts(mo.warmup, mo.tol, mo.max_cycles, mo.growth_limit)
+        r = _MRes()
+        hist = np.zeros(mo.max_cycles + 8, np.float64)
+        _check(lib().ehmg_multigrid_measure_convergence(self._h, int(seed) & (2**64 - 1), C.byref(o),
+                                                        C.byref(r), hist.ctypes.data, len(hist)))
+        return MeasureResult(r.factor, r.cycles, bool(r.diverged),
+                             list(hist[:min(r.n_history, len(hist))]))
 
     def precondition(self, r, z=None):
         """multigrid.hpp:136 -- z = one cycle from zero applied to r."""
