@@ -468,10 +468,31 @@ def run_b200_slabs(args, ws, rank, local):
     value = args.steps / (ms_max / 1e3)
     barrier(ws)
     # per-launch profile of one application on this rank -> launches per step
+    # and the dominant kernel's roofline on this rank's window
     E.profile_enable(True)
     d.time_precondition(r, 1)
-    launches_per_step = sum(c for (_, _, c, _) in E.profile_report())
+    prof = E.profile_report()
     E.profile_enable(False)
+    launches_per_step = sum(c for (_, _, c, _) in prof)
+    z0w, z1w, w0w, w1w = d.window()
+    kname, klev, kcount, kms = max(prof, key=lambda t: t[3])
+    wd = (n >> klev, n >> klev, max(1, (w1w - w0w) >> klev))
+    C = wd[0] * wd[1] * wd[2]
+    Nw = ndofs(wd)
+    nbytes = {"residual": 16 * 3 * Nw + 32 * C, "apply": 16 * 2 * Nw + 32 * C,
+              "vanka_update": 16 * 13 * (C // 2) + 3 * 16 * (Nw - C + C // 2)}.get(kname, 0)
+    peak, peak_src = load_peaks()
+    # an overlapped apply is split into interior + boundary-row launches:
+    # count whole-window evaluations (V(2,2): 3 pre-smoothing applies after
+    # the zero-start colour, 1 for the restriction, 4 post-smoothing)
+    evals = {"residual": 8, "vanka_update": 8}.get(kname, kcount)
+    per_eval = kms / evals
+    achieved = nbytes / (per_eval / 1e3) / 1e9 if nbytes else 0.0
+    roofline = {"bound": "hbm", "kernel": f"{kname}@L{klev} (rank-0 window {wd[0]}x{wd[1]}x{wd[2]})",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "alg_bytes_per_launch": nbytes, "avg_launch_ms": round(per_eval, 4),
+                "launches_per_eval": round(kcount / evals, 2), "peak_source": peak_src}
     barrier(ws)
     e_steps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
@@ -499,6 +520,12 @@ def run_b200_slabs(args, ws, rank, local):
         "e2e": {"value": round(e_steps / (e2e_ms / 1e3), 4), "unit": "V-cycles/s",
                 "h2d_bytes_per_step": 16 * N // ws, "d2h_bytes_per_step": 16 * N // ws},
         "halo_bytes_per_step_rank0": int(halo), "slab_rank0": [z0, z1, w0, w1],
+        # halo traffic against NVLink 5 (900 GB/s per direction per GPU): the
+        # bandwidth the exchanges would need if spread over the whole cycle
+        "halo_vs_nvlink": {"GBps_over_cycle": round(halo / (ms_max / args.steps / 1e3) / 1e9, 2),
+                           "nvlink_GBps_per_direction": 900.0,
+                           "frac": round(halo / (ms_max / args.steps / 1e3) / 1e9 / 900.0, 4)},
+        "roofline": roofline,
         "gmres_time_to_1e-6": solve, "setup_s": round(setup_s, 2), "clocks": clocks,
         "gpu_launches": int(launches_per_step * args.steps),
     }
