@@ -37,7 +37,12 @@ sys.path.insert(0, ROOT)
 NCU_TRAFFIC = {"residual@L0": 3004467000 + 1062199000,
                "source": "profiles/round1/ncu_stencil3d_t33.txt (ncu --set full, 256^3 residual)"}
 N_CELLS = 256
-LEVELS = 5
+LEVELS = 5  # at 256^3: coarsest level 16^3 cells (17^3 nodes), BASELINE configs[2]
+
+
+def levels_for(n):
+    """levels coarsening n^3 cells down to 16^3 (the BASELINE's 17^3 nodes)"""
+    return max(2, int(round(math.log2(n))) - 3)
 BETA = 2.0 / 3.0
 ALPHA = 0.5          # shift (see DESIGN.md: the 0.1 default stalls at 5 levels)
 DAMPING = 0.25       # experiments.hpp:221 default for >= 4 levels
@@ -47,16 +52,16 @@ LAM, MU, RHO = 2.0, 1.0, 1.0   # cs = 1, cp = 2
 PPW = 10.0
 
 
-def metric_name():
-    return "V-cycles/s (complex128) at 257^3 3D elastic Helmholtz"
+def metric_name(n=256):
+    return f"V-cycles/s (complex128) at {n + 1}^3 3D elastic Helmholtz"
 
 
 def workload_config(n):
     return {"workload": f"configs[2]: 3D homogeneous {n + 1}^3 nodes ({n}^3 cells), h=1/{n}",
             "media": "lambda=2 mu=1 rho=1 (cs=1, cp=2)", "omega": f"2*pi/({PPW:g}h)",
             "sponge_cells": SPONGE, "gamma_phys": GAMMA_PHYS, "beta": BETA, "alpha": ALPHA,
-            "cycle": "V(2,2) full red-black Vanka", "levels": LEVELS,
-            "coarsest": f"{n >> (LEVELS - 1)}^3 exact (LU-derived inverse in HBM)",
+            "cycle": "V(2,2) full red-black Vanka", "levels": levels_for(n),
+            "coarsest": f"{n >> (levels_for(n) - 1)}^3 exact (LU-derived inverse in HBM)",
             "damping": DAMPING, "source": "unit point source, x-component, centre",
             "krylov": "FGMRES(10), rtol 1e-6",
             "l2": (f"inputs ({field_gb(n):.2f} GB/field) larger than the 126 MB L2" if field_gb(n) > 0.126
@@ -273,7 +278,7 @@ def run_b200(args, ws, rank, local):
     E.lib().ehmg_set_device(local)
     n = args.n
     g, med, omega = build_problem(n, E)
-    opt = E.MgOptions(n_levels=LEVELS, cycle="v", nu1=2, nu2=2, damping=DAMPING,
+    opt = E.MgOptions(n_levels=levels_for(n), cycle="v", nu1=2, nu2=2, damping=DAMPING,
                       vanka_mode="full", sweep="red_black")
     t0 = time.perf_counter()
     mg = E.Multigrid(g, med, E.OperatorParams(BETA, omega, ALPHA), opt)
@@ -378,6 +383,7 @@ def run_b200(args, ws, rank, local):
     # hierarchy behind the complex128 FGMRES -- reported beside the headline
     mixed = None
     if args.mixed:
+        del mg  # the complex128 hierarchy is done: free HBM for the complex64 one
         mgm = E.Multigrid(g, med, E.OperatorParams(BETA, omega, ALPHA), opt, precision="mixed")
         for _ in range(args.warmup):
             mgm.precondition(r, z)
@@ -403,7 +409,7 @@ def run_b200(args, ws, rank, local):
         del mgm
 
     line = {
-        "metric": metric_name(), "value": round(value, 4), "unit": "V-cycles/s",
+        "metric": metric_name(n), "value": round(value, 4), "unit": "V-cycles/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
@@ -447,7 +453,7 @@ def run_b200_slabs(args, ws, rank, local):
     job = obj[0]
     n = args.n
     g, med, omega = build_problem(n, E)
-    opt = E.MgOptions(n_levels=LEVELS, cycle="v", nu1=2, nu2=2, damping=DAMPING,
+    opt = E.MgOptions(n_levels=levels_for(n), cycle="v", nu1=2, nu2=2, damping=DAMPING,
                       vanka_mode="full", sweep="red_black")
     t0 = time.perf_counter()
     d = E.DistributedSlabSolver(job, rank, ws, dev, g, med, E.OperatorParams(BETA, omega, ALPHA),
@@ -512,7 +518,7 @@ def run_b200_slabs(args, ws, rank, local):
     cfg = workload_config(n)
     cfg["parallelism"] = f"z-slab x{ws} (levels <= 64^3 agglomerated)"
     return {
-        "metric": metric_name(), "value": round(value, 4), "unit": "V-cycles/s", "n_gpus": ws,
+        "metric": metric_name(n), "value": round(value, 4), "unit": "V-cycles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "complex128 (f64)", "data": "synthetic (BASELINE configs[2] media recipe)",

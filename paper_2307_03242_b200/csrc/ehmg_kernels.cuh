@@ -260,17 +260,22 @@ __device__ __forceinline__ void vk_expand(const VkPar& V, const Geo& g, int full
 // Compact cache re-laid out per colour, component-major (SoA): entry e of
 // the cell with colour index t of colour col lives at soa[(col*cs + e)*nt + t],
 // so a warp of same-colour cells reads each entry fully coalesced.
+// aos holds the cells of planes [c0, c0 + cz) (a build chunk); colour
+// threads of those planes are the contiguous range [c0 P, (c0 + cz) P).
 template <int ND>
-__global__ void k_vanka_to_soa(Geo g, int full, const cplx* __restrict__ aos, cplx* __restrict__ soa) {
+__global__ void k_vanka_to_soa(Geo g, int full, const cplx* __restrict__ aos, cplx* __restrict__ soa, int c0,
+                               int cz) {
   const int stride = ND * ((full ? 4 : 2) + 4) + 1, blk = full ? 8 : 6, nu = full ? 4 : 2;
   const int cs = ND * nu + 1;
   const int64_t nt = colour_threads(g);
-  GRID_STRIDE(u, 2 * nt) {
-    const int col = (int)(u / nt);
-    const int64_t t = u % nt;
+  const int64_t P = nt / g.n[2], span = P * cz;
+  const int64_t plane = (int64_t)g.n[0] * g.n[1];
+  GRID_STRIDE(u, 2 * span) {
+    const int col = (int)(u / span);
+    const int64_t t = (int64_t)c0 * P + u % span;
     int c[3];
     if (!colour_cell(g, t, col, c)) continue;
-    const cplx* a = aos + g.clin(c) * stride;
+    const cplx* a = aos + (g.clin(c) - (int64_t)c0 * plane) * stride;
     for (int k = 0; k < ND; ++k)
       for (int e = 0; e < nu; ++e) soa[((int64_t)col * cs + k * nu + e) * nt + t] = a[k * blk + e];
     soa[((int64_t)col * cs + cs - 1) * nt + t] = a[stride - 1];

@@ -324,25 +324,34 @@ struct Smoother {
     const Geo g = z1 < 0 ? gg : make_window(gg, z0, z1);
     const int nz = z1 < 0 ? gg.n[2] : z1 - z0;
     {
-      DBuf<cplx> aos(g.ncells * stride);
+      // factorise in z-chunks of <= 8M cells: the reference-layout scratch
+      // (25 complex per 3D cell) never exceeds ~3.4 GB, so 513^3 builds fit
+      const int64_t plane = (int64_t)g.n[0] * g.n[1];
+      const int cz_max = g.nd == 3 ? (int)std::max<int64_t>(1, ((int64_t)8 << 20) / plane) : 1;
+      const int nzc = g.nd == 3 ? nz : 1;
+      DBuf<cplx> aos(plane * std::min(cz_max, nzc) * stride);
       DBuf<int> bad(1);
       bad.zero(s);
-      if (g.nd == 3)
-        k_vanka_build<3><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(gg, P, m, full, aos.p, bad.p, z0, nz);
-      else
-        k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(gg, P, m, full, aos.p, bad.p, 0, 1);
-      CK(cudaGetLastError());
+      const int64_t nt = colour_threads(g);
+      vk = make_vkpar(g, P);
+      soa.alloc(2 * nt * (g.nd * (full ? 4 : 2) + 1));
+      for (int c0 = 0; c0 < nzc; c0 += cz_max) {
+        const int cz = std::min(cz_max, nzc - c0);
+        if (g.nd == 3) {
+          k_vanka_build<3><<<grid_for(plane * cz, 148 * 64), kThreads, 0, s>>>(gg, P, m, full, aos.p, bad.p,
+                                                                             z0 + c0, cz);
+          k_vanka_to_soa<3><<<grid_for(2 * (nt / g.n[2]) * cz, 148 * 64), kThreads, 0, s>>>(g, full, aos.p, soa.p,
+                                                                                          c0, cz);
+        } else {
+          k_vanka_build<2><<<grid_for(g.ncells, 148 * 64), kThreads, 0, s>>>(gg, P, m, full, aos.p, bad.p, 0, 1);
+          k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, full, aos.p, soa.p, 0, 1);
+        }
+        CK(cudaGetLastError());
+      }
       int hb = 0;
       CK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (hb) throw Err(EHMG_ERUNTIME, "vanka: singular local cell system");
-      const int64_t nt = colour_threads(g);
-      vk = make_vkpar(g, P);
-      soa.alloc(2 * nt * (g.nd * (full ? 4 : 2) + 1));
-      if (g.nd == 3) k_vanka_to_soa<3><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, full, aos.p, soa.p);
-      else k_vanka_to_soa<2><<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, full, aos.p, soa.p);
-      CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(s));
     }
     res.alloc(g.ndofs);
   }

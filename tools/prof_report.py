@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--precision", default="double")
     a = ap.parse_args()
     g, med, omega = bench.build_problem(a.n, E)
-    opt = E.MgOptions(n_levels=bench.LEVELS, cycle="v", nu1=2, nu2=2, damping=bench.DAMPING,
+    opt = E.MgOptions(n_levels=bench.levels_for(a.n), cycle="v", nu1=2, nu2=2, damping=bench.DAMPING,
                       vanka_mode="full", sweep="red_black")
     mg = E.Multigrid(g, med, E.OperatorParams(bench.BETA, omega, bench.ALPHA), opt,
                      precision=a.precision)
