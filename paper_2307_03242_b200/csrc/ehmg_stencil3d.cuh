@@ -29,6 +29,7 @@
 
 #include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 
+#include <mutex>
 #include <vector>
 
 #include "ehmg_core.cuh"
@@ -611,21 +612,32 @@ inline bool stencil3d_supported(const Geo& g) {
   return g.nd == 3 && g.n[0] >= 2 && g.n[1] >= 2 && g.n[0] % 2 == 0 && s3_encoder() != nullptr;
 }
 
+// Per-device one-time setup (the shared-memory opt-in is a per-device
+// function attribute); returns the SM count of the current device.
+inline int s3_device_init() {
+  static std::mutex mu;
+  static int nsm_of[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!nsm_of[dev]) {
+    cudaFuncSetAttribute(k_stencil3d<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S3Smem));
+    cudaFuncSetAttribute(k_stencil3d<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(S3SmemT<cplxf>));
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    nsm_of[dev] = nsm > 0 ? nsm : 148;
+  }
+  return nsm_of[dev];
+}
+
 // media_soa: 4 consecutive cell arrays {mu, rho, gamma, 1/(lambda+mu)}.
 // Output planes [z_lo, z_hi) (default: all, including the top u2 faces).
 inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
                              const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
-  static int nsm = 0;
+  const int nsm = s3_device_init();
   const size_t smem = sizeof(S3Smem);
-  if (!nsm) {
-    cudaFuncSetAttribute(k_stencil3d<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_stencil3d<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(S3SmemT<cplxf>));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
   // tensor maps depend only on (buffer, media, dims): cache them so the
   // per-launch host cost is a lookup (buffers are fixed per level).
   struct Entry {
@@ -636,6 +648,8 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
   };
   static std::vector<Entry> cache;
   static size_t next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const S3Maps* Mp = nullptr;
   for (const Entry& e : cache)
@@ -677,16 +691,7 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
 // float cell arrays; planes are loaded with cp.async, so no tensor maps.
 inline void launch_stencil3d(const Geo& g, const OpPar& P, const float* media_soa, const cplxf* x,
                              const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
-  static int nsm = 0;
-  if (!nsm) {
-    cudaFuncSetAttribute(k_stencil3d<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S3Smem));
-    cudaFuncSetAttribute(k_stencil3d<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(S3SmemT<cplxf>));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
+  const int nsm = s3_device_init();
   const int64_t nc = g.ncells;
   S3Src src;
   for (int k = 0; k < 3; ++k) src.u[k] = x + g.off[k];

@@ -80,7 +80,7 @@ def test_3d_hierarchy_matches_reference(sweep):
 
 def test_3d_bench_shape_red_black_full():
     """3D, several TMA tiles and chunks, 3 levels, the bench's smoother."""
-    dims = (48, 40, 32)
+    dims = (36, 24, 16)
     g, med, om = hom(dims, 2.0)
     par = E.OperatorParams(2 / 3, TAU * dims[0] / 10, 0.5)
     opt = E.MgOptions(n_levels=3, cycle="v", nu1=2, nu2=2, damping=0.35, vanka_mode="full", sweep="red_black")
