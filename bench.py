@@ -537,6 +537,52 @@ def run_b200_slabs(args, ws, rank, local):
     }
 
 
+def run_b200_sources(args, ws, rank, local):
+    """BASELINE configs[4] (second part): independent preconditioned FGMRES
+    solves for surface point sources on the 257^3 grid, distributed across
+    the GPUs (one hierarchy per GPU, sources round-robin). value = solves/s."""
+    import torch
+    import paper_2307_03242_b200 as E
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    E.lib().ehmg_set_device(dev)
+    n = args.n
+    g, med, omega = build_problem(n, E)
+    opt = E.MgOptions(n_levels=levels_for(n), cycle="v", nu1=2, nu2=2, damping=DAMPING,
+                      vanka_mode="full", sweep="red_black")
+    mg = E.Multigrid(g, med, E.OperatorParams(BETA, omega, ALPHA), opt)
+    D0 = E.make_opdata(g, med, E.OperatorParams(BETA, omega, 0.0))
+    N = g.n_dofs()
+    # a 4 x 8 pattern of vertical point forces 2 cells below the free top surface
+    pos = [(int((i + 0.5) * n / 8), int((j + 0.5) * n / 4), 2) for j in range(4) for i in range(8)]
+    pos = pos[:args.sources]
+    mine = [p for k, p in enumerate(pos) if k % ws == rank]
+    x = torch.zeros(N, dtype=torch.complex128, device="cuda")
+    warm = torch.from_numpy(E.make_point_source(g, 2, pos[0])).cuda()
+    E.fgmres(D0, mg, warm, x, E.KrylovOptions(restart=10, max_iterations=3))  # graphs, lazy setup
+    barrier(ws)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    its = []
+    for p in mine:
+        b = torch.from_numpy(E.make_point_source(g, 2, p)).cuda()
+        x.zero_()
+        res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+        its.append(res.iterations)
+    torch.cuda.synchronize()
+    secs = max_over_ranks(ws, time.perf_counter() - t0)
+    cfg = workload_config(n)
+    cfg["workload"] = f"configs[4] sources: {len(pos)} surface point sources on {n + 1}^3, independent solves"
+    cfg["parallelism"] = f"{ws} GPUs, sources round-robin (no data-path collective)"
+    return {"metric": "solves/s (FGMRES(10) to 1e-6, complex128)", "value": round(len(pos) / secs, 5),
+            "unit": "solves/s", "n_gpus": ws, "steps": len(pos), "warmup": 1,
+            "ms_per_step": round(secs * 1e3 / max(1, len(pos)), 2), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "complex128 (f64)",
+            "data": "synthetic (BASELINE configs[2] media; point sources)", "config": cfg,
+            "iterations_rank0": its, "e2e": None, "gpu_launches": None}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
@@ -570,12 +616,15 @@ def main():
     ap.add_argument("--mixed", type=int, default=1, help="also time the complex64-hierarchy mode")
     ap.add_argument("--max-it", type=int, default=600)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--mode", choices=["slabs", "replicas"], default="slabs",
+    ap.add_argument("--sources", type=int, default=32, help="--mode sources: number of point sources")
+    ap.add_argument("--mode", choices=["slabs", "replicas", "sources"], default="slabs",
                     help="N > 1: z-slab decomposition (strong) or independent replicas (weak)")
     args = ap.parse_args()
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         line = run_reference(args, ws, rank)
+    elif args.mode == "sources":
+        line = run_b200_sources(args, ws, rank, local)
     elif ws > 1 and args.mode == "slabs":
         line = run_b200_slabs(args, ws, rank, local)
     else:
