@@ -31,6 +31,7 @@
 #include "../../include/ehmg_b200.h"
 #include "ehmg_comm.cuh"
 #include "ehmg_kernels.cuh"
+#include "ehmg_stencil2d.cuh"
 #include "ehmg_stencil3d.cuh"
 
 namespace ehmg {
@@ -238,7 +239,7 @@ static void launch_residual(const Geo& g, const OpPar& P, const MediaRef& mr, co
   } else if (g.nd == 3) {
     k_apply_generic<3><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
   } else {
-    k_apply_generic<2><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
+    launch_stencil2d<cplx>(g, P, m, x, b, y, s);
   }
   CK(cudaGetLastError());
 }
@@ -253,7 +254,7 @@ static void launch_residual(const Geo& g, const OpPar& P, const MediaRef& mr, co
   } else if (g.nd == 3) {
     k_apply_generic<3, cplxf><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
   } else {
-    k_apply_generic<2, cplxf><<<grid_for(g.ndofs, 148 * 64), kThreads, 0, s>>>(g, P, m, x, b, y);
+    launch_stencil2d<cplxf>(g, P, m, x, b, y, s);
   }
   CK(cudaGetLastError());
 }
