@@ -424,6 +424,8 @@ def run_b200(args, ws, rank, local):
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": NCU_TRAFFIC.get(f"{kname}@L{klev}") if n == N_CELLS else None,
                      "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
+                     "limiter": ("FP64 issue + shared-memory latency at the 11-warp register limit "
+                                 "(ncu: IPC 1.44, FP64 pipe 26%, DRAM 18%); see DESIGN.md"),
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "clocks": clocks,
     }
