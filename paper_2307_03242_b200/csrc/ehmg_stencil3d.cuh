@@ -463,37 +463,31 @@ __global__ void __launch_bounds__(S3Cfg<V>::THREADS, 1)
             return v * s3_im<R>(P, cnt);
           };
           const int czz = lz + hz0;
-          if (v0 && z < n2) {  // u0 row (operator.hpp:389 / :409)
-            C out = (S.f[0][t - 1] - S.f[0][t]) * ih;
-            out += (S.f[2][t] - S.f[2][t + S3_FX]) * ih;
-            out += (f02c - f02p) * ih;
-            out -= mass(0, qc0, qm0, mc0 + czz);
-            out += (pc - Pc[ui - 1]) * ih;
-            y[o0 + s0 * z] = b ? bb0 - out : out;
-          }
-          if (v1 && z < n2) {  // u1 row
-            C out = (S.f[3][t] - S.f[3][t + 1]) * ih;
-            out += (S.f[1][t - S3_FX] - S.f[1][t]) * ih;
-            out += (f12c - f12p) * ih;
-            out -= mass(1, qc1, qm1, mc1 + czz);
-            out += (pc - Pc[ui - S3_UX]) * ih;
-            y[o1 + s1 * z] = b ? bb1 - out : out;
-          }
-          if (v2) {  // u2 row (z <= n2)
-            C out = (S.f[4][t] - S.f[4][t + 1]) * ih;
-            out += (S.f[5][t] - S.f[5][t + S3_FX]) * ih;
-            out += (f22m - f22) * ih;
-            out -= mass(2, qc2, qm2, mc2 + lz + hz1);
-            out += (pc - S.p[pm][ui]) * ih;
-            y[o2 + s2 * z] = b ? bb2 - out : out;
-          }
-          if (v2 && z < n2) {  // p row (operator.hpp:416)
-            C out = d00;
-            out += d11;
-            out += d22;
-            out += S.ilm[z & 3][um] * pc;
-            y[o3 + s2 * z] = b ? bb3 - out : out;
-          }
+          // all four rows evaluated unconditionally (one basic block: the
+          // scheduler overlaps their shared-memory loads); stores predicated
+          C o0v = (S.f[0][t - 1] - S.f[0][t]) * ih;
+          o0v += (S.f[2][t] - S.f[2][t + S3_FX]) * ih;
+          o0v += (f02c - f02p) * ih;
+          o0v -= mass(0, qc0, qm0, mc0 + czz);
+          o0v += (pc - Pc[ui - 1]) * ih;
+          C o1v = (S.f[3][t] - S.f[3][t + 1]) * ih;
+          o1v += (S.f[1][t - S3_FX] - S.f[1][t]) * ih;
+          o1v += (f12c - f12p) * ih;
+          o1v -= mass(1, qc1, qm1, mc1 + czz);
+          o1v += (pc - Pc[ui - S3_UX]) * ih;
+          C o2v = (S.f[4][t] - S.f[4][t + 1]) * ih;
+          o2v += (S.f[5][t] - S.f[5][t + S3_FX]) * ih;
+          o2v += (f22m - f22) * ih;
+          o2v -= mass(2, qc2, qm2, mc2 + lz + hz1);
+          o2v += (pc - S.p[pm][ui]) * ih;
+          C o3v = d00;
+          o3v += d11;
+          o3v += d22;
+          o3v += S.ilm[z & 3][um] * pc;
+          if (v0 && z < n2) y[o0 + s0 * z] = b ? bb0 - o0v : o0v;
+          if (v1 && z < n2) y[o1 + s1 * z] = b ? bb1 - o1v : o1v;
+          if (v2) y[o2 + s2 * z] = b ? bb2 - o2v : o2v;
+          if (v2 && z < n2) y[o3 + s2 * z] = b ? bb3 - o3v : o3v;
         }
         f02c = f02p;
         f12c = f12p;
