@@ -33,6 +33,7 @@
 #include "ehmg_kernels.cuh"
 #include "ehmg_stencil2d.cuh"
 #include "ehmg_stencil3d.cuh"
+#include "ehmg_stencil3d_rr.cuh"
 
 namespace ehmg {
 

@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(S3Cfg<V>::THREADS, 1)
 }
 
 inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z_lo = 0, int z_hi = -1,
-                               int ty = S3_TY) {
+                               int ty = S3_TY, int tx = S3_TX) {
   S3Params s;
   s.g = g;
   s.beta = P.beta;
@@ -547,7 +547,7 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z
     for (int q = 0; q < c; ++q) wsf += (float)s.wn;
     s.inv_msum_f[c] = P.beta != 1.0 ? 1.0f / wsf : 1.0f;
   }
-  s.ntiles_x = (g.n[0] + 1 + S3_TX - 1) / S3_TX;
+  s.ntiles_x = (g.n[0] + 1 + tx - 1) / tx;
   s.ntiles_y = (g.n[1] + 1 + ty - 1) / ty;
   // z-chunks: minimise (rounds of persistent CTAs) x (planes per chunk + 2
   // warm-up planes) over chunk counts with >= 4 planes per chunk, so that
@@ -616,7 +616,6 @@ inline int s3_device_init() {
   if (dev < 0 || dev >= 64) dev = 0;
   std::lock_guard<std::mutex> lock(mu);
   if (!nsm_of[dev]) {
-    cudaFuncSetAttribute(k_stencil3d<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S3Smem));
     cudaFuncSetAttribute(k_stencil3d<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(S3SmemT<cplxf>));
     int nsm = 0;
@@ -624,61 +623,6 @@ inline int s3_device_init() {
     nsm_of[dev] = nsm > 0 ? nsm : 148;
   }
   return nsm_of[dev];
-}
-
-// media_soa: 4 consecutive cell arrays {mu, rho, gamma, 1/(lambda+mu)}.
-// Output planes [z_lo, z_hi) (default: all, including the top u2 faces).
-inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
-                             const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
-  const int nsm = s3_device_init();
-  const size_t smem = sizeof(S3Smem);
-  // tensor maps depend only on (buffer, media, dims): cache them so the
-  // per-launch host cost is a lookup (buffers are fixed per level).
-  struct Entry {
-    const void* x;
-    const void* m;
-    int n[3];
-    S3Maps M;
-  };
-  static std::vector<Entry> cache;
-  static size_t next = 0;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
-  const S3Maps* Mp = nullptr;
-  for (const Entry& e : cache)
-    if (e.x == x && e.m == media_soa && e.n[0] == n0 && e.n[1] == n1 && e.n[2] == n2) {
-      Mp = &e.M;
-      break;
-    }
-  if (!Mp) {
-    Entry e;
-    e.x = x;
-    e.m = media_soa;
-    e.n[0] = n0, e.n[1] = n1, e.n[2] = n2;
-    for (int k = 0; k < 3; ++k)
-      s3_encode(&e.M.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * S3_UX);
-    s3_encode(&e.M.p, x + g.off[3], 2 * n0, n1, n2, 2 * S3_UX);
-    const int64_t nc = g.ncells;
-    s3_encode(&e.M.mu, media_soa + 0 * nc, n0, n1, n2, S3_MX);
-    s3_encode(&e.M.rho, media_soa + 1 * nc, n0, n1, n2, S3_MX);
-    s3_encode(&e.M.gam, media_soa + 2 * nc, n0, n1, n2, S3_MX);
-    s3_encode(&e.M.ilm, media_soa + 3 * nc, n0, n1, n2, S3_MX);
-    if (cache.size() < 256) {
-      cache.push_back(e);
-      Mp = &cache.back().M;
-    } else {
-      cache[next] = e;
-      Mp = &cache[next].M;
-      next = (next + 1) % cache.size();
-    }
-  }
-  const S3Maps M = *Mp;
-  const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi);
-  if (sp.z_hi <= sp.z_lo) return;
-  const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
-  const int grid = items < nsm ? items : nsm;
-  k_stencil3d<cplx><<<grid, S3_THREADS, smem, s>>>(M, S3Src{}, sp, b, y);
 }
 
 // complex64 variant (single-precision hierarchy): media_soa holds the four

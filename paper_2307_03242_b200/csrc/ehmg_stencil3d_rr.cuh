@@ -1,0 +1,495 @@
+// ehmg_stencil3d_rr.cuh -- register-resident complex128 3D operator / residual.
+//
+// y = H x  or  r = b - H x  for the staggered mixed elastic-Helmholtz
+// operator (operator.hpp:389-421), all four components in one launch; the
+// complex128 production kernel (k_stencil3d<cplxf> in ehmg_stencil3d.cuh
+// serves the complex64 hierarchy).
+//
+// Why this shape. The 11-warp kernel (33x8 tiles, 352 threads) sat at the
+// 168-register cap of three warps per SM sub-partition and moved every
+// neighbour value through shared memory: ncu showed the LSU shared-memory
+// pipe ~70% busy and it, not HBM, bounded the launch. Here:
+//  * 8 warps (2 per sub-partition: 255-register cap). The thread grid is the
+//    32x8 flux window of a 30x6 output tile: lane = x, warp = y. Each thread
+//    keeps its own fluxes, mass products and the z-carried quantities in
+//    registers.
+//  * x-neighbour exchanges of computed values (F00, F10, F20, mass products,
+//    p) are warp shuffles; only y-neighbour fluxes (F11, F01, F21) and mass
+//    products go through shared memory.
+//  * The z-difference families (F02, F12, F22) spread in-plane: the spread of
+//    (plane z+1 - plane z) is the difference of the per-plane spreads (zero
+//    ghosts make the boundary terms vanish in both), so each plane's spread
+//    is formed once from the 3x3 neighbourhood already in registers and
+//    carried to the next plane.
+//  * The edge averages mu02, mu12 of planes (z-1, z) are the previous
+//    plane's (z, z+1) averages, carried: the media ring holds 3 planes.
+//  * Planes stream in by TMA (cp.async.bulk.tensor, mbarrier), one plane
+//    ahead; the hardware zero fill supplies the reference's zero ghosts
+//    (operator.hpp:172 GhostAcc).
+// Results follow the reference's per-term operation order except the
+// in-plane spread noted above (differences of spreads; <= 1e-15 relative).
+#pragma once
+
+#include "ehmg_stencil3d.cuh"
+
+namespace ehmg {
+
+constexpr int R3_TX = 30, R3_TY = 6;               // output columns / rows per tile
+constexpr int R3_FX = 32, R3_FY = 8;               // flux window = thread grid
+constexpr int R3_THREADS = R3_FX * R3_FY;          // 256
+constexpr int R3_UX = R3_FX + 2, R3_UY = R3_FY + 2;  // u / p / media window, origin (i0-2, j0-2)
+constexpr int R3_UN = R3_UX * R3_UY;
+constexpr int R3_US = (R3_UN + 7) / 8 * 8;    // complex slot stride: 128-byte aligned TMA destinations
+constexpr int R3_MS = (R3_UN + 15) / 16 * 16;  // double slot stride
+constexpr unsigned R3_CBYTES = R3_UN * 16, R3_DBYTES = R3_UN * 8;
+
+struct __align__(128) R3Smem {
+  cplx u[3][3][R3_US];  // [plane % 3][component]
+  cplx p[3][R3_US];     // [plane % 3]
+  double mu[3][R3_MS], rho[3][R3_MS], gam[3][R3_MS], ilm[3][R3_MS];  // [plane % 3]
+  cplx fy[3][R3_THREADS];     // y-exchanged fluxes at plane z: F11, F01, F21
+  cplx q[2][3][R3_THREADS];   // mass products md*u [plane & 1][component]
+  cplx bp[2][4][R3_THREADS];  // residual mode: b rows of the thread grid [plane & 1][component]
+  unsigned long long bar[2];
+};
+
+// x, media and (residual mode) b tensor maps; b boxes cover the thread grid.
+struct R3Maps {
+  S3Maps m;
+  CUtensorMap b[4];
+};
+constexpr unsigned R3_BBYTES = R3_THREADS * 16;
+
+__device__ __forceinline__ cplx r3_up(cplx v) {  // value of lane - 1
+  return mk(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ cplx r3_dn(cplx v) {  // value of lane + 1
+  return mk(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+__device__ __forceinline__ void r3_issue(R3Smem& S, const R3Maps& RM, int i0, int j0, int zu, int nu, int zm,
+                                         int nm, int zp, int np, bool hasb, int zb_, unsigned long long* bar) {
+  const S3Maps& M = RM.m;
+  s3_expect(bar, (unsigned)(nu * 3 * R3_CBYTES + nm * 4 * R3_DBYTES + np * R3_CBYTES + (hasb ? 4 * R3_BBYTES : 0)));
+  if (hasb)
+    for (int k = 0; k < 4; ++k) s3_tma(S.bp[zb_ & 1][k], &RM.b[k], 2 * (i0 - 1), j0 - 1, zb_, bar);
+  const int cx = 2 * (i0 - 2), cy = j0 - 2, mx = i0 - 2;  // i0 even: 16-byte aligned media start
+  for (int q = 0; q < nu; ++q) {
+    const int sl = s3_mod3(zu + q);
+    s3_tma(S.u[sl][0], &M.u[0], cx, cy, zu + q, bar);
+    s3_tma(S.u[sl][1], &M.u[1], cx, cy, zu + q, bar);
+    s3_tma(S.u[sl][2], &M.u[2], cx, cy, zu + q, bar);
+  }
+  for (int q = 0; q < nm; ++q) {
+    const int sl = s3_mod3(zm + q);
+    s3_tma(S.mu[sl], &M.mu, mx, cy, zm + q, bar);
+    s3_tma(S.rho[sl], &M.rho, mx, cy, zm + q, bar);
+    s3_tma(S.gam[sl], &M.gam, mx, cy, zm + q, bar);
+    s3_tma(S.ilm[sl], &M.ilm, mx, cy, zm + q, bar);
+  }
+  for (int q = 0; q < np; ++q) s3_tma(S.p[s3_mod3(zp + q)], &M.p, cx, cy, zp + q, bar);
+}
+
+// Per-item constants of one thread's position.
+struct R3Pos {
+  int ui, t, fy, i0, j0, zb, xg, yg;
+  double ix, iy, mu01s;
+  int fl00, fl11, fl01, fl10, fl20, fl21, i22, i02, i12, mc0, mc1, mc2;
+  bool interior, v0, v1, v2, q0ok, q1ok, q2ok;
+};
+
+// Quantities carried from plane to plane. Two instances alternate roles
+// (cur = newest values, nxt = the older ones, overwritten by this plane's
+// results), and the z loop is unrolled by two with the roles swapped, so the
+// carries stay in place instead of being copied register to register.
+struct R3Carry {
+  cplx r00, r11, r01, r10, r20, r21;  // z-family row sums: cur = plane z, nxt = plane z-1 -> z+1
+  cplx t0, t1, t2;                    // in-plane spreads of u0, u1, u2: cur = plane z
+  cplx f02, f12, f22;                 // in-plane family fluxes of the previous step
+  cplx q0, q1, q2;                    // mass products: cur = plane z, nxt = plane z-1 -> z+1
+  cplx p;                             // p at plane z-1 (cur) -> plane z (nxt)
+  double mu02, mu12;                  // edge averages of planes (z-1, z) (cur) -> (z, z+1) (nxt)
+};
+
+__device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3Params& P, const R3Pos& Q,
+                                        const cplx* __restrict__ b, cplx* __restrict__ y, int z, int& su0,
+                                        unsigned& seq, R3Carry& cur, R3Carry& nxt) {
+  typedef cplx C;
+  const C zc = mk(0.0, 0.0);
+  const Geo& g = P.g;
+  const int ui = Q.ui, t = Q.t, fy = Q.fy;
+  const double beta = P.beta, w = P.w, ih = g.inv_h, wn = P.wn;
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int n2g = g.gn2;
+
+  s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+  ++seq;
+  __syncthreads();  // all of step z-1 done: its slots may be refilled
+  if (t == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    r3_issue(S, maps, Q.i0, Q.j0, z + 2, 1, z + 2, 1, z + 1, 1, b != nullptr, z + 1, &S.bar[seq & 1]);
+  }
+  const int s0 = su0, s1 = su0 == 2 ? 0 : su0 + 1;
+  su0 = s1;
+  const C* U0 = S.u[s0][0];
+  const C* U1 = S.u[s0][1];
+  const C* U2 = S.u[s0][2];
+  const C* V0 = S.u[s1][0];
+  const C* V1 = S.u[s1][1];
+  const C* V2 = S.u[s1][2];
+  const double* MUc = S.mu[s0];
+  const double* MUp = S.mu[s1];
+  const double* RHc = S.rho[s0];
+  const double* RHp = S.rho[s1];
+  const double* GAc = S.gam[s0];
+  const double* GAp = S.gam[s1];
+  // uniform z quantities (global plane index zg decides the boundary rules)
+  const int zg = z + g.zoff;
+  const int lz = zg >= 1, hz0 = zg + 1 < n2g, hz1 = zg + 1 < n2g + 1;
+  const double izp = s3_inv<double>((zg + 1 >= 1) + (zg + 1 < n2g));
+  const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
+  const double al = P.alpha, w2 = P.omega2;
+  auto md = [&](double sr, double sg, double ic) {
+    const double rho_f = sr * ic, gam_f = sg * ic + al;
+    return mk(w2 * rho_f, -w2 * gam_f * rho_f);
+  };
+  const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
+  const bool zin2 = zg + 1 >= 0 && zg + 1 <= n2g;
+  C(*SQn)[R3_THREADS] = S.q[(z + 1) & 1];
+
+  // values the row evaluation after the barrier needs (rows 1..TY only)
+  C m0, m1, m2, o0v, o1v, o2v, o3v, pt0, pt1, pt2;
+  {
+  // ---- every flux family at this position (halo rows and columns too:
+  // skipping the unused families there costs more in warp imbalance at the
+  // barriers than it saves). Each result is
+  // consumed as soon as it exists (shuffled, stored or folded into a row) to
+  // keep live ranges short at the 255-register cap.
+  const double mc00 = MUc[ui], mc_l = MUc[ui - 1], mc_b = MUc[ui - R3_UX], mc_lb = MUc[ui - 1 - R3_UX];
+  const double mp00 = MUp[ui], mp_l = MUp[ui - 1], mp_b = MUp[ui - R3_UX];
+  const double rp00 = RHp[ui], gp00 = GAp[ui];
+  // mu on the edges (operator.hpp:108 order: first axis outer, second inner)
+  const double mu01 = (mc_lb + mc_l + mc_b + mc00) * Q.mu01s;
+  const double mu02p = (mc_l + mp_l + mc00 + mp00) * (Q.ix * izp);  // edges (z, z+1)
+  const double mu12p = (mc_b + mp_b + mc00 + mp00) * (Q.iy * izp);
+  auto spread = [](C mm, C m0_, C mp, C zm, C z0, C zp, C pm, C p0, C pp) {
+    const C a = mm + mp + 2.0 * m0_;
+    const C c = pm + pp + 2.0 * p0;
+    const C m_ = zm + zp + 2.0 * z0;
+    return a + c + 2.0 * m_;
+  };
+  // mass: beta*q + the x neighbours (shuffles) + the z-1 neighbour (the older
+  // carried product, whose register the new product then takes); the y
+  // neighbours and z+1 follow after the barrier
+  auto mass_head = [&](C qc, C qm) {
+    C m = beta * qc;
+    m += wn * r3_up(qc);
+    m += wn * r3_dn(qc);
+    m += wn * qm;
+    return m;
+  };
+  // ---- component 0: F00 (cell, +x pair), F01 (edge01, -y pair), F02 (edge02, +z pair)
+  {
+    const C vmm = V0[ui - R3_UX - 1], vm0 = V0[ui - R3_UX], vmp = V0[ui - R3_UX + 1];
+    const C v0m = V0[ui - 1], v00 = V0[ui], v0p = V0[ui + 1];
+    const C vpm = V0[ui + R3_UX - 1], vp0 = V0[ui + R3_UX], vpp = V0[ui + R3_UX + 1];
+    const C u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - R3_UX];
+    const C rn0 = (vmp - vm0) + (vpp - vp0) + 2.0 * (v0p - v00);
+    const C sz0 = (nxt.r00 + 2.0 * cur.r00) + rn0;
+    nxt.r00 = rn0;
+    const C d00 = (beta * (u0p - u00) + w * sz0) * (P.inv_wsum[Q.fl00 | zA] * ih);
+    o3v = d00;
+    const C f0 = mc00 * d00;
+    o0v = (r3_up(f0) - f0) * ih;
+    const C rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
+    const C sz1 = (nxt.r01 + 2.0 * cur.r01) + rn1;
+    nxt.r01 = rn1;
+    S.fy[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[zB | Q.fl01] * ih));
+    const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
+    nxt.f02 = mu02p * ((beta * (v00 - u00) + w * (tn - cur.t0)) * (P.inv_wsum[Q.i02] * ih));
+    nxt.t0 = tn;
+    m0 = mass_head(cur.q0, nxt.q0);
+    nxt.q0 = (zin && Q.q0ok) ? md(RHp[ui - 1] + rp00, GAp[ui - 1] + gp00, Q.ix) * v00 : zc;
+    SQn[0][t] = nxt.q0;
+  }
+  // ---- component 1: F11 (cell, +y pair), F10 (edge01, -x pair), F12 (edge12, +z pair)
+  {
+    const C vmm = V1[ui - R3_UX - 1], vm0 = V1[ui - R3_UX], vmp = V1[ui - R3_UX + 1];
+    const C v0m = V1[ui - 1], v00 = V1[ui], v0p = V1[ui + 1];
+    const C vpm = V1[ui + R3_UX - 1], vp0 = V1[ui + R3_UX], vpp = V1[ui + R3_UX + 1];
+    const C u00 = U1[ui], up0 = U1[ui + R3_UX], u0m = U1[ui - 1];
+    const C rn0 = (vpm - v0m) + (vpp - v0p) + 2.0 * (vp0 - v00);
+    const C sz0 = (nxt.r11 + 2.0 * cur.r11) + rn0;
+    nxt.r11 = rn0;
+    const C d11 = (beta * (up0 - u00) + w * sz0) * (P.inv_wsum[zB | Q.fl11] * ih);
+    o3v += d11;
+    S.fy[0][t] = mc00 * d11;
+    const C rn1 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
+    const C sz1 = (nxt.r10 + 2.0 * cur.r10) + rn1;
+    nxt.r10 = rn1;
+    const C f3 = mu01 * ((beta * (u00 - u0m) + w * sz1) * (P.inv_wsum[zB | Q.fl10] * ih));
+    o1v = (f3 - r3_dn(f3)) * ih;
+    const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
+    nxt.f12 = mu12p * ((beta * (v00 - u00) + w * (tn - cur.t1)) * (P.inv_wsum[Q.i12] * ih));
+    nxt.t1 = tn;
+    m1 = mass_head(cur.q1, nxt.q1);
+    nxt.q1 = (zin && Q.q1ok) ? md(RHp[ui - R3_UX] + rp00, GAp[ui - R3_UX] + gp00, Q.iy) * v00 : zc;
+    SQn[1][t] = nxt.q1;
+  }
+  // ---- component 2: F20 (edge02, -x pair), F21 (edge12, -y pair), F22 (cell, +z pair)
+  {
+    const C vmm = V2[ui - R3_UX - 1], vm0 = V2[ui - R3_UX], vmp = V2[ui - R3_UX + 1];
+    const C v0m = V2[ui - 1], v00 = V2[ui], v0p = V2[ui + 1];
+    const C vpm = V2[ui + R3_UX - 1], vp0 = V2[ui + R3_UX], vpp = V2[ui + R3_UX + 1];
+    const C u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - R3_UX];
+    const C rn0 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
+    const C sz0 = (nxt.r20 + 2.0 * cur.r20) + rn0;
+    nxt.r20 = rn0;
+    const C f4 = cur.mu02 * ((beta * (u00 - u0m) + w * sz0) * (P.inv_wsum[Q.fl20 | zC] * ih));
+    o2v = (f4 - r3_dn(f4)) * ih;
+    const C rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
+    const C sz1 = (nxt.r21 + 2.0 * cur.r21) + rn1;
+    nxt.r21 = rn1;
+    S.fy[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[Q.fl21 | zC] * ih));
+    const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
+    const C d22 = (beta * (v00 - u00) + w * (tn - cur.t2)) * (P.inv_wsum[Q.i22] * ih);  // cell (q, z)
+    o3v += d22;
+    nxt.f22 = mc00 * d22;  // zero-filled mu masks cells outside the box
+    nxt.t2 = tn;
+    m2 = mass_head(cur.q2, nxt.q2);
+    nxt.q2 = (zin2 && Q.q2ok) ? md(RHc[ui] + rp00, GAc[ui] + gp00, izp) * v00 : zc;
+    SQn[2][t] = nxt.q2;
+  }
+  nxt.mu02 = mu02p;
+  nxt.mu12 = mu12p;
+  const C pc = S.p[s0][ui];
+  o3v += S.ilm[s0][ui] * pc;
+  // x-neighbour p by shuffle (lanes 0 and 31 are halo: their wrapped values
+  // are never used)
+  pt0 = (pc - r3_up(pc)) * ih;
+  pt1 = pc;
+  pt2 = pc - cur.p;
+  nxt.p = pc;
+  }
+  __syncthreads();
+
+  if (Q.interior && z >= Q.zb) {
+    const int xg = Q.xg, yg = Q.yg;
+    // row offsets at plane z
+    const int64_t o0 = g.off[0] + xg + (int64_t)(n0 + 1) * (yg + n1 * z);
+    const int64_t o1 = g.off[1] + xg + (int64_t)n0 * (yg + (n1 + 1) * z);
+    const int64_t o2 = g.off[2] + xg + (int64_t)n0 * (yg + n1 * z);
+    const int64_t o3 = o2 + (g.off[3] - g.off[2]);
+    const C(*SQ)[R3_THREADS] = S.q[z & 1];
+    const int czz = lz + hz0;
+    o0v += (S.fy[1][t] - S.fy[1][t + R3_FX]) * ih;
+    o0v += (cur.f02 - nxt.f02) * ih;
+    m0 += wn * SQ[0][t - R3_FX];
+    m0 += wn * SQ[0][t + R3_FX];
+    m0 += wn * nxt.q0;
+    o0v -= m0 * P.inv_msum[Q.mc0 + czz];
+    o0v += pt0;
+    o1v += (S.fy[0][t - R3_FX] - S.fy[0][t]) * ih;
+    o1v += (cur.f12 - nxt.f12) * ih;
+    m1 += wn * SQ[1][t - R3_FX];
+    m1 += wn * SQ[1][t + R3_FX];
+    m1 += wn * nxt.q1;
+    o1v -= m1 * P.inv_msum[Q.mc1 + czz];
+    o1v += (pt1 - S.p[s0][ui - R3_UX]) * ih;
+    o2v += (S.fy[2][t] - S.fy[2][t + R3_FX]) * ih;
+    o2v += (cur.f22 - nxt.f22) * ih;
+    m2 += wn * SQ[2][t - R3_FX];
+    m2 += wn * SQ[2][t + R3_FX];
+    m2 += wn * nxt.q2;
+    o2v -= m2 * P.inv_msum[Q.mc2 + lz + hz1];
+    o2v += pt2 * ih;
+    if (b) {  // b planes arrived with this step's load group (TMA, zero outside)
+      const C(*BP)[R3_THREADS] = S.bp[z & 1];
+      o0v = BP[0][t] - o0v;
+      o1v = BP[1][t] - o1v;
+      o2v = BP[2][t] - o2v;
+      o3v = BP[3][t] - o3v;
+    }
+    if (Q.v0 && z < n2) y[o0] = o0v;
+    if (Q.v1 && z < n2) y[o1] = o1v;
+    if (Q.v2) y[o2] = o2v;
+    if (Q.v2 && z < n2) y[o3] = o3v;
+  }
+}
+
+__global__ void __launch_bounds__(R3_THREADS, 1)
+    k_stencil3d_rr(const __grid_constant__ R3Maps maps, const __grid_constant__ S3Params P,
+                   const cplx* __restrict__ b, cplx* __restrict__ y) {
+  extern __shared__ __align__(1024) unsigned char r3_raw[];
+  R3Smem& S = *reinterpret_cast<R3Smem*>(r3_raw);
+  const Geo& g = P.g;
+  const int t = threadIdx.x, fx = t & 31, fy = t >> 5;
+  const int n0 = g.n[0], n1 = g.n[1];
+
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned seq = 0;  // load groups issued so far (uniform)
+
+  const int items = P.ntiles_x * P.ntiles_y * P.nchunks;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int tile = item % (P.ntiles_x * P.ntiles_y);
+    const int chunk = item / (P.ntiles_x * P.ntiles_y);
+    R3Pos Q;
+    Q.t = t;
+    Q.fy = fy;
+    Q.ui = (fx + 1) + R3_UX * (fy + 1);  // own index in the u / p / media windows
+    Q.i0 = (tile % P.ntiles_x) * R3_TX;
+    Q.j0 = (tile / P.ntiles_x) * R3_TY;
+    const int zspan = P.z_hi - P.z_lo;
+    Q.zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
+    const int zend = P.z_lo + (int)(((int64_t)(chunk + 1) * zspan) / P.nchunks);
+    const int xg = Q.i0 - 1 + fx, yg = Q.j0 - 1 + fy;
+    Q.xg = xg;
+    Q.yg = yg;
+    const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
+    const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
+    Q.ix = s3_inv<double>(lx + hx1);
+    Q.iy = s3_inv<double>(ly + hy1);
+    Q.fl00 = ly | (hy0 << 1);
+    Q.fl11 = (lx << 2) | (hx0 << 3);
+    Q.fl01 = (lx << 2) | (hx1 << 3);
+    Q.fl10 = (ly << 2) | (hy1 << 3);
+    Q.fl20 = ly | (hy0 << 1);
+    Q.fl21 = lx | (hx0 << 1);
+    Q.i22 = lx | (hx0 << 1) | (ly << 2) | (hy0 << 3);
+    Q.i02 = ly | (hy0 << 1) | (lx << 2) | (hx1 << 3);
+    Q.i12 = lx | (hx0 << 1) | (ly << 2) | (hy1 << 3);
+    Q.mu01s = Q.ix * Q.iy;
+    Q.mc0 = (lx + (xg + 1 < n0 + 1)) + (ly + hy0);
+    Q.mc1 = (lx + hx0) + (ly + (yg + 1 < n1 + 1));
+    Q.mc2 = (lx + hx0) + (ly + hy0);
+    Q.interior = fx >= 1 && fx <= R3_TX && fy >= 1 && fy <= R3_TY;
+    Q.v0 = Q.interior && xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
+    Q.v1 = Q.interior && xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
+    Q.v2 = Q.interior && xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
+    Q.q0ok = xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
+    Q.q1ok = xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
+    Q.q2ok = xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
+
+    // two warm-up planes (three when needed to make the step count even)
+    const int zs = Q.zb - 2 - ((zend - Q.zb) & 1);
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      r3_issue(S, maps, Q.i0, Q.j0, zs, 2, zs, 2, zs, 1, false, 0, &S.bar[seq & 1]);
+    }
+    R3Carry A, B;
+    {
+      const cplx zc = mk(0.0, 0.0);
+      A.r00 = A.r11 = A.r01 = A.r10 = A.r20 = A.r21 = zc;
+      A.t0 = A.t1 = A.t2 = A.f02 = A.f12 = A.f22 = A.q0 = A.q1 = A.q2 = A.p = zc;
+      A.mu02 = A.mu12 = 0.0;
+      B = A;
+    }
+    int su0 = s3_mod3(zs);  // ring slot of plane z (u, p and media alike)
+    for (int z = zs; z < zend; z += 2) {
+      r3_step(S, maps, P, Q, b, y, z, su0, seq, A, B);
+      r3_step(S, maps, P, Q, b, y, z + 1, su0, seq, B, A);
+    }
+    // drain the group issued by the last step before the next item reuses smem
+    s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+    ++seq;
+    __syncthreads();
+  }
+}
+
+// 3D float64 map over a (d0, d1, d2) array with box (box0, box1, 1).
+inline bool r3_encode(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, int64_t d2, int box0,
+                      int box1) {
+  EncodeTiledFn enc = s3_encoder();
+  if (!enc) return false;
+  const cuuint64_t dim[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  const cuuint64_t str[2] = {(cuuint64_t)(d0 * 8), (cuuint64_t)(d0 * d1 * 8)};
+  const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dim, str, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline int r3_device_init() {
+  static std::mutex mu;
+  static int nsm_of[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!nsm_of[dev]) {
+    cudaFuncSetAttribute(k_stencil3d_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(R3Smem));
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    nsm_of[dev] = nsm > 0 ? nsm : 148;
+  }
+  return nsm_of[dev];
+}
+
+// media_soa: 4 consecutive cell arrays {mu, rho, gamma, 1/(lambda+mu)}.
+// Output planes [z_lo, z_hi) (default: all, including the top u2 faces).
+inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
+                             const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  const int nsm = r3_device_init();
+  // tensor maps depend only on (buffer, media, dims): cache them so the
+  // per-launch host cost is a lookup (buffers are fixed per level).
+  struct Entry {
+    const void* x;
+    const void* m;
+    const void* b;
+    int n[3];
+    R3Maps M;
+  };
+  static std::vector<Entry> cache;
+  static size_t next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const R3Maps* Mp = nullptr;
+  for (const Entry& e : cache)
+    if (e.x == x && e.m == media_soa && e.b == b && e.n[0] == n0 && e.n[1] == n1 && e.n[2] == n2) {
+      Mp = &e.M;
+      break;
+    }
+  if (!Mp) {
+    Entry e;
+    e.x = x;
+    e.m = media_soa;
+    e.b = b;
+    e.n[0] = n0, e.n[1] = n1, e.n[2] = n2;
+    for (int k = 0; k < 3; ++k)
+      r3_encode(&e.M.m.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_UX, R3_UY);
+    r3_encode(&e.M.m.p, x + g.off[3], 2 * n0, n1, n2, 2 * R3_UX, R3_UY);
+    const int64_t nc = g.ncells;
+    r3_encode(&e.M.m.mu, media_soa + 0 * nc, n0, n1, n2, R3_UX, R3_UY);
+    r3_encode(&e.M.m.rho, media_soa + 1 * nc, n0, n1, n2, R3_UX, R3_UY);
+    r3_encode(&e.M.m.gam, media_soa + 2 * nc, n0, n1, n2, R3_UX, R3_UY);
+    r3_encode(&e.M.m.ilm, media_soa + 3 * nc, n0, n1, n2, R3_UX, R3_UY);
+    if (b) {
+      for (int k = 0; k < 3; ++k)
+        r3_encode(&e.M.b[k], b + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_FX, R3_FY);
+      r3_encode(&e.M.b[3], b + g.off[3], 2 * n0, n1, n2, 2 * R3_FX, R3_FY);
+    }
+    if (cache.size() < 256) {
+      cache.push_back(e);
+      Mp = &cache.back().M;
+    } else {
+      cache[next] = e;
+      Mp = &cache[next].M;
+      next = (next + 1) % cache.size();
+    }
+  }
+  const R3Maps M = *Mp;
+  const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi, R3_TY, R3_TX);
+  if (sp.z_hi <= sp.z_lo) return;
+  const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
+  const int grid = items < nsm ? items : nsm;
+  k_stencil3d_rr<<<grid, R3_THREADS, sizeof(R3Smem), s>>>(M, sp, b, y);
+}
+
+}  // namespace ehmg

@@ -20,13 +20,24 @@ def main():
     ap.add_argument("libs", nargs="+")
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--one", action="store_true", help="(internal) time one library in this process")
+    ap.add_argument("--cmp", action="store_true", help="(internal) compare with the first library's output")
     a = ap.parse_args()
+    if not a.one:
+        # one process per library: two builds of the same library cannot share a process
+        import subprocess
+        for i, path in enumerate(a.libs):
+            subprocess.run([sys.executable, __file__, path, "--n", str(a.n), "--reps", str(a.reps), "--one"]
+                           + (["--cmp"] if i else []), check=False)
+        return
     n = a.n
     nc = n ** 3
-    lam = np.full(nc, 2.0)
-    mu = np.ones(nc)
-    rho = np.ones(nc)
-    gam = np.full(nc, 0.01)
+    rng = np.random.default_rng(5)
+    lam = 2.0 * rng.uniform(0.8, 1.2, nc)
+    mu = rng.uniform(0.8, 1.2, nc)
+    rho = rng.uniform(0.8, 1.2, nc)
+    gam = 0.01 * rng.uniform(0.5, 1.5, nc)
+    y_ref = None
     dims = (C.c_int * 3)(n, n, n)
     dp = lambda v: v.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
     for path in a.libs:
@@ -42,6 +53,8 @@ def main():
         torch.manual_seed(0)
         x = torch.randn(N, dtype=torch.complex128, device="cuda")
         y = torch.empty_like(x)
+        bvec = torch.randn(N, dtype=torch.complex128, device="cuda")
+        r = torch.empty_like(x)
         st = torch.cuda.ExternalStream(L.ehmg_op_stream(op))
         L.ehmg_last_error.restype = C.c_char_p
         for _ in range(3):
@@ -57,7 +70,26 @@ def main():
         e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
-        print(f"{path}: {ms:.4f} ms/apply  {N / ms / 1e6:.2f} GDOF/s  checksum {float(y.abs().sum()):.10e}")
+        for _ in range(2):
+            L.ehmg_residual(op, C.c_void_p(bvec.data_ptr()), C.c_void_p(x.data_ptr()), C.c_void_p(r.data_ptr()), 1)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(a.reps):
+            L.ehmg_residual(op, C.c_void_p(bvec.data_ptr()), C.c_void_p(x.data_ptr()), C.c_void_p(r.data_ptr()), 1)
+        e1.record(st)
+        torch.cuda.synchronize()
+        msr = e0.elapsed_time(e1) / a.reps
+        ref = f"/tmp/ab_stencil_ref_{n}.pt"
+        if not a.cmp:
+            torch.save({"y": y.cpu(), "r": r.cpu()}, ref)
+            err = errr = 0.0
+        else:
+            d = torch.load(ref)
+            y_ref, r_ref = d["y"].cuda(), d["r"].cuda()
+            err = float((y - y_ref).abs().max() / y_ref.abs().max())
+            errr = float((r - r_ref).abs().max() / r_ref.abs().max())
+        print(f"{path}: apply {ms:.4f} ms ({N / ms / 1e6:.2f} GDOF/s)  residual {msr:.4f} ms  "
+              f"rel diff vs first lib: apply {err:.2e} residual {errr:.2e}")
         L.ehmg_op_destroy(op)
         sys.stdout.flush()
 
