@@ -305,7 +305,7 @@ __global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict_
 // T = cplx or cplxf: storage and arithmetic type (the single-precision
 // hierarchy updates in float, as the reference's VankaSmoother<float>).
 template <int ND, class T = cplx>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 2 : 4) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
+__global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
                                                            const T* __restrict__ r, int color, double w,
                                                            T* __restrict__ x) {
   typedef typename VT<T>::R R;
@@ -318,51 +318,57 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 2 : 4) k
     if (!colour_cell(g, t, color, c)) continue;
     const T* q = soa + (int64_t)color * cs * nt + t;
     auto Q = [&](int e) { return q[(int64_t)e * nt]; };
+    // every load of the cell is issued before any arithmetic (r, x and the
+    // cache entries are independent HBM streams: ~27 complex in flight per
+    // thread instead of a load -> use -> load chain)
     const int64_t pi = g.off[ND] + g.clin(c);
     int64_t fi[ND][2];
-    T rr[ND][2];
-    T dpa = r[pi];
-    const T b0 = VT<T>::mk((R)V.ih, 0), b1 = VT<T>::mk(-(R)V.ih, 0);
-    auto loadU = [&](int k, T* U) {
-      if (full) {
-        U[0] = Q(4 * k), U[1] = Q(4 * k + 1), U[2] = Q(4 * k + 2), U[3] = Q(4 * k + 3);
-      } else {
-        U[0] = Q(2 * k), U[3] = Q(2 * k + 1), U[1] = U[2] = zero;
-      }
-    };
+    T rr[ND][2], xx[ND][2], U[ND][4];
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       int f1[3];
       sh(c, k, 1, f1);
       fi[k][0] = g.off[k] + g.flin(k, c);
       fi[k][1] = g.off[k] + g.flin(k, f1);
-      rr[k][0] = r[fi[k][0]];
-      rr[k][1] = r[fi[k][1]];
-      T U[4];
-      loadU(k, U);
-      const R c0 = (R)vk_c0<ND>(V, g, k, c);
-      const T k0 = VT<T>::mk(c0, 0), k1 = VT<T>::mk(-c0, 0);
-      const T h0 = k0 * U[0] + k1 * U[2], h1 = k0 * U[1] + k1 * U[3];
-      dpa -= h0 * rr[k][0] + h1 * rr[k][1];
     }
-    const T dp = Q(cs - 1) * dpa;
+    const T rp = r[pi], xp = x[pi], sinv = Q(cs - 1);
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      T U[4];
-      loadU(k, U);  // second read hits L1
-      const T g0 = U[0] * b0 + U[1] * b1, g1 = U[2] * b0 + U[3] * b1;
+      rr[k][0] = r[fi[k][0]];
+      rr[k][1] = r[fi[k][1]];
+      xx[k][0] = x[fi[k][0]];
+      xx[k][1] = x[fi[k][1]];
+      if (full) {
+        U[k][0] = Q(4 * k), U[k][1] = Q(4 * k + 1), U[k][2] = Q(4 * k + 2), U[k][3] = Q(4 * k + 3);
+      } else {
+        U[k][0] = Q(2 * k), U[k][3] = Q(2 * k + 1), U[k][1] = U[k][2] = zero;
+      }
+    }
+    T dpa = rp;
+    const T b0 = VT<T>::mk((R)V.ih, 0), b1 = VT<T>::mk(-(R)V.ih, 0);
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const R c0 = (R)vk_c0<ND>(V, g, k, c);
+      const T k0 = VT<T>::mk(c0, 0), k1 = VT<T>::mk(-c0, 0);
+      const T h0 = k0 * U[k][0] + k1 * U[k][2], h1 = k0 * U[k][1] + k1 * U[k][3];
+      dpa -= h0 * rr[k][0] + h1 * rr[k][1];
+    }
+    const T dp = sinv * dpa;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const T g0 = U[k][0] * b0 + U[k][1] * b1, g1 = U[k][2] * b0 + U[k][3] * b1;
       T du0, du1;
       if (full) {
-        du0 = U[0] * rr[k][0] + U[1] * rr[k][1] - g0 * dp;
-        du1 = U[2] * rr[k][0] + U[3] * rr[k][1] - g1 * dp;
+        du0 = U[k][0] * rr[k][0] + U[k][1] * rr[k][1] - g0 * dp;
+        du1 = U[k][2] * rr[k][0] + U[k][3] * rr[k][1] - g1 * dp;
       } else {
-        du0 = U[0] * rr[k][0] - g0 * dp;
-        du1 = U[3] * rr[k][1] - g1 * dp;
+        du0 = U[k][0] * rr[k][0] - g0 * dp;
+        du1 = U[k][3] * rr[k][1] - g1 * dp;
       }
-      x[fi[k][0]] += wr * du0;
-      x[fi[k][1]] += wr * du1;
+      x[fi[k][0]] = xx[k][0] + wr * du0;
+      x[fi[k][1]] = xx[k][1] + wr * du1;
     }
-    x[pi] += wr * dp;
+    x[pi] = xp + wr * dp;
   }
 }
 
