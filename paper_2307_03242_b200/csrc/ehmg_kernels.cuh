@@ -563,6 +563,8 @@ __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const V* __res
   const Taps t0 = prolong_taps(f0, F0, C == 0);
   const Taps t1 = prolong_taps(f1, F1, C == 1);
   const Taps t2 = prolong_taps(f2 + gf.zoff, gf.gn2 + (C == 2), C == 2);
+  V* o = xf + gf.off[C] + f0 + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
+  const V old = accumulate ? *o : V{};  // issued first: overlaps the coarse gathers
   const V* base = xc + gc.off[C];
   cplx s2 = mk(0, 0);
 #pragma unroll
@@ -586,8 +588,7 @@ __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const V* __res
     }
     s2 += t2.w[q2] * s1;
   }
-  V* o = xf + gf.off[C] + f0 + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
-  *o = narrow<V>(accumulate ? wide(*o) + s2 : s2);
+  *o = narrow<V>(accumulate ? wide(old) + s2 : s2);
 }
 
 // ------------------------------------------------------------------ media
