@@ -47,9 +47,9 @@ struct __align__(128) R3Smem {
   cplx u[3][3][R3_US];  // [plane % 3][component]
   cplx p[3][R3_US];     // [plane % 3]
   double mu[3][R3_MS], rho[3][R3_MS], gam[3][R3_MS], ilm[3][R3_MS];  // [plane % 3]
-  cplx fy[3][R3_THREADS];     // y-exchanged fluxes at plane z: F11, F01, F21
-  cplx q[2][3][R3_THREADS];   // mass products md*u [plane & 1][component]
-  cplx bp[2][4][R3_THREADS];  // residual mode: b rows of the thread grid [plane & 1][component]
+  cplx fy[2][3][R3_THREADS];  // y-exchanged fluxes F11, F01, F21 [plane & 1]
+  cplx q[3][3][R3_THREADS];   // mass products md*u [plane % 3][component]
+  cplx bp[3][4][R3_THREADS];  // residual mode: b rows of the thread grid [plane % 3][component]
   unsigned long long bar[2];
 };
 
@@ -72,7 +72,7 @@ __device__ __forceinline__ void r3_issue(R3Smem& S, const R3Maps& RM, int i0, in
   const S3Maps& M = RM.m;
   s3_expect(bar, (unsigned)(nu * 3 * R3_CBYTES + nm * 4 * R3_DBYTES + np * R3_CBYTES + (hasb ? 4 * R3_BBYTES : 0)));
   if (hasb)
-    for (int k = 0; k < 4; ++k) s3_tma(S.bp[zb_ & 1][k], &RM.b[k], 2 * (i0 - 1), j0 - 1, zb_, bar);
+    for (int k = 0; k < 4; ++k) s3_tma(S.bp[s3_mod3(zb_)][k], &RM.b[k], 2 * (i0 - 1), j0 - 1, zb_, bar);
   const int cx = 2 * (i0 - 2), cy = j0 - 2, mx = i0 - 2;  // i0 even: 16-byte aligned media start
   for (int q = 0; q < nu; ++q) {
     const int sl = s3_mod3(zu + q);
@@ -122,9 +122,13 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int n2g = g.gn2;
 
+  // One block barrier per plane (the one between the two phases below).
+  // The slots refilled here -- u / media of plane z-1, p and b of plane z-2,
+  // exchange buffers two planes back -- were last read before the previous
+  // plane's barrier, so a warp may start this plane while others still
+  // finish the previous plane's rows.
   s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
   ++seq;
-  __syncthreads();  // all of step z-1 done: its slots may be refilled
   if (t == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     r3_issue(S, maps, Q.i0, Q.j0, z + 2, 1, z + 2, 1, z + 1, 1, b != nullptr, z + 1, &S.bar[seq & 1]);
@@ -155,7 +159,8 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
   };
   const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
   const bool zin2 = zg + 1 >= 0 && zg + 1 <= n2g;
-  C(*SQn)[R3_THREADS] = S.q[(z + 1) & 1];
+  C(*SQn)[R3_THREADS] = S.q[s1];
+  C(*FY)[R3_THREADS] = S.fy[z & 1];
 
   // values the row evaluation after the barrier needs (rows 1..TY only)
   C m0, m1, m2, o0v, o1v, o2v, o3v, pt0, pt1, pt2;
@@ -204,7 +209,7 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     const C rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
     const C sz1 = (nxt.r01 + 2.0 * cur.r01) + rn1;
     nxt.r01 = rn1;
-    S.fy[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[zB | Q.fl01] * ih));
+    FY[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[zB | Q.fl01] * ih));
     const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
     nxt.f02 = mu02p * ((beta * (v00 - u00) + w * (tn - cur.t0)) * (P.inv_wsum[Q.i02] * ih));
     nxt.t0 = tn;
@@ -223,7 +228,7 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     nxt.r11 = rn0;
     const C d11 = (beta * (up0 - u00) + w * sz0) * (P.inv_wsum[zB | Q.fl11] * ih);
     o3v += d11;
-    S.fy[0][t] = mc00 * d11;
+    FY[0][t] = mc00 * d11;
     const C rn1 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
     const C sz1 = (nxt.r10 + 2.0 * cur.r10) + rn1;
     nxt.r10 = rn1;
@@ -250,7 +255,7 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     const C rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
     const C sz1 = (nxt.r21 + 2.0 * cur.r21) + rn1;
     nxt.r21 = rn1;
-    S.fy[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[Q.fl21 | zC] * ih));
+    FY[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[Q.fl21 | zC] * ih));
     const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
     const C d22 = (beta * (v00 - u00) + w * (tn - cur.t2)) * (P.inv_wsum[Q.i22] * ih);  // cell (q, z)
     o3v += d22;
@@ -280,23 +285,23 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     const int64_t o1 = g.off[1] + xg + (int64_t)n0 * (yg + (n1 + 1) * z);
     const int64_t o2 = g.off[2] + xg + (int64_t)n0 * (yg + n1 * z);
     const int64_t o3 = o2 + (g.off[3] - g.off[2]);
-    const C(*SQ)[R3_THREADS] = S.q[z & 1];
+    const C(*SQ)[R3_THREADS] = S.q[s0];
     const int czz = lz + hz0;
-    o0v += (S.fy[1][t] - S.fy[1][t + R3_FX]) * ih;
+    o0v += (FY[1][t] - FY[1][t + R3_FX]) * ih;
     o0v += (cur.f02 - nxt.f02) * ih;
     m0 += wn * SQ[0][t - R3_FX];
     m0 += wn * SQ[0][t + R3_FX];
     m0 += wn * nxt.q0;
     o0v -= m0 * P.inv_msum[Q.mc0 + czz];
     o0v += pt0;
-    o1v += (S.fy[0][t - R3_FX] - S.fy[0][t]) * ih;
+    o1v += (FY[0][t - R3_FX] - FY[0][t]) * ih;
     o1v += (cur.f12 - nxt.f12) * ih;
     m1 += wn * SQ[1][t - R3_FX];
     m1 += wn * SQ[1][t + R3_FX];
     m1 += wn * nxt.q1;
     o1v -= m1 * P.inv_msum[Q.mc1 + czz];
     o1v += (pt1 - S.p[s0][ui - R3_UX]) * ih;
-    o2v += (S.fy[2][t] - S.fy[2][t + R3_FX]) * ih;
+    o2v += (FY[2][t] - FY[2][t + R3_FX]) * ih;
     o2v += (cur.f22 - nxt.f22) * ih;
     m2 += wn * SQ[2][t - R3_FX];
     m2 += wn * SQ[2][t + R3_FX];
@@ -304,7 +309,7 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     o2v -= m2 * P.inv_msum[Q.mc2 + lz + hz1];
     o2v += pt2 * ih;
     if (b) {  // b planes arrived with this step's load group (TMA, zero outside)
-      const C(*BP)[R3_THREADS] = S.bp[z & 1];
+      const C(*BP)[R3_THREADS] = S.bp[s0];
       o0v = BP[0][t] - o0v;
       o1v = BP[1][t] - o1v;
       o2v = BP[2][t] - o2v;
