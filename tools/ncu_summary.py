@@ -60,17 +60,28 @@ def report(path):
     return "\n".join(out)
 
 
-def launches(path):
+SETUP = ("cutlass", "trsm", "getr", "ipiv", "k_identity", "vanka_build", "vanka_to_soa", "coarse_matrix",
+         "laswp", "laset", "coarsen_media", "swap")
+
+
+def launches(path, steady=False):
+    """steady: only the launches after the last setup kernel (LU inverse,
+    Vanka factorisation): the cycles the bench times."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
     iK, iV, iG = h.index("Kernel Name"), h.index("Metric Value"), h.index("Grid Size")
     agg = collections.defaultdict(lambda: [0, 0.0])
-    for r in rows[hi + 1:]:
+    body = rows[hi + 1:]
+    if steady:
+        last = max([i for i, r in enumerate(body) if any(k in r[iK] for k in SETUP)], default=-1)
+        body = body[last + 1:]
+    for r in body:
         agg[(r[iK].split("(")[0], r[iG])][0] += 1
         agg[(r[iK].split("(")[0], r[iG])][1] += float(r[iV].replace(",", ""))
     tot = sum(v[1] for v in agg.values())
-    out = [f"# ncu launch list summary: {path} (gpu__time_duration.sum, cold-cache, serialised)",
+    out = [f"# ncu launch list summary: {path} (gpu__time_duration.sum, cold-cache, serialised"
+           + (", launches after the last setup kernel)" if steady else ")"),
            f"{'kernel':40s} {'grid':16s} {'launches':>8s} {'total_ms':>10s} {'share':>7s} {'avg_us':>9s}"]
     for (k, g), (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         out.append(f"{k[:40]:40s} {g:16s} {c:8d} {t / 1e6:10.3f} {100 * t / tot:6.1f}% {t / c / 1e3:9.1f}")
@@ -79,4 +90,4 @@ def launches(path):
 
 if __name__ == "__main__":
     p = sys.argv[1]
-    print(launches(p) if p.endswith(".csv") else report(p))
+    print(launches(p, "--steady" in sys.argv) if p.endswith(".csv") else report(p))
