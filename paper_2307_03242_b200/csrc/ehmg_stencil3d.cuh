@@ -627,8 +627,9 @@ inline int s3_device_init() {
 
 // complex64 variant (single-precision hierarchy): media_soa holds the four
 // float cell arrays; planes are loaded with cp.async, so no tensor maps.
-inline void launch_stencil3d(const Geo& g, const OpPar& P, const float* media_soa, const cplxf* x,
-                             const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+// Fallback for n0 % 4 != 0 (ehmg_stencil3d_rr.cuh dispatches).
+inline void launch_stencil3d_ca(const Geo& g, const OpPar& P, const float* media_soa, const cplxf* x,
+                                const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
   const int nsm = s3_device_init();
   const int64_t nc = g.ncells;
   S3Src src;

@@ -1,9 +1,12 @@
-// ehmg_stencil3d_rr.cuh -- register-resident complex128 3D operator / residual.
+// ehmg_stencil3d_rr.cuh -- register-resident 3D operator / residual.
 //
 // y = H x  or  r = b - H x  for the staggered mixed elastic-Helmholtz
-// operator (operator.hpp:389-421), all four components in one launch; the
-// complex128 production kernel (k_stencil3d<cplxf> in ehmg_stencil3d.cuh
-// serves the complex64 hierarchy).
+// operator (operator.hpp:389-421), all four components in one launch.
+// V = cplx: the complex128 production kernel. V = cplxf: the complex64
+// hierarchy of the mixed-precision mode (experiments.hpp:241), same design;
+// its u0 rows (n0+1 complex64 = an odd number of 8-byte values) are not
+// 16-byte strided, which tensor maps require, so u0 (and b) planes arrive
+// by cp.async two planes ahead instead of TMA.
 //
 // Why this shape. The 11-warp kernel (33x8 tiles, 352 threads) sat at the
 // 168-register cap of three warps per SM sub-partition and moved every
@@ -39,46 +42,67 @@ constexpr int R3_FX = 32, R3_FY = 8;               // flux window = thread grid
 constexpr int R3_THREADS = R3_FX * R3_FY;          // 256
 constexpr int R3_UX = R3_FX + 2, R3_UY = R3_FY + 2;  // u / p / media window, origin (i0-2, j0-2)
 constexpr int R3_UN = R3_UX * R3_UY;
-constexpr int R3_US = (R3_UN + 7) / 8 * 8;    // complex slot stride: 128-byte aligned TMA destinations
-constexpr int R3_MS = (R3_UN + 15) / 16 * 16;  // double slot stride
-constexpr unsigned R3_CBYTES = R3_UN * 16, R3_DBYTES = R3_UN * 8;
 
-struct __align__(128) R3Smem {
-  cplx u[3][3][R3_US];  // [plane % 3][component]
-  cplx p[3][R3_US];     // [plane % 3]
-  double mu[3][R3_MS], rho[3][R3_MS], gam[3][R3_MS], ilm[3][R3_MS];  // [plane % 3]
-  cplx fy[2][3][R3_THREADS];  // y-exchanged fluxes F11, F01, F21 [plane & 1]
-  cplx q[3][3][R3_THREADS];   // mass products md*u [plane % 3][component]
-  cplx bp[3][4][R3_THREADS];  // residual mode: b rows of the thread grid [plane % 3][component]
+// Shared-memory layout per element type. Slots are 128-byte aligned (TMA
+// destinations). complex64: media rows start at a 16-byte aligned column
+// ((i0-2) & ~3) with a 36-wide pitch; u0 and b sit in 4-plane cp.async rings.
+template <class V>
+struct __align__(128) R3SmemT {
+  typedef typename VT<V>::R R;
+  static constexpr bool F = sizeof(R) == 4;
+  static constexpr int US = F ? (R3_UN + 15) / 16 * 16 : (R3_UN + 7) / 8 * 8;
+  static constexpr int MX = F ? 36 : R3_UX;  // media pitch
+  static constexpr int MN = MX * R3_UY;
+  static constexpr int MS = (MN + 31) / 32 * 32;
+  static constexpr int NB = F ? 4 : 3;   // b ring
+  static constexpr int NU0 = F ? 4 : 1;  // u0 ring (complex64 only)
+  static constexpr unsigned CBYTES = R3_UN * sizeof(V), MBYTES = MN * sizeof(R), BBYTES = R3_THREADS * sizeof(V);
+  V u[3][3][US];  // [plane % 3][component] (complex64: component 0 unused)
+  V p[3][US];     // [plane % 3]
+  R mu[3][MS], rho[3][MS], gam[3][MS], ilm[3][MS];  // [plane % 3]
+  V fy[2][3][R3_THREADS];   // y-exchanged fluxes F11, F01, F21 [plane & 1]
+  V q[3][3][R3_THREADS];    // mass products md*u [plane % 3][component]
+  V bp[NB][4][R3_THREADS];  // residual mode: b rows of the thread grid [plane % NB][component]
   unsigned long long bar[2];
+  V u0x[NU0][F ? US : 1];  // complex64: u0 [plane & 3] by cp.async (a placeholder for complex128);
+                           // last, so the TMA destinations above keep their 128-byte alignment
 };
+typedef R3SmemT<cplx> R3Smem;
 
 // x, media and (residual mode) b tensor maps; b boxes cover the thread grid.
 struct R3Maps {
   S3Maps m;
   CUtensorMap b[4];
 };
-constexpr unsigned R3_BBYTES = R3_THREADS * 16;
 
-__device__ __forceinline__ cplx r3_up(cplx v) {  // value of lane - 1
-  return mk(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+template <class V>
+__device__ __forceinline__ V r3_up(V v) {  // value of lane - 1
+  return VT<V>::mk(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
-__device__ __forceinline__ cplx r3_dn(cplx v) {  // value of lane + 1
-  return mk(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+template <class V>
+__device__ __forceinline__ V r3_dn(V v) {  // value of lane + 1
+  return VT<V>::mk(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
 }
 
-__device__ __forceinline__ void r3_issue(R3Smem& S, const R3Maps& RM, int i0, int j0, int zu, int nu, int zm,
+// TMA load group: u planes zu.. (complex128: all three components;
+// complex64: u1, u2), media planes zm.., p planes zp.., b plane zb_
+// (complex128 residual mode).
+template <class V>
+__device__ __forceinline__ void r3_issue(R3SmemT<V>& S, const R3Maps& RM, int i0, int j0, int zu, int nu, int zm,
                                          int nm, int zp, int np, bool hasb, int zb_, unsigned long long* bar) {
+  typedef R3SmemT<V> SM;
+  constexpr bool F = SM::F;
   const S3Maps& M = RM.m;
-  s3_expect(bar, (unsigned)(nu * 3 * R3_CBYTES + nm * 4 * R3_DBYTES + np * R3_CBYTES + (hasb ? 4 * R3_BBYTES : 0)));
-  if (hasb)
+  constexpr int ku0 = F ? 1 : 0;
+  s3_expect(bar, (unsigned)(nu * (3 - ku0) * SM::CBYTES + nm * 4 * SM::MBYTES + np * SM::CBYTES +
+                            (hasb && !F ? 4 * SM::BBYTES : 0)));
+  if (!F && hasb)
     for (int k = 0; k < 4; ++k) s3_tma(S.bp[s3_mod3(zb_)][k], &RM.b[k], 2 * (i0 - 1), j0 - 1, zb_, bar);
-  const int cx = 2 * (i0 - 2), cy = j0 - 2, mx = i0 - 2;  // i0 even: 16-byte aligned media start
+  const int cx = 2 * (i0 - 2), cy = j0 - 2;
+  const int mx = F ? ((i0 - 2) & ~3) : i0 - 2;  // 16-byte aligned media start (i0 is even)
   for (int q = 0; q < nu; ++q) {
     const int sl = s3_mod3(zu + q);
-    s3_tma(S.u[sl][0], &M.u[0], cx, cy, zu + q, bar);
-    s3_tma(S.u[sl][1], &M.u[1], cx, cy, zu + q, bar);
-    s3_tma(S.u[sl][2], &M.u[2], cx, cy, zu + q, bar);
+    for (int k = ku0; k < 3; ++k) s3_tma(S.u[sl][k], &M.u[k], cx, cy, zu + q, bar);
   }
   for (int q = 0; q < nm; ++q) {
     const int sl = s3_mod3(zm + q);
@@ -90,10 +114,45 @@ __device__ __forceinline__ void r3_issue(R3Smem& S, const R3Maps& RM, int i0, in
   for (int q = 0; q < np; ++q) s3_tma(S.p[s3_mod3(zp + q)], &M.p, cx, cy, zp + q, bar);
 }
 
+// complex64: 8-byte cp.async with zero fill outside the array (the tensor
+// maps' out-of-bounds rule), issued by every thread.
+__device__ __forceinline__ void r3_cp8(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s3_saddr(dst)), "l"(src), "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void r3_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void r3_cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// u0 window of plane z (origin (i0-2, j0-2), 34 x 10) into dst
+__device__ __forceinline__ void r3_u0_plane(cplxf* dst, const cplxf* u0, const Geo& g, int i0, int j0, int z, int t) {
+  const int d0 = g.n[0] + 1, d1 = g.n[1], d2 = g.n[2];
+  const bool zin = z >= 0 && z < d2;
+  for (int e = t; e < R3_UN; e += R3_THREADS) {
+    const int r = e / R3_UX, c = e - r * R3_UX, x = i0 - 2 + c, yy = j0 - 2 + r;
+    const bool ok = zin && x >= 0 && x < d0 && yy >= 0 && yy < d1;
+    r3_cp8(&dst[e], ok ? u0 + ((int64_t)z * d1 + yy) * d0 + x : u0, ok);
+  }
+}
+// b rows of the thread grid (origin (i0-1, j0-1)) of plane z, all four components
+__device__ __forceinline__ void r3_b_plane(cplxf (*dst)[R3_THREADS], const cplxf* b, const Geo& g, int i0, int j0,
+                                           int z, int t) {
+  const int x = i0 - 1 + (t % R3_FX), yy = j0 - 1 + t / R3_FX;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int d0 = g.n[0] + (k == 0), d1 = g.n[1] + (k == 1), d2 = g.n[2] + (k == 2);
+    const cplxf* base = b + g.off[k];
+    const bool ok = z >= 0 && z < d2 && x >= 0 && x < d0 && yy >= 0 && yy < d1;
+    r3_cp8(&dst[k][t], ok ? base + ((int64_t)z * d1 + yy) * d0 + x : base, ok);
+  }
+}
+
 // Per-item constants of one thread's position.
+template <class R>
 struct R3Pos {
-  int ui, t, fy, i0, j0, zb, xg, yg;
-  double ix, iy, mu01s;
+  int ui, um, t, fy, i0, j0, zb, xg, yg;
+  R ix, iy, mu01s;
   int fl00, fl11, fl01, fl10, fl20, fl21, i22, i02, i12, mc0, mc1, mc2;
   bool interior, v0, v1, v2, q0ok, q1ok, q2ok;
 };
@@ -102,23 +161,31 @@ struct R3Pos {
 // (cur = newest values, nxt = the older ones, overwritten by this plane's
 // results), and the z loop is unrolled by two with the roles swapped, so the
 // carries stay in place instead of being copied register to register.
+template <class V>
 struct R3Carry {
-  cplx r00, r11, r01, r10, r20, r21;  // z-family row sums: cur = plane z, nxt = plane z-1 -> z+1
-  cplx t0, t1, t2;                    // in-plane spreads of u0, u1, u2: cur = plane z
-  cplx f02, f12, f22;                 // in-plane family fluxes of the previous step
-  cplx q0, q1, q2;                    // mass products: cur = plane z, nxt = plane z-1 -> z+1
-  cplx p;                             // p at plane z-1 (cur) -> plane z (nxt)
-  double mu02, mu12;                  // edge averages of planes (z-1, z) (cur) -> (z, z+1) (nxt)
+  typedef typename VT<V>::R R;
+  V r00, r11, r01, r10, r20, r21;  // z-family row sums: cur = plane z, nxt = plane z-1 -> z+1
+  V t0, t1, t2;                    // in-plane spreads of u0, u1, u2: cur = plane z
+  V f02, f12, f22;                 // in-plane family fluxes of the previous step
+  V q0, q1, q2;                    // mass products: cur = plane z, nxt = plane z-1 -> z+1
+  V p;                             // p at plane z-1 (cur) -> plane z (nxt)
+  R mu02, mu12;                    // edge averages of planes (z-1, z) (cur) -> (z, z+1) (nxt)
 };
 
-__device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3Params& P, const R3Pos& Q,
-                                        const cplx* __restrict__ b, cplx* __restrict__ y, int z, int& su0,
-                                        unsigned& seq, R3Carry& cur, R3Carry& nxt) {
-  typedef cplx C;
-  const C zc = mk(0.0, 0.0);
+template <class V>
+__device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const S3Params& P,
+                                        const R3Pos<typename VT<V>::R>& Q, const V* __restrict__ x,
+                                        const V* __restrict__ b, V* __restrict__ y, int z, int& su0,
+                                        unsigned& seq, R3Carry<V>& cur, R3Carry<V>& nxt) {
+  typedef V C;
+  typedef typename VT<V>::R R;
+  constexpr bool F = R3SmemT<V>::F;
+  const C zc = VT<V>::mk(0, 0);
   const Geo& g = P.g;
-  const int ui = Q.ui, t = Q.t, fy = Q.fy;
-  const double beta = P.beta, w = P.w, ih = g.inv_h, wn = P.wn;
+  const int ui = Q.ui, um = Q.um, t = Q.t, fy = Q.fy;
+  const R beta = (R)P.beta, w = (R)P.w, ih = (R)g.inv_h, wn = (R)P.wn;
+  auto IW = [&](int i) -> R { return s3_iw<R>(P, i); };
+  auto IM = [&](int i) -> R { return s3_im<R>(P, i); };
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int n2g = g.gn2;
 
@@ -131,31 +198,39 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
   ++seq;
   if (t == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    r3_issue(S, maps, Q.i0, Q.j0, z + 2, 1, z + 2, 1, z + 1, 1, b != nullptr, z + 1, &S.bar[seq & 1]);
+    r3_issue<V>(S, maps, Q.i0, Q.j0, z + 2, 1, z + 2, 1, z + 1, 1, b != nullptr, z + 1, &S.bar[seq & 1]);
+  }
+  if constexpr (F) {
+    // u0 of plane z+3 and b of plane z+2 by cp.async (one group per plane,
+    // completed at the next plane's barrier)
+    r3_u0_plane(S.u0x[(z + 3) & 3], x + g.off[0], g, Q.i0, Q.j0, z + 3, t);
+    if (b) r3_b_plane(S.bp[(z + 2) & 3], b, g, Q.i0, Q.j0, z + 2, t);
+    r3_cp_commit();
   }
   const int s0 = su0, s1 = su0 == 2 ? 0 : su0 + 1;
   su0 = s1;
-  const C* U0 = S.u[s0][0];
+  const C* U0 = F ? S.u0x[z & 3] : S.u[s0][0];
   const C* U1 = S.u[s0][1];
   const C* U2 = S.u[s0][2];
-  const C* V0 = S.u[s1][0];
+  const C* V0 = F ? S.u0x[(z + 1) & 3] : S.u[s1][0];
   const C* V1 = S.u[s1][1];
   const C* V2 = S.u[s1][2];
-  const double* MUc = S.mu[s0];
-  const double* MUp = S.mu[s1];
-  const double* RHc = S.rho[s0];
-  const double* RHp = S.rho[s1];
-  const double* GAc = S.gam[s0];
-  const double* GAp = S.gam[s1];
+  const R* MUc = S.mu[s0];
+  const R* MUp = S.mu[s1];
+  const R* RHc = S.rho[s0];
+  const R* RHp = S.rho[s1];
+  const R* GAc = S.gam[s0];
+  const R* GAp = S.gam[s1];
+  constexpr int MX = R3SmemT<V>::MX;
   // uniform z quantities (global plane index zg decides the boundary rules)
   const int zg = z + g.zoff;
   const int lz = zg >= 1, hz0 = zg + 1 < n2g, hz1 = zg + 1 < n2g + 1;
-  const double izp = s3_inv<double>((zg + 1 >= 1) + (zg + 1 < n2g));
+  const R izp = s3_inv<R>((zg + 1 >= 1) + (zg + 1 < n2g));
   const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
-  const double al = P.alpha, w2 = P.omega2;
-  auto md = [&](double sr, double sg, double ic) {
-    const double rho_f = sr * ic, gam_f = sg * ic + al;
-    return mk(w2 * rho_f, -w2 * gam_f * rho_f);
+  const R al = (R)P.alpha, w2 = (R)P.omega2;
+  auto md = [&](R sr, R sg, R ic) {
+    const R rho_f = sr * ic, gam_f = sg * ic + al;
+    return VT<V>::mk(w2 * rho_f, -w2 * gam_f * rho_f);
   };
   const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
   const bool zin2 = zg + 1 >= 0 && zg + 1 <= n2g;
@@ -170,18 +245,18 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
   // barriers than it saves). Each result is
   // consumed as soon as it exists (shuffled, stored or folded into a row) to
   // keep live ranges short at the 255-register cap.
-  const double mc00 = MUc[ui], mc_l = MUc[ui - 1], mc_b = MUc[ui - R3_UX], mc_lb = MUc[ui - 1 - R3_UX];
-  const double mp00 = MUp[ui], mp_l = MUp[ui - 1], mp_b = MUp[ui - R3_UX];
-  const double rp00 = RHp[ui], gp00 = GAp[ui];
+  const R mc00 = MUc[um], mc_l = MUc[um - 1], mc_b = MUc[um - MX], mc_lb = MUc[um - 1 - MX];
+  const R mp00 = MUp[um], mp_l = MUp[um - 1], mp_b = MUp[um - MX];
+  const R rp00 = RHp[um], gp00 = GAp[um];
   // mu on the edges (operator.hpp:108 order: first axis outer, second inner)
-  const double mu01 = (mc_lb + mc_l + mc_b + mc00) * Q.mu01s;
-  const double mu02p = (mc_l + mp_l + mc00 + mp00) * (Q.ix * izp);  // edges (z, z+1)
-  const double mu12p = (mc_b + mp_b + mc00 + mp00) * (Q.iy * izp);
+  const R mu01 = (mc_lb + mc_l + mc_b + mc00) * Q.mu01s;
+  const R mu02p = (mc_l + mp_l + mc00 + mp00) * (Q.ix * izp);  // edges (z, z+1)
+  const R mu12p = (mc_b + mp_b + mc00 + mp00) * (Q.iy * izp);
   auto spread = [](C mm, C m0_, C mp, C zm, C z0, C zp, C pm, C p0, C pp) {
-    const C a = mm + mp + 2.0 * m0_;
-    const C c = pm + pp + 2.0 * p0;
-    const C m_ = zm + zp + 2.0 * z0;
-    return a + c + 2.0 * m_;
+    const C a = mm + mp + R(2) * m0_;
+    const C c = pm + pp + R(2) * p0;
+    const C m_ = zm + zp + R(2) * z0;
+    return a + c + R(2) * m_;
   };
   // mass: beta*q + the x neighbours (shuffles) + the z-1 neighbour (the older
   // carried product, whose register the new product then takes); the y
@@ -199,22 +274,22 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     const C v0m = V0[ui - 1], v00 = V0[ui], v0p = V0[ui + 1];
     const C vpm = V0[ui + R3_UX - 1], vp0 = V0[ui + R3_UX], vpp = V0[ui + R3_UX + 1];
     const C u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - R3_UX];
-    const C rn0 = (vmp - vm0) + (vpp - vp0) + 2.0 * (v0p - v00);
-    const C sz0 = (nxt.r00 + 2.0 * cur.r00) + rn0;
+    const C rn0 = (vmp - vm0) + (vpp - vp0) + R(2) * (v0p - v00);
+    const C sz0 = (nxt.r00 + R(2) * cur.r00) + rn0;
     nxt.r00 = rn0;
-    const C d00 = (beta * (u0p - u00) + w * sz0) * (P.inv_wsum[Q.fl00 | zA] * ih);
+    const C d00 = (beta * (u0p - u00) + w * sz0) * (IW(Q.fl00 | zA) * ih);
     o3v = d00;
     const C f0 = mc00 * d00;
     o0v = (r3_up(f0) - f0) * ih;
-    const C rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
-    const C sz1 = (nxt.r01 + 2.0 * cur.r01) + rn1;
+    const C rn1 = (v0m - vmm) + (v0p - vmp) + R(2) * (v00 - vm0);
+    const C sz1 = (nxt.r01 + R(2) * cur.r01) + rn1;
     nxt.r01 = rn1;
-    FY[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[zB | Q.fl01] * ih));
+    FY[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (IW(zB | Q.fl01) * ih));
     const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
-    nxt.f02 = mu02p * ((beta * (v00 - u00) + w * (tn - cur.t0)) * (P.inv_wsum[Q.i02] * ih));
+    nxt.f02 = mu02p * ((beta * (v00 - u00) + w * (tn - cur.t0)) * (IW(Q.i02) * ih));
     nxt.t0 = tn;
     m0 = mass_head(cur.q0, nxt.q0);
-    nxt.q0 = (zin && Q.q0ok) ? md(RHp[ui - 1] + rp00, GAp[ui - 1] + gp00, Q.ix) * v00 : zc;
+    nxt.q0 = (zin && Q.q0ok) ? md(RHp[um - 1] + rp00, GAp[um - 1] + gp00, Q.ix) * v00 : zc;
     SQn[0][t] = nxt.q0;
   }
   // ---- component 1: F11 (cell, +y pair), F10 (edge01, -x pair), F12 (edge12, +z pair)
@@ -223,22 +298,22 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     const C v0m = V1[ui - 1], v00 = V1[ui], v0p = V1[ui + 1];
     const C vpm = V1[ui + R3_UX - 1], vp0 = V1[ui + R3_UX], vpp = V1[ui + R3_UX + 1];
     const C u00 = U1[ui], up0 = U1[ui + R3_UX], u0m = U1[ui - 1];
-    const C rn0 = (vpm - v0m) + (vpp - v0p) + 2.0 * (vp0 - v00);
-    const C sz0 = (nxt.r11 + 2.0 * cur.r11) + rn0;
+    const C rn0 = (vpm - v0m) + (vpp - v0p) + R(2) * (vp0 - v00);
+    const C sz0 = (nxt.r11 + R(2) * cur.r11) + rn0;
     nxt.r11 = rn0;
-    const C d11 = (beta * (up0 - u00) + w * sz0) * (P.inv_wsum[zB | Q.fl11] * ih);
+    const C d11 = (beta * (up0 - u00) + w * sz0) * (IW(zB | Q.fl11) * ih);
     o3v += d11;
     FY[0][t] = mc00 * d11;
-    const C rn1 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
-    const C sz1 = (nxt.r10 + 2.0 * cur.r10) + rn1;
+    const C rn1 = (vm0 - vmm) + (vp0 - vpm) + R(2) * (v00 - v0m);
+    const C sz1 = (nxt.r10 + R(2) * cur.r10) + rn1;
     nxt.r10 = rn1;
-    const C f3 = mu01 * ((beta * (u00 - u0m) + w * sz1) * (P.inv_wsum[zB | Q.fl10] * ih));
+    const C f3 = mu01 * ((beta * (u00 - u0m) + w * sz1) * (IW(zB | Q.fl10) * ih));
     o1v = (f3 - r3_dn(f3)) * ih;
     const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
-    nxt.f12 = mu12p * ((beta * (v00 - u00) + w * (tn - cur.t1)) * (P.inv_wsum[Q.i12] * ih));
+    nxt.f12 = mu12p * ((beta * (v00 - u00) + w * (tn - cur.t1)) * (IW(Q.i12) * ih));
     nxt.t1 = tn;
     m1 = mass_head(cur.q1, nxt.q1);
-    nxt.q1 = (zin && Q.q1ok) ? md(RHp[ui - R3_UX] + rp00, GAp[ui - R3_UX] + gp00, Q.iy) * v00 : zc;
+    nxt.q1 = (zin && Q.q1ok) ? md(RHp[um - MX] + rp00, GAp[um - MX] + gp00, Q.iy) * v00 : zc;
     SQn[1][t] = nxt.q1;
   }
   // ---- component 2: F20 (edge02, -x pair), F21 (edge12, -y pair), F22 (cell, +z pair)
@@ -247,28 +322,28 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     const C v0m = V2[ui - 1], v00 = V2[ui], v0p = V2[ui + 1];
     const C vpm = V2[ui + R3_UX - 1], vp0 = V2[ui + R3_UX], vpp = V2[ui + R3_UX + 1];
     const C u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - R3_UX];
-    const C rn0 = (vm0 - vmm) + (vp0 - vpm) + 2.0 * (v00 - v0m);
-    const C sz0 = (nxt.r20 + 2.0 * cur.r20) + rn0;
+    const C rn0 = (vm0 - vmm) + (vp0 - vpm) + R(2) * (v00 - v0m);
+    const C sz0 = (nxt.r20 + R(2) * cur.r20) + rn0;
     nxt.r20 = rn0;
-    const C f4 = cur.mu02 * ((beta * (u00 - u0m) + w * sz0) * (P.inv_wsum[Q.fl20 | zC] * ih));
+    const C f4 = cur.mu02 * ((beta * (u00 - u0m) + w * sz0) * (IW(Q.fl20 | zC) * ih));
     o2v = (f4 - r3_dn(f4)) * ih;
-    const C rn1 = (v0m - vmm) + (v0p - vmp) + 2.0 * (v00 - vm0);
-    const C sz1 = (nxt.r21 + 2.0 * cur.r21) + rn1;
+    const C rn1 = (v0m - vmm) + (v0p - vmp) + R(2) * (v00 - vm0);
+    const C sz1 = (nxt.r21 + R(2) * cur.r21) + rn1;
     nxt.r21 = rn1;
-    FY[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (P.inv_wsum[Q.fl21 | zC] * ih));
+    FY[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (IW(Q.fl21 | zC) * ih));
     const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
-    const C d22 = (beta * (v00 - u00) + w * (tn - cur.t2)) * (P.inv_wsum[Q.i22] * ih);  // cell (q, z)
+    const C d22 = (beta * (v00 - u00) + w * (tn - cur.t2)) * (IW(Q.i22) * ih);  // cell (q, z)
     o3v += d22;
     nxt.f22 = mc00 * d22;  // zero-filled mu masks cells outside the box
     nxt.t2 = tn;
     m2 = mass_head(cur.q2, nxt.q2);
-    nxt.q2 = (zin2 && Q.q2ok) ? md(RHc[ui] + rp00, GAc[ui] + gp00, izp) * v00 : zc;
+    nxt.q2 = (zin2 && Q.q2ok) ? md(RHc[um] + rp00, GAc[um] + gp00, izp) * v00 : zc;
     SQn[2][t] = nxt.q2;
   }
   nxt.mu02 = mu02p;
   nxt.mu12 = mu12p;
   const C pc = S.p[s0][ui];
-  o3v += S.ilm[s0][ui] * pc;
+  o3v += S.ilm[s0][um] * pc;
   // x-neighbour p by shuffle (lanes 0 and 31 are halo: their wrapped values
   // are never used)
   pt0 = (pc - r3_up(pc)) * ih;
@@ -276,6 +351,7 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
   pt2 = pc - cur.p;
   nxt.p = pc;
   }
+  if constexpr (F) r3_cp_wait<1>();  // this thread's cp.async group of the previous plane
   __syncthreads();
 
   if (Q.interior && z >= Q.zb) {
@@ -292,24 +368,24 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
     m0 += wn * SQ[0][t - R3_FX];
     m0 += wn * SQ[0][t + R3_FX];
     m0 += wn * nxt.q0;
-    o0v -= m0 * P.inv_msum[Q.mc0 + czz];
+    o0v -= m0 * IM(Q.mc0 + czz);
     o0v += pt0;
     o1v += (FY[0][t - R3_FX] - FY[0][t]) * ih;
     o1v += (cur.f12 - nxt.f12) * ih;
     m1 += wn * SQ[1][t - R3_FX];
     m1 += wn * SQ[1][t + R3_FX];
     m1 += wn * nxt.q1;
-    o1v -= m1 * P.inv_msum[Q.mc1 + czz];
+    o1v -= m1 * IM(Q.mc1 + czz);
     o1v += (pt1 - S.p[s0][ui - R3_UX]) * ih;
     o2v += (FY[2][t] - FY[2][t + R3_FX]) * ih;
     o2v += (cur.f22 - nxt.f22) * ih;
     m2 += wn * SQ[2][t - R3_FX];
     m2 += wn * SQ[2][t + R3_FX];
     m2 += wn * nxt.q2;
-    o2v -= m2 * P.inv_msum[Q.mc2 + lz + hz1];
+    o2v -= m2 * IM(Q.mc2 + lz + hz1);
     o2v += pt2 * ih;
     if (b) {  // b planes arrived with this step's load group (TMA, zero outside)
-      const C(*BP)[R3_THREADS] = S.bp[s0];
+      const C(*BP)[R3_THREADS] = S.bp[F ? (z & 3) : s0];
       o0v = BP[0][t] - o0v;
       o1v = BP[1][t] - o1v;
       o2v = BP[2][t] - o2v;
@@ -322,11 +398,14 @@ __device__ __forceinline__ void r3_step(R3Smem& S, const R3Maps& maps, const S3P
   }
 }
 
+template <class V>
 __global__ void __launch_bounds__(R3_THREADS, 1)
     k_stencil3d_rr(const __grid_constant__ R3Maps maps, const __grid_constant__ S3Params P,
-                   const cplx* __restrict__ b, cplx* __restrict__ y) {
+                   const V* __restrict__ x, const V* __restrict__ b, V* __restrict__ y) {
+  typedef typename VT<V>::R R;
+  constexpr bool F = R3SmemT<V>::F;
   extern __shared__ __align__(1024) unsigned char r3_raw[];
-  R3Smem& S = *reinterpret_cast<R3Smem*>(r3_raw);
+  R3SmemT<V>& S = *reinterpret_cast<R3SmemT<V>*>(r3_raw);
   const Geo& g = P.g;
   const int t = threadIdx.x, fx = t & 31, fy = t >> 5;
   const int n0 = g.n[0], n1 = g.n[1];
@@ -343,11 +422,13 @@ __global__ void __launch_bounds__(R3_THREADS, 1)
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int tile = item % (P.ntiles_x * P.ntiles_y);
     const int chunk = item / (P.ntiles_x * P.ntiles_y);
-    R3Pos Q;
+    R3Pos<R> Q;
     Q.t = t;
     Q.fy = fy;
-    Q.ui = (fx + 1) + R3_UX * (fy + 1);  // own index in the u / p / media windows
+    Q.ui = (fx + 1) + R3_UX * (fy + 1);  // own index in the u / p windows
     Q.i0 = (tile % P.ntiles_x) * R3_TX;
+    // media window: origin column (i0-2) rounded down to a 16-byte boundary
+    Q.um = (fx + 1 + (F ? ((Q.i0 - 2) & 3) : 0)) + R3SmemT<V>::MX * (fy + 1);
     Q.j0 = (tile / P.ntiles_x) * R3_TY;
     const int zspan = P.z_hi - P.z_lo;
     Q.zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
@@ -357,8 +438,8 @@ __global__ void __launch_bounds__(R3_THREADS, 1)
     Q.yg = yg;
     const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
     const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
-    Q.ix = s3_inv<double>(lx + hx1);
-    Q.iy = s3_inv<double>(ly + hy1);
+    Q.ix = s3_inv<R>(lx + hx1);
+    Q.iy = s3_inv<R>(ly + hy1);
     Q.fl00 = ly | (hy0 << 1);
     Q.fl11 = (lx << 2) | (hx0 << 3);
     Q.fl01 = (lx << 2) | (hx1 << 3);
@@ -384,38 +465,48 @@ __global__ void __launch_bounds__(R3_THREADS, 1)
     const int zs = Q.zb - 2 - ((zend - Q.zb) & 1);
     if (t == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      r3_issue(S, maps, Q.i0, Q.j0, zs, 2, zs, 2, zs, 1, false, 0, &S.bar[seq & 1]);
+      r3_issue<V>(S, maps, Q.i0, Q.j0, zs, 2, zs, 2, zs, 1, false, 0, &S.bar[seq & 1]);
     }
-    R3Carry A, B;
+    if constexpr (F) {  // u0 planes zs, zs+1 now, zs+2 in flight (completed at step zs's barrier)
+      r3_u0_plane(S.u0x[zs & 3], x + g.off[0], g, Q.i0, Q.j0, zs, t);
+      r3_u0_plane(S.u0x[(zs + 1) & 3], x + g.off[0], g, Q.i0, Q.j0, zs + 1, t);
+      r3_cp_commit();
+      r3_u0_plane(S.u0x[(zs + 2) & 3], x + g.off[0], g, Q.i0, Q.j0, zs + 2, t);
+      r3_cp_commit();
+      r3_cp_wait<1>();
+      __syncthreads();
+    }
+    R3Carry<V> A, B;
     {
-      const cplx zc = mk(0.0, 0.0);
+      const V zc = VT<V>::mk(0, 0);
       A.r00 = A.r11 = A.r01 = A.r10 = A.r20 = A.r21 = zc;
       A.t0 = A.t1 = A.t2 = A.f02 = A.f12 = A.f22 = A.q0 = A.q1 = A.q2 = A.p = zc;
-      A.mu02 = A.mu12 = 0.0;
+      A.mu02 = A.mu12 = R(0);
       B = A;
     }
     int su0 = s3_mod3(zs);  // ring slot of plane z (u, p and media alike)
     for (int z = zs; z < zend; z += 2) {
-      r3_step(S, maps, P, Q, b, y, z, su0, seq, A, B);
-      r3_step(S, maps, P, Q, b, y, z + 1, su0, seq, B, A);
+      r3_step<V>(S, maps, P, Q, x, b, y, z, su0, seq, A, B);
+      r3_step<V>(S, maps, P, Q, x, b, y, z + 1, su0, seq, B, A);
     }
-    // drain the group issued by the last step before the next item reuses smem
+    // drain the groups issued by the last step before the next item reuses smem
     s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
     ++seq;
+    if constexpr (F) r3_cp_wait<0>();
     __syncthreads();
   }
 }
 
-// 3D float64 map over a (d0, d1, d2) array with box (box0, box1, 1).
+// 3D float64 / float32 map over a (d0, d1, d2) array with box (box0, box1, 1).
 inline bool r3_encode(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, int64_t d2, int box0,
-                      int box1) {
+                      int box1, int esize = 8) {
   EncodeTiledFn enc = s3_encoder();
   if (!enc) return false;
   const cuuint64_t dim[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
-  const cuuint64_t str[2] = {(cuuint64_t)(d0 * 8), (cuuint64_t)(d0 * d1 * 8)};
+  const cuuint64_t str[2] = {(cuuint64_t)(d0 * esize), (cuuint64_t)(d0 * d1 * esize)};
   const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1};
   const cuuint32_t es[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dim, str, box, es,
+  return enc(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dim, str, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -428,7 +519,9 @@ inline int r3_device_init() {
   if (dev < 0 || dev >= 64) dev = 0;
   std::lock_guard<std::mutex> lock(mu);
   if (!nsm_of[dev]) {
-    cudaFuncSetAttribute(k_stencil3d_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(R3Smem));
+    cudaFuncSetAttribute(k_stencil3d_rr<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(R3Smem));
+    cudaFuncSetAttribute(k_stencil3d_rr<cplxf>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(R3SmemT<cplxf>));
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     nsm_of[dev] = nsm > 0 ? nsm : 148;
@@ -436,12 +529,17 @@ inline int r3_device_init() {
   return nsm_of[dev];
 }
 
-// media_soa: 4 consecutive cell arrays {mu, rho, gamma, 1/(lambda+mu)}.
-// Output planes [z_lo, z_hi) (default: all, including the top u2 faces).
-inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
-                             const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+// media_soa: 4 consecutive cell arrays {mu, rho, gamma, 1/(lambda+mu)}
+// (float for the complex64 kernel). Output planes [z_lo, z_hi) (default:
+// all, including the top u2 faces).
+template <class V>
+inline void launch_stencil3d_rr(const Geo& g, const OpPar& P, const typename VT<V>::R* media_soa, const V* x,
+                                const V* b, V* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  typedef typename VT<V>::R R;
+  constexpr bool F = sizeof(R) == 4;
+  constexpr int es = sizeof(R);
   const int nsm = r3_device_init();
-  // tensor maps depend only on (buffer, media, dims): cache them so the
+  // tensor maps depend only on (buffers, media, dims): cache them so the
   // per-launch host cost is a lookup (buffers are fixed per level).
   struct Entry {
     const void* x;
@@ -455,9 +553,10 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const void* bkey = F ? nullptr : (const void*)b;  // complex64 b arrives by cp.async
   const R3Maps* Mp = nullptr;
   for (const Entry& e : cache)
-    if (e.x == x && e.m == media_soa && e.b == b && e.n[0] == n0 && e.n[1] == n1 && e.n[2] == n2) {
+    if (e.x == x && e.m == media_soa && e.b == bkey && e.n[0] == n0 && e.n[1] == n1 && e.n[2] == n2) {
       Mp = &e.M;
       break;
     }
@@ -465,20 +564,23 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
     Entry e;
     e.x = x;
     e.m = media_soa;
-    e.b = b;
+    e.b = bkey;
     e.n[0] = n0, e.n[1] = n1, e.n[2] = n2;
-    for (int k = 0; k < 3; ++k)
-      r3_encode(&e.M.m.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_UX, R3_UY);
-    r3_encode(&e.M.m.p, x + g.off[3], 2 * n0, n1, n2, 2 * R3_UX, R3_UY);
+    for (int k = F ? 1 : 0; k < 3; ++k)
+      r3_encode(&e.M.m.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_UX, R3_UY,
+                es);
+    r3_encode(&e.M.m.p, x + g.off[3], 2 * n0, n1, n2, 2 * R3_UX, R3_UY, es);
     const int64_t nc = g.ncells;
-    r3_encode(&e.M.m.mu, media_soa + 0 * nc, n0, n1, n2, R3_UX, R3_UY);
-    r3_encode(&e.M.m.rho, media_soa + 1 * nc, n0, n1, n2, R3_UX, R3_UY);
-    r3_encode(&e.M.m.gam, media_soa + 2 * nc, n0, n1, n2, R3_UX, R3_UY);
-    r3_encode(&e.M.m.ilm, media_soa + 3 * nc, n0, n1, n2, R3_UX, R3_UY);
-    if (b) {
+    constexpr int MX = R3SmemT<V>::MX;
+    r3_encode(&e.M.m.mu, media_soa + 0 * nc, n0, n1, n2, MX, R3_UY, es);
+    r3_encode(&e.M.m.rho, media_soa + 1 * nc, n0, n1, n2, MX, R3_UY, es);
+    r3_encode(&e.M.m.gam, media_soa + 2 * nc, n0, n1, n2, MX, R3_UY, es);
+    r3_encode(&e.M.m.ilm, media_soa + 3 * nc, n0, n1, n2, MX, R3_UY, es);
+    if (bkey) {
       for (int k = 0; k < 3; ++k)
-        r3_encode(&e.M.b[k], b + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_FX, R3_FY);
-      r3_encode(&e.M.b[3], b + g.off[3], 2 * n0, n1, n2, 2 * R3_FX, R3_FY);
+        r3_encode(&e.M.b[k], b + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_FX, R3_FY,
+                  es);
+      r3_encode(&e.M.b[3], b + g.off[3], 2 * n0, n1, n2, 2 * R3_FX, R3_FY, es);
     }
     if (cache.size() < 256) {
       cache.push_back(e);
@@ -494,7 +596,22 @@ inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_s
   if (sp.z_hi <= sp.z_lo) return;
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
-  k_stencil3d_rr<<<grid, R3_THREADS, sizeof(R3Smem), s>>>(M, sp, b, y);
+  k_stencil3d_rr<V><<<grid, R3_THREADS, sizeof(R3SmemT<V>), s>>>(M, sp, x, b, y);
+}
+
+inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
+                             const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  launch_stencil3d_rr<cplx>(g, P, media_soa, x, b, y, s, z_lo, z_hi);
+}
+
+// complex64: the register-resident kernel needs 16-byte float media rows
+// (n0 % 4 == 0); other even widths take the cp.async 20-warp kernel.
+inline void launch_stencil3d(const Geo& g, const OpPar& P, const float* media_soa, const cplxf* x,
+                             const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  if (g.n[0] % 4 == 0 && stencil3d_supported(g))
+    launch_stencil3d_rr<cplxf>(g, P, media_soa, x, b, y, s, z_lo, z_hi);
+  else
+    launch_stencil3d_ca(g, P, media_soa, x, b, y, s, z_lo, z_hi);
 }
 
 }  // namespace ehmg
