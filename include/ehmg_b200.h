@@ -112,6 +112,15 @@ int ehmg_multigrid_destroy(ehmg_mg mg);
 int ehmg_multigrid_n_levels(ehmg_mg mg);
 int ehmg_multigrid_cycle(ehmg_mg mg, const double* b, double* x, int where);
 int ehmg_multigrid_precondition(ehmg_mg mg, const double* r, double* z, int where);
+/* multigrid.hpp:136 Multigrid::precondition applied to `count` right-hand
+ * sides held in host memory (r[i] -> z[i]; the multi-source runs of
+ * experiments.hpp call it once per source). The host<->device copies of
+ * neighbouring right-hand sides overlap the cycle of the current one (two
+ * staging buffers per direction, copy streams beside the solver stream);
+ * pinned host buffers are needed for the overlap. Results equal `count`
+ * ehmg_multigrid_precondition calls. Pointers may repeat (an output buffer
+ * reused two or more entries later is written in order). */
+int ehmg_multigrid_precondition_many(ehmg_mg mg, int count, const double* const* r, double* const* z);
 uint64_t ehmg_multigrid_stream(ehmg_mg mg);
 /* Replay `count` preconditioner applications on device buffers and return
  * the CUDA-event time of the whole batch in milliseconds (bench helper). */

@@ -739,10 +739,19 @@ struct ehmg_mg_s {
     cudaGraphExec_t exec;
   };
   std::vector<GraphEntry> graphs;
+  // precondition_many: host<->device copy streams, staging pairs, events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  DBuf<cplx> rst[2], zst[2];
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   ~ehmg_mg_s() {
     for (auto& e : graphs)
       if (e.exec) cudaGraphExecDestroy(e.exec);
     L.clear();
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
+        if (e) cudaEventDestroy(e);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
     if (s) cudaStreamDestroy(s);
   }
 
@@ -1620,6 +1629,52 @@ int ehmg_multigrid_precondition(ehmg_mg mg, const double* r, double* z, int wher
     cplx* dz = out_dev(z, mg->hx, n, where);
     mg->precondition(dr, dz);
     from_dev(z, dz, n, where, mg->s);
+  });
+}
+
+// Three-stage pipeline over right-hand sides i = 0..count-1, staging pair
+// k = i & 1: s_in copies r[i] into rst[k] once the cycle of i-2 released it;
+// the solver stream runs the cycle rst[k] -> zst[k] once that copy landed
+// and the copy-out of i-2 released zst[k]; s_out copies zst[k] to z[i].
+int ehmg_multigrid_precondition_many(ehmg_mg mg, int count, const double* const* r, double* const* z) {
+  return guard([&] {
+    if (count < 0 || (count > 0 && (!r || !z))) throw Err(EHMG_EINVAL, "precondition_many: bad batch");
+    if (count == 0) return;
+    CK(cudaSetDevice(mg->dev));
+    const int64_t n = mg->L[0]->g.ndofs;
+    if (!mg->s_in) {
+      CK(cudaStreamCreateWithFlags(&mg->s_in, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&mg->s_out, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&mg->ev_in[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&mg->ev_comp[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&mg->ev_out[k], cudaEventDisableTiming));
+      }
+    }
+    for (int k = 0; k < 2; ++k) {
+      if (mg->rst[k].n < n) mg->rst[k].alloc(n);
+      if (mg->zst[k].n < n) mg->zst[k].alloc(n);
+    }
+    // nothing in flight from an earlier call may still use the staging pairs
+    CK(cudaEventRecord(mg->ev_comp[0], mg->s));
+    CK(cudaStreamWaitEvent(mg->s_in, mg->ev_comp[0], 0));
+    CK(cudaStreamWaitEvent(mg->s_out, mg->ev_comp[0], 0));
+    for (int i = 0; i < count; ++i) {
+      if (!r[i] || !z[i]) throw Err(EHMG_EINVAL, "precondition_many: null buffer");
+      const int k = i & 1;
+      if (i >= 2) CK(cudaStreamWaitEvent(mg->s_in, mg->ev_comp[k], 0));
+      CK(cudaMemcpyAsync(mg->rst[k].p, r[i], sizeof(cplx) * n, cudaMemcpyHostToDevice, mg->s_in));
+      CK(cudaEventRecord(mg->ev_in[k], mg->s_in));
+      CK(cudaStreamWaitEvent(mg->s, mg->ev_in[k], 0));
+      if (i >= 2) CK(cudaStreamWaitEvent(mg->s, mg->ev_out[k], 0));
+      mg->precondition(mg->rst[k].p, mg->zst[k].p);
+      CK(cudaEventRecord(mg->ev_comp[k], mg->s));
+      CK(cudaStreamWaitEvent(mg->s_out, mg->ev_comp[k], 0));
+      CK(cudaMemcpyAsync(z[i], mg->zst[k].p, sizeof(cplx) * n, cudaMemcpyDeviceToHost, mg->s_out));
+      CK(cudaEventRecord(mg->ev_out[k], mg->s_out));
+    }
+    CK(cudaStreamSynchronize(mg->s_out));
+    CK(cudaStreamSynchronize(mg->s));
   });
 }
 

@@ -108,6 +108,7 @@ def lib():
         L.ehmg_multigrid_n_levels.argtypes = [vp]
         L.ehmg_multigrid_cycle.argtypes = [vp, vp, vp, C.c_int]
         L.ehmg_multigrid_precondition.argtypes = [vp, vp, vp, C.c_int]
+        L.ehmg_multigrid_precondition_many.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
         L.ehmg_multigrid_stream.argtypes = [vp]
         L.ehmg_multigrid_stream.restype = C.c_uint64
         L.ehmg_multigrid_time_precondition.argtypes = [vp, vp, vp, C.c_int, dp]
@@ -627,6 +628,28 @@ class Multigrid:
             raise ValueError("r and z must both be host arrays or both device tensors")
         _check(lib().ehmg_multigrid_precondition(self._h, pr, pz, wr))
         return z
+
+    def precondition_many(self, rs, zs=None):
+        """multigrid.hpp:136 precondition over several host right-hand sides
+        (r[i] -> z[i]); host<->device copies of neighbouring right-hand sides
+        overlap the current cycle (pinned host arrays for the overlap).
+        Output arrays may repeat (written in order)."""
+        rs = list(rs)
+        if zs is None:
+            zs = [np.zeros(self.n, np.complex128) for _ in rs]
+        zs = list(zs)
+        if len(zs) != len(rs):
+            raise ValueError("precondition_many: as many outputs as right-hand sides")
+        pr = (C.c_void_p * max(1, len(rs)))()
+        pz = (C.c_void_p * max(1, len(rs)))()
+        for i, (r, z) in enumerate(zip(rs, zs)):
+            a, wr = _ptr(r, self.n)
+            b, wz = _ptr(z, self.n, writable=True)
+            if wr != HOST or wz != HOST:
+                raise ValueError("precondition_many takes host arrays (device buffers: precondition)")
+            pr[i], pz[i] = a, b
+        _check(lib().ehmg_multigrid_precondition_many(self._h, len(rs), pr, pz))
+        return zs
 
     def time_precondition(self, r_dev, z_dev, count: int) -> float:
         """CUDA-event time (ms) of `count` preconditioner applications."""
