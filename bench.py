@@ -434,8 +434,9 @@ def run_b200(args, ws, rank, local):
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": NCU_TRAFFIC.get(f"{kname}@L{klev}") if n == N_CELLS else None,
                      "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
-                     "limiter": ("shared-memory/shuffle (LSU) pipe ~74% busy + FP64 latency at 8 warps x 254 "
-                                 "registers (ncu: IPC 1.64, FP64 pipe 44%, DRAM 38%); see DESIGN.md"),
+                     "limiter": ("shared-memory/shuffle (LSU) pipe: 477 B of LSU traffic per DOF vs 56 B of "
+                                 "HBM, LSU bound = 67% of the HBM roofline; ncu: LSU 74% busy, IPC 1.64, FP64 "
+                                 "pipe 44%, DRAM 38% at 8 warps x 254 registers; see DESIGN.md"),
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "clocks": clocks,
     }
