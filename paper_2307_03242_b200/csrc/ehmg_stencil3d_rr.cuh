@@ -172,9 +172,55 @@ struct R3Carry {
   R mu02, mu12;                    // edge averages of planes (z-1, z) (cur) -> (z, z+1) (nxt)
 };
 
+// Per-position constants of thread t for the tile at (i0, j0).
+template <class V>
+__device__ __forceinline__ R3Pos<typename VT<V>::R> r3_pos(const Geo& g, int t, int i0, int j0, int zb) {
+  typedef typename VT<V>::R R;
+  constexpr bool F = R3SmemT<V>::F;
+  const int fx = t & 31, fy = t >> 5;
+  const int n0 = g.n[0], n1 = g.n[1];
+  R3Pos<R> Q;
+  Q.t = t;
+  Q.fy = fy;
+  Q.ui = (fx + 1) + R3_UX * (fy + 1);  // own index in the u / p windows
+  Q.i0 = i0;
+  // media window: origin column (i0-2) rounded down to a 16-byte boundary
+  Q.um = (fx + 1 + (F ? ((Q.i0 - 2) & 3) : 0)) + R3SmemT<V>::MX * (fy + 1);
+  Q.j0 = j0;
+  Q.zb = zb;
+  const int xg = Q.i0 - 1 + fx, yg = Q.j0 - 1 + fy;
+  Q.xg = xg;
+  Q.yg = yg;
+  const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
+  const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
+  Q.ix = s3_inv<R>(lx + hx1);
+  Q.iy = s3_inv<R>(ly + hy1);
+  Q.fl00 = ly | (hy0 << 1);
+  Q.fl11 = (lx << 2) | (hx0 << 3);
+  Q.fl01 = (lx << 2) | (hx1 << 3);
+  Q.fl10 = (ly << 2) | (hy1 << 3);
+  Q.fl20 = ly | (hy0 << 1);
+  Q.fl21 = lx | (hx0 << 1);
+  Q.i22 = lx | (hx0 << 1) | (ly << 2) | (hy0 << 3);
+  Q.i02 = ly | (hy0 << 1) | (lx << 2) | (hx1 << 3);
+  Q.i12 = lx | (hx0 << 1) | (ly << 2) | (hy1 << 3);
+  Q.mu01s = Q.ix * Q.iy;
+  Q.mc0 = (lx + (xg + 1 < n0 + 1)) + (ly + hy0);
+  Q.mc1 = (lx + hx0) + (ly + (yg + 1 < n1 + 1));
+  Q.mc2 = (lx + hx0) + (ly + hy0);
+  Q.interior = fx >= 1 && fx <= R3_TX && fy >= 1 && fy <= R3_TY;
+  Q.v0 = Q.interior && xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
+  Q.v1 = Q.interior && xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
+  Q.v2 = Q.interior && xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
+  Q.q0ok = xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
+  Q.q1ok = xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
+  Q.q2ok = xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
+  return Q;
+}
+
 template <class V>
 __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const S3Params& P,
-                                        const R3Pos<typename VT<V>::R>& Q, const V* __restrict__ x,
+                                        const R3Pos<typename VT<V>::R>& Qb, const V* __restrict__ x,
                                         const V* __restrict__ b, V* __restrict__ y, int z, int& su0,
                                         unsigned& seq, R3Carry<V>& cur, R3Carry<V>& nxt) {
   typedef V C;
@@ -182,6 +228,7 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   constexpr bool F = R3SmemT<V>::F;
   const C zc = VT<V>::mk(0, 0);
   const Geo& g = P.g;
+  const R3Pos<R>& Q = Qb;
   const int ui = Q.ui, um = Q.um, t = Q.t, fy = Q.fy;
   const R beta = (R)P.beta, w = (R)P.w, ih = (R)g.inv_h, wn = (R)P.wn;
   auto IW = [&](int i) -> R { return s3_iw<R>(P, i); };
@@ -422,44 +469,10 @@ __global__ void __launch_bounds__(R3_THREADS, 1)
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int tile = item % (P.ntiles_x * P.ntiles_y);
     const int chunk = item / (P.ntiles_x * P.ntiles_y);
-    R3Pos<R> Q;
-    Q.t = t;
-    Q.fy = fy;
-    Q.ui = (fx + 1) + R3_UX * (fy + 1);  // own index in the u / p windows
-    Q.i0 = (tile % P.ntiles_x) * R3_TX;
-    // media window: origin column (i0-2) rounded down to a 16-byte boundary
-    Q.um = (fx + 1 + (F ? ((Q.i0 - 2) & 3) : 0)) + R3SmemT<V>::MX * (fy + 1);
-    Q.j0 = (tile / P.ntiles_x) * R3_TY;
     const int zspan = P.z_hi - P.z_lo;
-    Q.zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
+    const int zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
     const int zend = P.z_lo + (int)(((int64_t)(chunk + 1) * zspan) / P.nchunks);
-    const int xg = Q.i0 - 1 + fx, yg = Q.j0 - 1 + fy;
-    Q.xg = xg;
-    Q.yg = yg;
-    const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
-    const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
-    Q.ix = s3_inv<R>(lx + hx1);
-    Q.iy = s3_inv<R>(ly + hy1);
-    Q.fl00 = ly | (hy0 << 1);
-    Q.fl11 = (lx << 2) | (hx0 << 3);
-    Q.fl01 = (lx << 2) | (hx1 << 3);
-    Q.fl10 = (ly << 2) | (hy1 << 3);
-    Q.fl20 = ly | (hy0 << 1);
-    Q.fl21 = lx | (hx0 << 1);
-    Q.i22 = lx | (hx0 << 1) | (ly << 2) | (hy0 << 3);
-    Q.i02 = ly | (hy0 << 1) | (lx << 2) | (hx1 << 3);
-    Q.i12 = lx | (hx0 << 1) | (ly << 2) | (hy1 << 3);
-    Q.mu01s = Q.ix * Q.iy;
-    Q.mc0 = (lx + (xg + 1 < n0 + 1)) + (ly + hy0);
-    Q.mc1 = (lx + hx0) + (ly + (yg + 1 < n1 + 1));
-    Q.mc2 = (lx + hx0) + (ly + hy0);
-    Q.interior = fx >= 1 && fx <= R3_TX && fy >= 1 && fy <= R3_TY;
-    Q.v0 = Q.interior && xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
-    Q.v1 = Q.interior && xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
-    Q.v2 = Q.interior && xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
-    Q.q0ok = xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
-    Q.q1ok = xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
-    Q.q2ok = xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
+    const R3Pos<R> Q = r3_pos<V>(g, t, (tile % P.ntiles_x) * R3_TX, (tile / P.ntiles_x) * R3_TY, zb);
 
     // two warm-up planes (three when needed to make the step count even)
     const int zs = Q.zb - 2 - ((zend - Q.zb) & 1);
