@@ -103,6 +103,32 @@ struct SlabLevel {
   DBuf<cplx> r, bc, ec, in_lo, in_hi, ctmp;
   cplx* peer_lo = nullptr;  // inbox pointers (own or IPC-mapped)
   cplx* peer_hi = nullptr;
+  // complex64 hierarchy (precision 1, experiments.hpp:241)
+  DBuf<cplxf> rf, bcf, ecf, in_lof, in_hif, ctmpf;
+  cplxf* peer_lof = nullptr;
+  cplxf* peer_hif = nullptr;
+};
+// slab-level vectors by element type
+template <class V> struct SB;
+template <> struct SB<cplx> {
+  static cplx* r(SlabLevel& L) { return L.r.p; }
+  static cplx* bc(SlabLevel& L) { return L.bc.p; }
+  static cplx* ec(SlabLevel& L) { return L.ec.p; }
+  static cplx* ctmp(SlabLevel& L) { return L.ctmp.p; }
+  static cplx* in_lo(SlabLevel& L) { return L.in_lo.p; }
+  static cplx* in_hi(SlabLevel& L) { return L.in_hi.p; }
+  static cplx* peer_lo(const SlabLevel& L) { return L.peer_lo; }
+  static cplx* peer_hi(const SlabLevel& L) { return L.peer_hi; }
+};
+template <> struct SB<cplxf> {
+  static cplxf* r(SlabLevel& L) { return L.rf.p; }
+  static cplxf* bc(SlabLevel& L) { return L.bcf.p; }
+  static cplxf* ec(SlabLevel& L) { return L.ecf.p; }
+  static cplxf* ctmp(SlabLevel& L) { return L.ctmpf.p; }
+  static cplxf* in_lo(SlabLevel& L) { return L.in_lof.p; }
+  static cplxf* in_hi(SlabLevel& L) { return L.in_hif.p; }
+  static cplxf* peer_lo(const SlabLevel& L) { return L.peer_lof; }
+  static cplxf* peer_hi(const SlabLevel& L) { return L.peer_hif; }
 };
 
 struct ehmg_slab_mg_s {
@@ -118,9 +144,19 @@ struct ehmg_slab_mg_s {
   std::unique_ptr<ehmg_mg_s> rep;                           // replicated levels [La, nl)
   DBuf<cplx> brep, erep;                                    // level-La full rhs / correction (this rank)
   std::vector<cplx*> brep_of;                               // every rank's brep (own or IPC-mapped)
+  int prec = 0;                                             // 1: complex64 hierarchy
+  DBuf<cplxf> brepf, erepf;
+  std::vector<cplxf*> brepf_of;
+  std::vector<std::unique_ptr<DBuf<cplxf>>> bwf, xwf;      // complex64 level-0 windows
   std::vector<void*> mapped;                                // IPC mappings to close
   std::vector<std::unique_ptr<DBuf<cplx>>> bw, xw;         // level-0 windows of local slabs
   int64_t exchanged_bytes = 0;
+  const std::vector<cplx*>& rep_of(cplx*) const { return brep_of; }
+  const std::vector<cplxf*>& rep_of(cplxf*) const { return brepf_of; }
+  cplx* rep_b(cplx*) { return brep.p; }
+  cplxf* rep_b(cplxf*) { return brepf.p; }
+  cplx* rep_e(cplx*) { return erep.p; }
+  cplxf* rep_e(cplxf*) { return erepf.p; }
 
   // Overlap of the smoothing ghost exchanges with the stencil rows that do not
   // read ghost planes: pushes/pulls run on sx, the interior rows on s.
@@ -146,21 +182,25 @@ struct ehmg_slab_mg_s {
     if (comm) comm->barrier();
   }
   void sync_barrier() { sync_barrier(s); }
-  void copy(cplx* dst, const cplx* src, int64_t n, cudaStream_t st) {
+  template <class V>
+  void copy(V* dst, const V* src, int64_t n, cudaStream_t st) {
     if (n <= 0) return;
-    CK(cudaMemcpyAsync(dst, src, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st));
-    exchanged_bytes += (int64_t)sizeof(cplx) * n;
+    CK(cudaMemcpyAsync(dst, src, sizeof(V) * n, cudaMemcpyDeviceToDevice, st));
+    exchanged_bytes += (int64_t)sizeof(V) * n;
   }
-  void copy(cplx* dst, const cplx* src, int64_t n) { copy(dst, src, n, s); }
+  template <class V>
+  void copy(V* dst, const V* src, int64_t n) { copy(dst, src, n, s); }
   // global planes [a, b) of component k between a window array and an inbox block
-  void to_inbox(cplx* inbox, const SlabGeo& dst, bool above, const cplx* v, const SlabGeo& src, int k,
+  template <class V>
+  void to_inbox(V* inbox, const SlabGeo& dst, bool above, const V* v, const SlabGeo& src, int k,
                 cudaStream_t st) {
     int a, b;
     dst.ghost(k, above, a, b);
     const int64_t ps = slab_plane(src.g, k);
     copy(inbox + dst.inbox_off(k, above), v + src.g.off[k] + (a - src.g.zoff) * ps, ps * (b - a), st);
   }
-  void from_inbox(cplx* v, const SlabGeo& dst, bool above, const cplx* inbox, int k, cudaStream_t st) {
+  template <class V>
+  void from_inbox(V* v, const SlabGeo& dst, bool above, const V* inbox, int k, cudaStream_t st) {
     int a, b;
     dst.ghost(k, above, a, b);
     const int64_t ps = slab_plane(dst.g, k);
@@ -168,29 +208,31 @@ struct ehmg_slab_mg_s {
   }
 
   // ghost exchange of one field per local slab (V indexed by slab), copies on st
-  void exchange(int l, const std::vector<cplx*>& V, cudaStream_t st) {
+  template <class V>
+  void exchange(int l, const std::vector<V*>& X, cudaStream_t st) {
     sync_barrier(st);  // neighbours finished updating owned planes and reading inboxes
     for (int q = q_lo; q < q_hi; ++q) {
       const SlabLevel& me = *L[l][q];
       if (q + 1 < P_()) {
         const SlabLevel& up = *L[l][q + 1];
-        for (int k = 0; k < 4; ++k) to_inbox(up.peer_lo, up.sg, false, V[q], me.sg, k, st);
+        for (int k = 0; k < 4; ++k) to_inbox(SB<V>::peer_lo(up), up.sg, false, (const V*)X[q], me.sg, k, st);
       }
       if (q > 0) {
         const SlabLevel& dn = *L[l][q - 1];
-        for (int k = 0; k < 4; ++k) to_inbox(dn.peer_hi, dn.sg, true, V[q], me.sg, k, st);
+        for (int k = 0; k < 4; ++k) to_inbox(SB<V>::peer_hi(dn), dn.sg, true, (const V*)X[q], me.sg, k, st);
       }
     }
     sync_barrier(st);  // all pushes landed
     for (int q = q_lo; q < q_hi; ++q) {
       SlabLevel& me = *L[l][q];
       for (int k = 0; k < 4; ++k) {
-        if (q > 0) from_inbox(V[q], me.sg, false, me.in_lo.p, k, st);
-        if (q + 1 < P_()) from_inbox(V[q], me.sg, true, me.in_hi.p, k, st);
+        if (q > 0) from_inbox(X[q], me.sg, false, (const V*)SB<V>::in_lo(me), k, st);
+        if (q + 1 < P_()) from_inbox(X[q], me.sg, true, (const V*)SB<V>::in_hi(me), k, st);
       }
     }
   }
-  void exchange(int l, const std::vector<cplx*>& V) { exchange(l, V, s); }
+  template <class V>
+  void exchange(int l, const std::vector<V*>& X) { exchange(l, X, s); }
 
   // Output planes of slab q (window-local, [a, b)) whose rows read no ghost
   // plane: rows at plane z read planes z-1..z+1 of every component.
@@ -203,8 +245,12 @@ struct ehmg_slab_mg_s {
   // r = b - H x on every local slab. When x's ghosts are stale (an update
   // since the last exchange) the exchange runs on sx while s computes the
   // interior rows; the rows next to the ghost planes follow the exchange.
-  void residual_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool for_restrict) {
-    auto out = [&](int q) { SlabLevel& sl = *L[l][q]; return for_restrict ? sl.r.p : sl.sm.res.p; };
+  template <class V>
+  void residual_all(int l, const std::vector<V*>& B, const std::vector<V*>& X, bool for_restrict) {
+    auto out = [&](int q) {
+      SlabLevel& sl = *L[l][q];
+      return for_restrict ? SB<V>::r(sl) : sl.sm.resbuf((const V*)nullptr);
+    };
     if (!pend[l]) {
       for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& sl = *L[l][q];
@@ -233,45 +279,49 @@ struct ehmg_slab_mg_s {
     pend[l] = 0;
   }
   // refresh stale ghosts (before transfers read them)
-  void settle(int l, const std::vector<cplx*>& X) {
+  template <class V>
+  void settle(int l, const std::vector<V*>& X) {
     if (!pend[l]) return;
     exchange(l, X);
     pend[l] = 0;
   }
 
-  void sweep_all(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool xzero = false) {
+  template <class V>
+  void sweep_all(int l, const std::vector<V*>& B, const std::vector<V*>& X, bool xzero = false) {
     for (int color = 0; color < 2; ++color) {
       const bool first_zero = xzero && color == 0;  // residual is b itself
       if (!first_zero) residual_all(l, B, X, false);
       for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& sl = *L[l][q];
-        sl.sm.update(sl.sg.g, first_zero ? B[q] : sl.sm.res.p, X[q], opt.damping, color, s);
+        const V* rr = first_zero ? (const V*)B[q] : (const V*)sl.sm.resbuf((const V*)nullptr);
+        sl.sm.update(sl.sg.g, rr, X[q], opt.damping, color, s);
       }
       pend[l] = 1;
     }
   }
 
   // multigrid.hpp:217 cycle_at on the distributed levels (B ghosts valid)
-  void cycle(int l, const std::vector<cplx*>& B, const std::vector<cplx*>& X, bool xzero = false) {
+  template <class V>
+  void cycle(int l, const std::vector<V*>& B, const std::vector<V*>& X, bool xzero = false) {
     const int La = plan.La, nl = plan.nl;
     for (int q = 0; q < opt.nu1; ++q) sweep_all(l, B, X, xzero && q == 0);
     residual_all(l, B, X, true);
     const bool next_coarsest = (l + 2 == nl);
     const int repeat = (opt.cycle == 2 && !next_coarsest) ? 2 : 1;
     if (l + 1 < La) {
-      std::vector<cplx*> BC(P_(), nullptr), EC(P_(), nullptr);
+      std::vector<V*> BC(P_(), nullptr), EC(P_(), nullptr);
       for (int q = q_lo; q < q_hi; ++q) {
         SlabLevel& f = *L[l][q];
         SlabLevel& c = *L[l + 1][q];
-        launch_transfer(f.sg.g, c.sg.g, true, f.r.p, c.bc.p, false, s);
-        CK(cudaMemsetAsync(c.ec.p, 0, sizeof(cplx) * c.sg.g.ndofs, s));
-        BC[q] = c.bc.p;
-        EC[q] = c.ec.p;
+        launch_transfer(f.sg.g, c.sg.g, true, (const V*)SB<V>::r(f), SB<V>::bc(c), false, s);
+        CK(cudaMemsetAsync(SB<V>::ec(c), 0, sizeof(V) * c.sg.g.ndofs, s));
+        BC[q] = SB<V>::bc(c);
+        EC[q] = SB<V>::ec(c);
       }
       exchange(l + 1, BC);
       for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC, r == 0);
       for (int q = q_lo; q < q_hi; ++q)
-        launch_transfer(L[l][q]->sg.g, L[l + 1][q]->sg.g, false, L[l + 1][q]->ec.p, X[q], true, s);
+        launch_transfer(L[l][q]->sg.g, L[l + 1][q]->sg.g, false, (const V*)SB<V>::ec(*L[l + 1][q]), X[q], true, s);
     } else {
       // agglomerate: push each slab's restricted owned planes into every rank's full array
       const Geo& gc = G[La];
@@ -280,32 +330,55 @@ struct ehmg_slab_mg_s {
         SlabLevel& f = *L[l][q];
         const int c0 = f.sg.Z0 / 2, c1 = f.sg.Z1 / 2;
         const Geo cw = make_window(gc, c0, c1);
-        launch_transfer(f.sg.g, cw, true, f.r.p, f.ctmp.p, false, s);
+        launch_transfer(f.sg.g, cw, true, (const V*)SB<V>::r(f), SB<V>::ctmp(f), false, s);
         const bool last = (q + 1 == P_());
-        for (cplx* dst : brep_of)
+        for (V* dst : rep_of((V*)nullptr))
           for (int k = 0; k < 4; ++k) {
             const int b = (k == 2 && last) ? c1 + 1 : c1;
             const int64_t ps = slab_plane(gc, k);
-            copy(dst + gc.off[k] + c0 * ps, f.ctmp.p + cw.off[k], ps * (b - c0));
+            copy(dst + gc.off[k] + c0 * ps, (const V*)SB<V>::ctmp(f) + cw.off[k], ps * (b - c0));
           }
       }
       sync_barrier();  // the full coarse rhs is assembled on every rank
-      CK(cudaMemsetAsync(erep.p, 0, sizeof(cplx) * gc.ndofs, s));
+      V* bb = rep_b((V*)nullptr);
+      V* ee = rep_e((V*)nullptr);
+      CK(cudaMemsetAsync(ee, 0, sizeof(V) * gc.ndofs, s));
       CK(cudaStreamSynchronize(s));
-      for (int r = 0; r < repeat; ++r) rep->cycle_at(0, brep.p, erep.p, r == 0);
+      for (int r = 0; r < repeat; ++r) rep->cycle_t<V>(0, bb, ee, r == 0);
       CK(cudaStreamSynchronize(rep->s));
-      for (int q = q_lo; q < q_hi; ++q) launch_transfer(L[l][q]->sg.g, gc, false, erep.p, X[q], true, s);
+      for (int q = q_lo; q < q_hi; ++q) launch_transfer(L[l][q]->sg.g, gc, false, (const V*)ee, X[q], true, s);
     }
     for (int q = 0; q < opt.nu2; ++q) sweep_all(l, B, X);
     settle(l, X);
   }
 
-  // z = M r on the level-0 windows of the local slabs (ghosts of B refreshed here)
+  // z = M r on the level-0 windows of the local slabs (ghosts of B refreshed
+  // here); precision 1 converts the windows to complex64 and back
+  // (multigrid.hpp:310 convert_field) around the complex64 cycle.
   void precondition_windows(const std::vector<cplx*>& B, const std::vector<cplx*>& X) {
-    exchange(0, B);
-    for (int q = q_lo; q < q_hi; ++q)
-      CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
-    cycle(0, B, X, true);
+    if (prec == 0) {
+      exchange(0, B);
+      for (int q = q_lo; q < q_hi; ++q)
+        CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
+      cycle(0, B, X, true);
+      return;
+    }
+    std::vector<cplxf*> Bf(P_(), nullptr), Xf(P_(), nullptr);
+    for (int q = q_lo; q < q_hi; ++q) {
+      const int64_t n = L[0][q]->sg.g.ndofs;
+      Bf[q] = bwf[q - q_lo]->p;
+      Xf[q] = xwf[q - q_lo]->p;
+      k_convert<cplxf, cplx><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, B[q], Bf[q]);
+      CK(cudaGetLastError());
+      CK(cudaMemsetAsync(Xf[q], 0, sizeof(cplxf) * n, s));
+    }
+    exchange(0, Bf);  // complex64 ghost planes
+    cycle(0, Bf, Xf, true);
+    for (int q = q_lo; q < q_hi; ++q) {
+      const int64_t n = L[0][q]->sg.g.ndofs;
+      k_convert<cplx, cplxf><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, Xf[q], X[q]);
+      CK(cudaGetLastError());
+    }
   }
 
   // global array <-> level-0 windows of the local slabs
@@ -340,9 +413,13 @@ struct ehmg_slab_mg_s {
   void precondition(const cplx* r, cplx* z) {
     auto B = windows(bw), X = windows(xw);
     scatter(r, B);
-    for (int q = q_lo; q < q_hi; ++q)
-      CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
-    cycle(0, B, X, true);
+    if (prec == 0) {
+      for (int q = q_lo; q < q_hi; ++q)
+        CK(cudaMemsetAsync(X[q], 0, sizeof(cplx) * L[0][q]->sg.g.ndofs, s));
+      cycle(0, B, X, true);
+    } else {
+      precondition_windows(B, X);
+    }
     gather(X, z);
     CK(cudaStreamSynchronize(s));
   }
@@ -354,10 +431,12 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   if (g0.nd != 3) throw Err(EHMG_EINVAL, "slab: z-slab decomposition is 3D only");
   if (opt.cycle == 3) throw Err(EHMG_EINVAL, "slab: K-cycles need a distributed inner Krylov (not supported)");
   if (opt.sweep != 1) throw Err(EHMG_EINVAL, "slab: only red-black sweeps decompose");
-  if (opt.precision != 0) throw Err(EHMG_EINVAL, "slab: mixed precision is single-GPU only");
+  if (opt.precision != 0 && opt.precision != 1) throw Err(EHMG_EINVAL, "slab: precision must be 0 or 1");
   if (!stencil3d_supported(g0)) throw Err(EHMG_EINVAL, "slab: needs an even x extent (TMA stencil)");
   auto sm = std::make_unique<ehmg_slab_mg_s>();
   sm->opt = opt;
+  sm->prec = opt.precision;
+  const bool mixed = opt.precision == 1;
   sm->P = P;
   sm->comm = comm;
   sm->plan = make_slab_plan(g0.n[2], opt.n_levels, nslabs, agg_n2);
@@ -397,16 +476,42 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
       if (sl->local) {
         sl->media.window_of(*gm[l], sm->G[l], w0, w1, s);
         sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1);
-        sl->r.alloc(sl->sg.g.ndofs);
-        if (l > 0) {
-          sl->bc.alloc(sl->sg.g.ndofs);
-          sl->ec.alloc(sl->sg.g.ndofs);
+        const int64_t nd = sl->sg.g.ndofs;
+        const int64_t ilo = std::max<int64_t>(1, sl->sg.inbox_size(false));
+        const int64_t ihi = std::max<int64_t>(1, sl->sg.inbox_size(true));
+        const int64_t nct = l == La - 1 ? make_window(sm->G[La], sl->sg.Z0 / 2, sl->sg.Z1 / 2).ndofs : 0;
+        if (mixed) {
+          // complex64 cache (factorised in double, rounded), float media, float vectors
+          sl->sm.make_float(sl->sg.g, s);
+          sl->media.make_float(sl->sg.g.ncells, s);
+          sl->rf.alloc(nd);
+          if (l > 0) {
+            sl->bcf.alloc(nd);
+            sl->ecf.alloc(nd);
+          }
+          sl->in_lof.alloc(ilo);
+          sl->in_hif.alloc(ihi);
+          sl->peer_lof = sl->in_lof.p;
+          sl->peer_hif = sl->in_hif.p;
+          if (nct) sl->ctmpf.alloc(nct);
+          if (l == 0) {  // complex128 level-0 exchanges of the distributed FGMRES operator
+            sl->in_lo.alloc(ilo);
+            sl->in_hi.alloc(ihi);
+            sl->peer_lo = sl->in_lo.p;
+            sl->peer_hi = sl->in_hi.p;
+          }
+        } else {
+          sl->r.alloc(nd);
+          if (l > 0) {
+            sl->bc.alloc(nd);
+            sl->ec.alloc(nd);
+          }
+          sl->in_lo.alloc(ilo);
+          sl->in_hi.alloc(ihi);
+          sl->peer_lo = sl->in_lo.p;
+          sl->peer_hi = sl->in_hi.p;
+          if (nct) sl->ctmp.alloc(nct);
         }
-        sl->in_lo.alloc(std::max<int64_t>(1, sl->sg.inbox_size(false)));
-        sl->in_hi.alloc(std::max<int64_t>(1, sl->sg.inbox_size(true)));
-        sl->peer_lo = sl->in_lo.p;
-        sl->peer_hi = sl->in_hi.p;
-        if (l == La - 1) sl->ctmp.alloc(make_window(sm->G[La], sl->sg.Z0 / 2, sl->sg.Z1 / 2).ndofs);
       }
       sm->L[l].push_back(std::move(sl));
     }
@@ -414,41 +519,70 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   for (int q = sm->q_lo; q < sm->q_hi; ++q) {
     sm->bw.emplace_back(new DBuf<cplx>(sm->L[0][q]->sg.g.ndofs));
     sm->xw.emplace_back(new DBuf<cplx>(sm->L[0][q]->sg.g.ndofs));
+    if (mixed) {
+      sm->bwf.emplace_back(new DBuf<cplxf>(sm->L[0][q]->sg.g.ndofs));
+      sm->xwf.emplace_back(new DBuf<cplxf>(sm->L[0][q]->sg.g.ndofs));
+    }
   }
   CK(cudaStreamSynchronize(s));
   sm->rep = build_mg(sm->G[La], nullptr, gm[La].get(), P, opt, nl - La);
-  sm->brep.alloc(sm->G[La].ndofs);
-  sm->erep.alloc(sm->G[La].ndofs);
-  sm->brep_of.push_back(sm->brep.p);
+  if (mixed) {
+    sm->brepf.alloc(sm->G[La].ndofs);
+    sm->erepf.alloc(sm->G[La].ndofs);
+    sm->brepf_of.push_back(sm->brepf.p);
+  } else {
+    sm->brep.alloc(sm->G[La].ndofs);
+    sm->erep.alloc(sm->G[La].ndofs);
+    sm->brep_of.push_back(sm->brep.p);
+  }
   if (comm && comm->n > 1) {
     // share inbox and coarse-rhs buffers through CUDA IPC (peer pointers)
     struct Blob {
-      cudaIpcMemHandle_t h[2 * 8 + 1];
+      cudaIpcMemHandle_t h[2 * 8 + 1 + 2];  // inboxes per level, coarse rhs, complex128 level-0 inboxes (mixed)
     } mine{}, all[kCommMaxRanks];
     const int q = comm->rank;
     for (int l = 0; l < La; ++l) {
-      CK(cudaIpcGetMemHandle(&mine.h[2 * l], sm->L[l][q]->in_lo.p));
-      CK(cudaIpcGetMemHandle(&mine.h[2 * l + 1], sm->L[l][q]->in_hi.p));
+      SlabLevel& me = *sm->L[l][q];
+      CK(cudaIpcGetMemHandle(&mine.h[2 * l], mixed ? (void*)me.in_lof.p : (void*)me.in_lo.p));
+      CK(cudaIpcGetMemHandle(&mine.h[2 * l + 1], mixed ? (void*)me.in_hif.p : (void*)me.in_hi.p));
     }
-    CK(cudaIpcGetMemHandle(&mine.h[16], sm->brep.p));
+    CK(cudaIpcGetMemHandle(&mine.h[16], mixed ? (void*)sm->brepf.p : (void*)sm->brep.p));
+    if (mixed) {
+      CK(cudaIpcGetMemHandle(&mine.h[17], sm->L[0][q]->in_lo.p));
+      CK(cudaIpcGetMemHandle(&mine.h[18], sm->L[0][q]->in_hi.p));
+    }
     comm->exchange_blob(&mine, sizeof(Blob), all);
     sm->brep_of.clear();
+    sm->brepf_of.clear();
     for (int r = 0; r < comm->n; ++r) {
       if (r == q) {
-        sm->brep_of.push_back(sm->brep.p);
+        if (mixed) sm->brepf_of.push_back(sm->brepf.p);
+        else sm->brep_of.push_back(sm->brep.p);
         continue;
       }
       auto open = [&](cudaIpcMemHandle_t h) {
         void* p = nullptr;
         CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
         sm->mapped.push_back(p);
-        return static_cast<cplx*>(p);
+        return p;
       };
       for (int l = 0; l < La; ++l) {
-        sm->L[l][r]->peer_lo = open(all[r].h[2 * l]);
-        sm->L[l][r]->peer_hi = open(all[r].h[2 * l + 1]);
+        SlabLevel& peer = *sm->L[l][r];
+        if (mixed) {
+          peer.peer_lof = static_cast<cplxf*>(open(all[r].h[2 * l]));
+          peer.peer_hif = static_cast<cplxf*>(open(all[r].h[2 * l + 1]));
+        } else {
+          peer.peer_lo = static_cast<cplx*>(open(all[r].h[2 * l]));
+          peer.peer_hi = static_cast<cplx*>(open(all[r].h[2 * l + 1]));
+        }
       }
-      sm->brep_of.push_back(open(all[r].h[16]));
+      if (mixed) {
+        sm->brepf_of.push_back(static_cast<cplxf*>(open(all[r].h[16])));
+        sm->L[0][r]->peer_lo = static_cast<cplx*>(open(all[r].h[17]));
+        sm->L[0][r]->peer_hi = static_cast<cplx*>(open(all[r].h[18]));
+      } else {
+        sm->brep_of.push_back(static_cast<cplx*>(open(all[r].h[16])));
+      }
     }
   }
   CK(cudaStreamSynchronize(s));

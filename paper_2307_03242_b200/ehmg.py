@@ -694,10 +694,12 @@ class SlabMultigrid:
     <= agg_n2 agglomerated. Same options and results as Multigrid."""
 
     def __init__(self, grid: StaggeredGrid, media: MediaModel, par: OperatorParams,
-                 opt: MgOptions, nslabs: int, agg_n2: int = 64):
+                 opt: MgOptions, nslabs: int, agg_n2: int = 64, precision: str = "double"):
+        if precision not in ("double", "mixed"):
+            raise ValueError(f"config: unknown precision '{precision}'")
         o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
                     0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
-                    opt.k_inner_iterations, opt.k_inner_rtol)
+                    opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0)
         arrs = media.arrays(grid)
         h = C.c_void_p()
         _check(lib().ehmg_slab_multigrid_create(grid.ndim, _dims_arr(grid.dims), grid.h,
@@ -739,10 +741,13 @@ class DistributedSlabSolver:
     Fields are full host arrays; results carry this rank's owned planes."""
 
     def __init__(self, job: str, rank: int, nranks: int, device: int, grid: StaggeredGrid,
-                 media: MediaModel, par: OperatorParams, opt: MgOptions, agg_n2: int = 64):
+                 media: MediaModel, par: OperatorParams, opt: MgOptions, agg_n2: int = 64,
+                 precision: str = "double"):
+        if precision not in ("double", "mixed"):
+            raise ValueError(f"config: unknown precision '{precision}'")
         o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
                     0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
-                    opt.k_inner_iterations, opt.k_inner_rtol)
+                    opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0)
         arrs = media.arrays(grid)
         h = C.c_void_p()
         _check(lib().ehmg_dist_create(job.encode(), rank, nranks, device, grid.ndim,

@@ -33,10 +33,10 @@ def _problem():
     return g, med, par, opt, r, b
 
 
-def _rank(rank, ws, job, q):
+def _rank(rank, ws, job, q, precision="double"):
     try:
         g, med, par, opt, r, b = _problem()
-        d = E.DistributedSlabSolver(job, rank, ws, 0, g, med, par, opt, agg_n2=8)
+        d = E.DistributedSlabSolver(job, rank, ws, 0, g, med, par, opt, agg_n2=8, precision=precision)
         z = d.precondition(r)
         D0 = E.OperatorParams(par.beta, par.omega, 0.0)
         x, res = d.solve(b, E.KrylovOptions(restart=10, max_iterations=200))
@@ -47,11 +47,11 @@ def _rank(rank, ws, job, q):
         q.put((rank, None, None, None, -1, "error", repr(e)))
 
 
-@pytest.mark.parametrize("ws", [2, 3])
-def test_distributed_slabs_match_single_process(ws):
+@pytest.mark.parametrize("ws,precision", [(2, "double"), (3, "double"), (2, "mixed")])
+def test_distributed_slabs_match_single_process(ws, precision):
     g, med, par, opt, r, b = _problem()
-    z_ref = E.Multigrid(g, med, par, opt).precondition(r)
-    mg = E.Multigrid(g, med, par, opt)
+    z_ref = E.Multigrid(g, med, par, opt, precision=precision).precondition(r)
+    mg = E.Multigrid(g, med, par, opt, precision=precision)
     D0 = E.make_opdata(g, med, E.OperatorParams(par.beta, par.omega, 0.0))
     x_ref = np.zeros(g.n_dofs(), complex)
     res_ref = E.fgmres(D0, mg, b, x_ref, E.KrylovOptions(restart=10, max_iterations=200))
@@ -60,7 +60,7 @@ def test_distributed_slabs_match_single_process(ws):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     job = f"t{os.getpid()}_{uuid.uuid4().hex[:8]}"
-    procs = [ctx.Process(target=_rank, args=(k, ws, job, q)) for k in range(ws)]
+    procs = [ctx.Process(target=_rank, args=(k, ws, job, q, precision)) for k in range(ws)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(ws)]
@@ -77,5 +77,5 @@ def test_distributed_slabs_match_single_process(ws):
         x[mask] = xr[mask]
         cover += mask
     assert np.all(cover == 1)  # owned planes partition the DOFs
-    assert np.abs(z - z_ref).max() / np.abs(z_ref).max() < 1e-13
-    assert np.abs(x - x_ref).max() / np.abs(x_ref).max() < 1e-8
+    assert np.abs(z - z_ref).max() / np.abs(z_ref).max() < (1e-13 if precision == "double" else 1e-12)
+    assert np.abs(x - x_ref).max() / np.abs(x_ref).max() < (1e-8 if precision == "double" else 1e-6)

@@ -58,3 +58,25 @@ def test_slab_preconditioned_fgmres_matches():
     z_ref = E.Multigrid(g, med, par, opt).precondition(b)
     sm = E.SlabMultigrid(g, med, par, opt, nslabs=4, agg_n2=8)
     assert np.abs(sm.precondition(b) - z_ref).max() / np.abs(z_ref).max() < 1e-13
+
+
+@pytest.mark.parametrize("dims,nl,ns,agg", [
+    ((24, 16, 64), 4, 2, 8),
+    ((32, 32, 128), 4, 4, 16),
+])
+def test_slab_mixed_cycle_equals_single_domain_mixed(dims, nl, ns, agg):
+    """precision "mixed" (experiments.hpp:241) in the z-slab mode: the
+    complex64 hierarchy decomposed into slabs reproduces the undecomposed
+    complex64 hierarchy (same float operations on the owned planes)."""
+    g, m, b = _problem(dims, 5)
+    omega = 2 * np.pi * dims[0] / 10
+    par = E.OperatorParams(2 / 3, omega, 0.3)
+    opt = E.MgOptions(n_levels=nl, cycle="v", nu1=2, nu2=2, damping=0.35, vanka_mode="full",
+                      sweep="red_black")
+    z1 = E.Multigrid(g, m, par, opt, precision="mixed").precondition(b)
+    zs = E.SlabMultigrid(g, m, par, opt, nslabs=ns, agg_n2=agg, precision="mixed").precondition(b)
+    zd = E.Multigrid(g, m, par, opt).precondition(b)
+    err = np.abs(zs - z1).max() / np.abs(z1).max()
+    assert err < 1e-12, err
+    # and the mixed cycle stays within float rounding of the complex128 cycle
+    assert np.abs(zs - zd).max() / np.abs(zd).max() < 1e-4
