@@ -307,7 +307,7 @@ __global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict_
 template <int ND, class T = cplx>
 __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
                                                            const T* __restrict__ r, int color, double w,
-                                                           T* __restrict__ x) {
+                                                           T* __restrict__ x, int xzero) {
   typedef typename VT<T>::R R;
   const int nu = full ? 4 : 2, cs = ND * nu + 1;
   const T zero = VT<T>::mk(0, 0);
@@ -331,13 +331,16 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k
       fi[k][0] = g.off[k] + g.flin(k, c);
       fi[k][1] = g.off[k] + g.flin(k, f1);
     }
-    const T rp = r[pi], xp = x[pi], sinv = Q(cs - 1);
+    // xzero: x is zero (or not yet written) on entry -- it is not read, and
+    // this colour's cells also write the zeros no cell of this colour owns
+    // (needs an even n0: the x-partner of every cell has the other colour)
+    const T rp = r[pi], xp = xzero ? zero : x[pi], sinv = Q(cs - 1);
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       rr[k][0] = r[fi[k][0]];
       rr[k][1] = r[fi[k][1]];
-      xx[k][0] = x[fi[k][0]];
-      xx[k][1] = x[fi[k][1]];
+      xx[k][0] = xzero ? zero : x[fi[k][0]];
+      xx[k][1] = xzero ? zero : x[fi[k][1]];
       if (full) {
         U[k][0] = Q(4 * k), U[k][1] = Q(4 * k + 1), U[k][2] = Q(4 * k + 2), U[k][3] = Q(4 * k + 3);
       } else {
@@ -369,6 +372,21 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k
       x[fi[k][1]] = xx[k][1] + wr * du1;
     }
     x[pi] = xp + wr * dp;
+    if (xzero) {
+      // the x-partner (other colour): its p, and its faces on the domain
+      // boundary (interior faces belong to a cell of this colour)
+      int pc[3] = {c[0] ^ 1, c[1], c[2]};
+      x[g.off[ND] + g.clin(pc)] = zero;
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        if (pc[k] == 0) x[g.off[k] + g.flin(k, pc)] = zero;
+        if (pc[k] == g.n[k] - 1) {
+          int f1[3];
+          sh(pc, k, 1, f1);
+          x[g.off[k] + g.flin(k, f1)] = zero;
+        }
+      }
+    }
   }
 }
 

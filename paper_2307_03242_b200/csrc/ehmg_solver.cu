@@ -382,6 +382,9 @@ struct Smoother {
     }
     for (int color = 0; color < 2; ++color) colour_phase(g, P, mr, b, x, w, color, s, xzero && color == 0);
   }
+  // colour 0 of a sweep from a zero iterate can also write x's zeros itself
+  // (no memset) when every cell's x-partner has the other colour
+  static bool zero_fill_ok(const Geo& g) { return g.n[0] % 2 == 0 && g.zoff == 0; }
   // One red-black colour (global parity `color`; windows shift the local parity).
   template <class V>
   void colour_phase(const Geo& g, const OpPar& P, const MediaRef& mr, const V* b, V* x, double w, int color,
@@ -389,19 +392,19 @@ struct Smoother {
     V* rb = resbuf(b);
     const V* r = xzero ? b : rb;
     if (!xzero) launch_residual(g, P, mr, x, b, rb, s);
-    update(g, r, x, w, color, s);
+    update(g, r, x, w, color, s, xzero && zero_fill_ok(g));
   }
   // Vanka update of one colour from a precomputed residual r.
   template <class V>
-  void update(const Geo& g, const V* r, V* x, double w, int color, cudaStream_t s) {
+  void update(const Geo& g, const V* r, V* x, double w, int color, cudaStream_t s, bool xzero = false) {
     const int64_t nt = colour_threads(g);
     const int lc = color ^ (g.zoff & 1);
     const V* cq = cache(r);
     Prof pf("vanka_update", s);
     if (g.nd == 3)
-      k_vanka_update<3, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x);
+      k_vanka_update<3, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x, xzero);
     else
-      k_vanka_update<2, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x);
+      k_vanka_update<2, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x, xzero);
     CK(cudaGetLastError());
   }
 };
@@ -762,14 +765,12 @@ struct ehmg_mg_s {
   void precondition_direct(const cplx* r, cplx* z) {
     const int64_t n = L[0]->g.ndofs;
     if (prec == 0) {
-      CK(cudaMemsetAsync(z, 0, sizeof(cplx) * n, s));
-      cycle_at(0, r, z, true);
+      cycle_at(0, r, z, true);  // cycle_t clears z where the first sweep does not
       return;
     }
     // multigrid.hpp:310 convert_field in, float cycle, convert out
     k_convert<cplxf, cplx><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, r, rin.p);
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(zout.p, 0, sizeof(cplxf) * n, s));
     cycle_t<cplxf>(0, rin.p, zout.p, true);
     k_convert<cplx, cplxf><<<grid_for(n, 148 * 64), kThreads, 0, s>>>(n, zout.p, z);
     CK(cudaGetLastError());
@@ -836,6 +837,10 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
   }
   Level& lev = *L[l];
   Level& nxt = *L[l + 1];
+  // xzero: x holds zero or nothing yet; the first red-black colour writes
+  // every DOF itself where it can, otherwise x is cleared here
+  if (xzero && (opt.sweep == 0 || opt.nu1 == 0 || !Smoother::zero_fill_ok(lev.g)))
+    CK(cudaMemsetAsync(x, 0, sizeof(V) * lev.g.ndofs, s));
   for (int q = 0; q < opt.nu1; ++q)
     lev.sm.sweep(lev.g, lev.P, lev.media.ref(), b, x, opt.damping, opt.sweep, s, xzero && q == 0);
   V* const lr = LB<V>::r(lev);
@@ -843,7 +848,6 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
   V* const nec = LB<V>::ec(nxt);
   launch_residual(lev.g, lev.P, lev.media.ref(), x, b, lr, s);
   launch_transfer(lev.g, nxt.g, true, (const V*)lr, nbc, false, s);
-  CK(cudaMemsetAsync(nec, 0, sizeof(V) * nxt.g.ndofs, s));
   const bool next_coarsest = (l + 2 == nl);
   switch (opt.cycle) {
     case 0:
@@ -863,14 +867,12 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
         ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol,
                                0.99, 2};
         nxt.inner.init(nxt.g.ndofs, opt.k_inner_iterations, s);
+        CK(cudaMemsetAsync(nec, 0, sizeof(V) * nxt.g.ndofs, s));  // the inner solve's initial guess
         std::vector<double> hist;
         Fgmres::Fn A = [&](const cplx* in, cplx* out) {
           launch_residual(nxt.g, nxt.P, nxt.media.ref(), in, nullptr, out, s);
         };
-        Fgmres::Fn M = [&](const cplx* in, cplx* out) {
-          CK(cudaMemsetAsync(out, 0, sizeof(cplx) * nxt.g.ndofs, s));
-          cycle_at(l + 1, in, out, true);
-        };
+        Fgmres::Fn M = [&](const cplx* in, cplx* out) { cycle_at(l + 1, in, out, true); };
         nxt.inner.run(A, M, nxt.bc.p, nxt.ec.p, ko, hist);
       }
       break;
