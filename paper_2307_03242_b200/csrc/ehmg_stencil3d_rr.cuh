@@ -27,10 +27,19 @@
 //  * The edge averages mu02, mu12 of planes (z-1, z) are the previous
 //    plane's (z, z+1) averages, carried: the media ring holds 3 planes.
 //  * Planes stream in by TMA (cp.async.bulk.tensor, mbarrier), one plane
-//    ahead; the hardware zero fill supplies the reference's zero ghosts
-//    (operator.hpp:172 GhostAcc).
+//    ahead, b rows included (residual mode); the hardware zero fill supplies
+//    the reference's zero ghosts (operator.hpp:172 GhostAcc).
+//  * One block barrier per plane: exchange buffers and rings are deep enough
+//    that every slot refilled in a plane was last read before the previous
+//    plane's barrier, so warps finishing a plane early start the next.
+//  * Carried values live in two R3Carry instances whose roles swap every
+//    plane (z loop unrolled by two): no register-to-register copies.
+// Bounded by the LSU pipe (shared memory + shuffles), not HBM: DESIGN.md
+// derives the shared-memory roofline (477 B of LSU traffic per DOF).
 // Results follow the reference's per-term operation order except the
-// in-plane spread noted above (differences of spreads; <= 1e-15 relative).
+// in-plane spread noted above (differences of spreads) and the mass sum's
+// association (x neighbours and z-1 before the y neighbours); <= 3e-16
+// relative against the previous term-order kernel.
 #pragma once
 
 #include "ehmg_stencil3d.cuh"
