@@ -48,6 +48,7 @@ def levels_for(n):
 BETA = 2.0 / 3.0
 ALPHA = 0.5          # shift (the 0.1 default stalls at 5 levels)
 DAMPING = 0.25       # experiments.hpp:221 default for >= 4 levels
+AGG_N2 = 32          # z-slab mode: levels with <= 32 cell planes (< 65^3 nodes) are agglomerated
 SPONGE = 24
 GAMMA_PHYS = 0.01
 LAM, MU, RHO = 2.0, 1.0, 1.0   # cs = 1, cp = 2
@@ -453,7 +454,8 @@ def run_b200(args, ws, rank, local):
 def run_b200_slabs(args, ws, rank, local):
     """N > 1: one z-slab per GPU (strong scaling of one V-cycle over the
     fixed 257^3 problem). Ghost planes move by CUDA-IPC peer copies over
-    NVLink; levels <= 64^3 are agglomerated (replicated on every rank)."""
+    NVLink; levels below 65^3 nodes (<= 32^3 cells) are agglomerated
+    (replicated on every rank), as BASELINE configs[3] states."""
     import torch
     import torch.distributed as dist
     import paper_2307_03242_b200 as E
@@ -470,7 +472,7 @@ def run_b200_slabs(args, ws, rank, local):
                       vanka_mode="full", sweep="red_black")
     t0 = time.perf_counter()
     d = E.DistributedSlabSolver(job, rank, ws, dev, g, med, E.OperatorParams(BETA, omega, ALPHA),
-                                opt, agg_n2=64)
+                                opt, agg_n2=AGG_N2)
     setup_s = time.perf_counter() - t0
     rng = np.random.default_rng(1234)
     N = g.n_dofs()
@@ -529,7 +531,7 @@ def run_b200_slabs(args, ws, rank, local):
                  "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5)}
     d.close()
     cfg = workload_config(n)
-    cfg["parallelism"] = f"z-slab x{ws} (levels <= 64^3 agglomerated)"
+    cfg["parallelism"] = f"z-slab x{ws} (levels below 65^3 nodes agglomerated)"
     return {
         "metric": metric_name(n), "value": round(value, 4), "unit": "V-cycles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
