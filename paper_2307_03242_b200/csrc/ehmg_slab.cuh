@@ -148,6 +148,7 @@ struct ehmg_slab_mg_s {
   DBuf<cplxf> brepf, erepf;
   std::vector<cplxf*> brepf_of;
   std::vector<std::unique_ptr<DBuf<cplxf>>> bwf, xwf;      // complex64 level-0 windows
+  std::vector<void*> cx_of;  // every rank's coarsest-level solution buffer (row-partitioned solve)
   std::vector<void*> mapped;                                // IPC mappings to close
   std::vector<std::unique_ptr<DBuf<cplx>>> bw, xw;         // level-0 windows of local slabs
   int64_t exchanged_bytes = 0;
@@ -538,8 +539,17 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   if (comm && comm->n > 1) {
     // share inbox and coarse-rhs buffers through CUDA IPC (peer pointers)
     struct Blob {
-      cudaIpcMemHandle_t h[2 * 8 + 1 + 2];  // inboxes per level, coarse rhs, complex128 level-0 inboxes (mixed)
+      // inboxes per level, coarse rhs, complex128 level-0 inboxes (mixed), coarsest solution
+      cudaIpcMemHandle_t h[2 * 8 + 1 + 2 + 1];
     } mine{}, all[kCommMaxRanks];
+    // the coarsest level's solution buffer of the replicated hierarchy
+    void* cx = nullptr;
+    {
+      ehmg_mg_s& R = *sm->rep;
+      if (R.L.size() == 1) cx = mixed ? (void*)sm->erepf.p : (void*)sm->erep.p;
+      else cx = mixed ? (void*)R.L.back()->ecf.p : (void*)R.L.back()->ec.p;
+    }
+    CK(cudaIpcGetMemHandle(&mine.h[19], cx));
     const int q = comm->rank;
     for (int l = 0; l < La; ++l) {
       SlabLevel& me = *sm->L[l][q];
@@ -554,8 +564,10 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
     comm->exchange_blob(&mine, sizeof(Blob), all);
     sm->brep_of.clear();
     sm->brepf_of.clear();
+    sm->cx_of.assign(comm->n, nullptr);
     for (int r = 0; r < comm->n; ++r) {
       if (r == q) {
+        sm->cx_of[r] = cx;
         if (mixed) sm->brepf_of.push_back(sm->brepf.p);
         else sm->brep_of.push_back(sm->brep.p);
         continue;
@@ -583,6 +595,28 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
       } else {
         sm->brep_of.push_back(static_cast<cplx*>(open(all[r].h[16])));
       }
+      sm->cx_of[r] = open(all[r].h[19]);
+    }
+    // Row-partitioned coarsest solve: rank q keeps rows [r0, r1) of A^-1
+    // (1/n of the dense inverse, and of the per-cycle GEMV), then pushes its
+    // rows of the solution into every rank's buffer.
+    {
+      ehmg_mg_s& R = *sm->rep;
+      const int64_t nco = R.nco, r0 = nco * q / comm->n, r1 = nco * (q + 1) / comm->n;
+      R.split_coarse(r0, r1, R.s);
+      ehmg_slab_mg_s* smp = sm.get();
+      R.coarse_gather = [smp, r0, r1](void* x, size_t es) {
+        ehmg_mg_s& RR = *smp->rep;
+        NodeComm& cm = *smp->comm;
+        CK(cudaStreamSynchronize(RR.s));
+        cm.barrier();  // every rank has its rows and no longer reads its previous solution
+        for (int r = 0; r < cm.n; ++r)
+          if (r != cm.rank && r1 > r0)
+            CK(cudaMemcpyAsync(static_cast<char*>(smp->cx_of[r]) + r0 * es, static_cast<char*>(x) + r0 * es,
+                               (r1 - r0) * es, cudaMemcpyDeviceToDevice, RR.s));
+        CK(cudaStreamSynchronize(RR.s));
+        cm.barrier();  // all row blocks landed
+      };
     }
   }
   CK(cudaStreamSynchronize(s));

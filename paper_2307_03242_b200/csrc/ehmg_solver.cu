@@ -733,6 +733,29 @@ struct ehmg_mg_s {
   DBuf<cplxf> ainvf, rin, zout;
   const cplx* coarse_inv(const cplx*) const { return ainv.p; }
   const cplxf* coarse_inv(const cplxf*) const { return ainvf.p; }
+  // Row-partitioned coarsest solve (one z-slab per process): this rank keeps
+  // rows [c_r0, c_r1) of A^-1, computes those rows of x and all-gathers x
+  // (coarse_gather pushes the block into every rank's x, then a barrier).
+  int64_t c_r0 = 0, c_r1 = -1;
+  std::function<void(void* x, size_t esize)> coarse_gather;
+  void split_coarse(int64_t r0, int64_t r1, cudaStream_t st) {
+    const int64_t rows = r1 - r0;
+    if (prec == 0) {
+      DBuf<cplx> blk(rows * nco);
+      CK(cudaMemcpyAsync(blk.p, ainv.p + r0 * nco, sizeof(cplx) * rows * nco, cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      std::swap(ainv.p, blk.p);
+      std::swap(ainv.n, blk.n);
+    } else {
+      DBuf<cplxf> blk(rows * nco);
+      CK(cudaMemcpyAsync(blk.p, ainvf.p + r0 * nco, sizeof(cplxf) * rows * nco, cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      std::swap(ainvf.p, blk.p);
+      std::swap(ainvf.n, blk.n);
+    }
+    c_r0 = r0;
+    c_r1 = r1;
+  }
   // CUDA graphs of whole preconditioner applications, one per (r, z) pair:
   // a V(2,2) cycle is ~75 launches, many of them short on the coarse levels.
   struct GraphEntry {
@@ -831,8 +854,16 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
   g_level = l;
   if (l + 1 == nl) {
     Prof pf("coarse_solve", s);
-    k_gemv_rows<V><<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x);
-    CK(cudaGetLastError());
+    if (c_r1 < 0) {
+      k_gemv_rows<V><<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x);
+      CK(cudaGetLastError());
+    } else {
+      const int64_t rows = c_r1 - c_r0;
+      if (rows > 0)
+        k_gemv_rows<V><<<grid_for(rows * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x + c_r0, rows);
+      CK(cudaGetLastError());
+      coarse_gather(x, sizeof(V));
+    }
     return;
   }
   Level& lev = *L[l];
