@@ -164,6 +164,7 @@ struct ehmg_slab_mg_s {
   cudaStream_t sx = nullptr;
   cudaEvent_t ev_upd = nullptr, ev_x = nullptr;
   std::vector<char> pend;  // per level: the smoothed iterate's ghosts are stale
+  std::vector<int> xpar;   // per level: inbox half of the next exchange
 
   ~ehmg_slab_mg_s() {
     for (void* p : mapped) cudaIpcCloseMemHandle(p);
@@ -208,32 +209,51 @@ struct ehmg_slab_mg_s {
     copy(v + dst.g.off[k] + (a - dst.g.zoff) * ps, inbox + dst.inbox_off(k, above), ps * (b - a), st);
   }
 
-  // ghost exchange of one field per local slab (V indexed by slab), copies on st
+  // Ghost exchange of one field per local slab (V indexed by slab). Every
+  // inbox holds two halves used in turn (parity per level; all ranks make
+  // the same exchange calls), and all copies run on sx: a push into parity
+  // k can only follow the neighbour's pulls from k two exchanges back, which
+  // its stream finished before the previous exchange's barrier. One barrier
+  // per exchange: after the pushes, before the pulls.
+  // on_sx: the caller already made sx wait for the update (overlap mode) and
+  // orders s after the pulls itself.
   template <class V>
-  void exchange(int l, const std::vector<V*>& X, cudaStream_t st) {
-    sync_barrier(st);  // neighbours finished updating owned planes and reading inboxes
+  void exchange(int l, const std::vector<V*>& X, bool on_sx = false) {
+    if (!on_sx) {
+      CK(cudaEventRecord(ev_upd, s));
+      CK(cudaStreamWaitEvent(sx, ev_upd, 0));
+    }
+    const int par = xpar[l];
+    xpar[l] ^= 1;
     for (int q = q_lo; q < q_hi; ++q) {
       const SlabLevel& me = *L[l][q];
       if (q + 1 < P_()) {
         const SlabLevel& up = *L[l][q + 1];
-        for (int k = 0; k < 4; ++k) to_inbox(SB<V>::peer_lo(up), up.sg, false, (const V*)X[q], me.sg, k, st);
+        V* box = SB<V>::peer_lo(up) + par * inbox_half(up.sg, false);
+        for (int k = 0; k < 4; ++k) to_inbox(box, up.sg, false, (const V*)X[q], me.sg, k, sx);
       }
       if (q > 0) {
         const SlabLevel& dn = *L[l][q - 1];
-        for (int k = 0; k < 4; ++k) to_inbox(SB<V>::peer_hi(dn), dn.sg, true, (const V*)X[q], me.sg, k, st);
+        V* box = SB<V>::peer_hi(dn) + par * inbox_half(dn.sg, true);
+        for (int k = 0; k < 4; ++k) to_inbox(box, dn.sg, true, (const V*)X[q], me.sg, k, sx);
       }
     }
-    sync_barrier(st);  // all pushes landed
+    sync_barrier(sx);  // all pushes landed
     for (int q = q_lo; q < q_hi; ++q) {
       SlabLevel& me = *L[l][q];
+      const V* lo = (const V*)SB<V>::in_lo(me) + par * inbox_half(me.sg, false);
+      const V* hi = (const V*)SB<V>::in_hi(me) + par * inbox_half(me.sg, true);
       for (int k = 0; k < 4; ++k) {
-        if (q > 0) from_inbox(X[q], me.sg, false, (const V*)SB<V>::in_lo(me), k, st);
-        if (q + 1 < P_()) from_inbox(X[q], me.sg, true, (const V*)SB<V>::in_hi(me), k, st);
+        if (q > 0) from_inbox(X[q], me.sg, false, lo, k, sx);
+        if (q + 1 < P_()) from_inbox(X[q], me.sg, true, hi, k, sx);
       }
     }
+    if (!on_sx) {
+      CK(cudaEventRecord(ev_x, sx));
+      CK(cudaStreamWaitEvent(s, ev_x, 0));
+    }
   }
-  template <class V>
-  void exchange(int l, const std::vector<V*>& X) { exchange(l, X, s); }
+  static int64_t inbox_half(const SlabGeo& sg, bool above) { return std::max<int64_t>(1, sg.inbox_size(above)); }
 
   // Output planes of slab q (window-local, [a, b)) whose rows read no ghost
   // plane: rows at plane z read planes z-1..z+1 of every component.
@@ -267,7 +287,7 @@ struct ehmg_slab_mg_s {
       interior_rows(q, sl.sg, a, b);
       if (b > a) launch_residual(sl.sg.g, P, sl.media.ref(), X[q], B[q], out(q), s, a, b);
     }
-    exchange(l, X, sx);
+    exchange(l, X, true);
     CK(cudaEventRecord(ev_x, sx));
     CK(cudaStreamWaitEvent(s, ev_x, 0));
     for (int q = q_lo; q < q_hi; ++q) {
@@ -466,6 +486,7 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   }
   sm->L.resize(La);
   sm->pend.assign(La, 0);
+  sm->xpar.assign(La, 0);
   for (int l = 0; l < La; ++l) {
     for (int q = 0; q < nslabs; ++q) {
       auto sl = std::make_unique<SlabLevel>();
@@ -478,8 +499,9 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
         sl->media.window_of(*gm[l], sm->G[l], w0, w1, s);
         sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1);
         const int64_t nd = sl->sg.g.ndofs;
-        const int64_t ilo = std::max<int64_t>(1, sl->sg.inbox_size(false));
-        const int64_t ihi = std::max<int64_t>(1, sl->sg.inbox_size(true));
+        // two halves per inbox (exchanges alternate between them)
+        const int64_t ilo = 2 * ehmg_slab_mg_s::inbox_half(sl->sg, false);
+        const int64_t ihi = 2 * ehmg_slab_mg_s::inbox_half(sl->sg, true);
         const int64_t nct = l == La - 1 ? make_window(sm->G[La], sl->sg.Z0 / 2, sl->sg.Z1 / 2).ndofs : 0;
         if (mixed) {
           // complex64 cache (factorised in double, rounded), float media, float vectors
