@@ -30,7 +30,7 @@ def problem(dims, seed=3):
     return g, med, omega
 
 
-@pytest.mark.parametrize("dims", [(64, 64), (32, 32, 32), (36, 20, 24)])
+@pytest.mark.parametrize("dims", [(64, 64), (32, 32, 32), (36, 20, 24), (64, 24, 20)])
 def test_mixed_vcycle_close_to_double(dims):
     g, med, omega = problem(dims)
     opt = E.MgOptions(n_levels=3, cycle="v", nu1=2, nu2=2, damping=0.35, vanka_mode="full",
