@@ -1,9 +1,14 @@
-// ehmg_stencil3d.cuh -- bandwidth-tuned 3D operator / residual kernel.
+// ehmg_stencil3d.cuh -- shared 3D-stencil machinery (tensor-map encoder,
+// TMA/mbarrier helpers, boundary-renormalisation tables, z-chunk planning)
+// and the 11/20-warp shared-memory kernel k_stencil3d.
 //
 // y = H x  or  r = b - H x  for the staggered mixed elastic-Helmholtz
 // operator (operator.hpp:389-421), all four components in one launch.
+// Production kernels live in ehmg_stencil3d_rr.cuh (k_stencil3d_rr); the
+// kernel below now serves only the complex64 hierarchy on widths with
+// n0 % 4 != 0 (its cp.async path), and documents the previous design:
 //
-// Design (B200, complex128, HBM-bound):
+// Design (B200, complex128 and complex64):
 //  * 2.5D tiling. A CTA owns a 33x8 tile of the (i,j) index plane plus a
 //    one-cell flux halo (35x10 = 350 positions, one thread each, 11 warps)
 //    and marches a z-chunk (persistent CTAs stride over tile x chunk items).
