@@ -571,42 +571,62 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const V* __re
   xc[gc.off[C] + o0 + (int64_t)D0 * (o1 + (int64_t)D1 * o2)] = narrow<V>(s2);
 }
 
+// Prolongation(+add) for one component; each thread produces kProlongNX
+// fine values 32 apart along x, so the y/z taps and coarse row addresses
+// (most of the per-output instructions) are formed once per thread.
+constexpr int kProlongNX = 4;
 template <int C, class V = cplx>
 __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const V* __restrict__ xc,
                                                   V* __restrict__ xf, int accumulate) {
-  const int f0 = blockIdx.x * 32 + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y, f2 = blockIdx.z;
+  const int fx0 = blockIdx.x * (32 * kProlongNX) + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y, f2 = blockIdx.z;
   const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
-  if (f0 >= F0 || f1 >= F1) return;
+  if (fx0 >= F0 || f1 >= F1) return;
   const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1), D2 = gc.n[2] + (C == 2);
-  const Taps t0 = prolong_taps(f0, F0, C == 0);
   const Taps t1 = prolong_taps(f1, F1, C == 1);
   const Taps t2 = prolong_taps(f2 + gf.zoff, gf.gn2 + (C == 2), C == 2);
-  V* o = xf + gf.off[C] + f0 + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
-  const V old = accumulate ? *o : V{};  // issued first: overlaps the coarse gathers
   const V* base = xc + gc.off[C];
-  cplx s2 = mk(0, 0);
+  // coarse rows (q2, q1) and whether the z tap lies in this coarse window
+  const V* row[2][2];
+  bool zok[2];
 #pragma unroll
   for (int q2 = 0; q2 < 2; ++q2) {
-    if (q2 >= t2.cnt) break;
-    const int z = t2.idx[q2] - gc.zoff;
-    cplx s1 = mk(0, 0);
-    if (z >= 0 && z < D2) {
+    const int z = (q2 < t2.cnt ? t2.idx[q2] : t2.idx[0]) - gc.zoff;
+    zok[q2] = q2 < t2.cnt && z >= 0 && z < D2;
 #pragma unroll
-      for (int q1 = 0; q1 < 2; ++q1) {
-        if (q1 >= t1.cnt) break;
-        const V* row = base + (int64_t)D0 * (t1.idx[q1] + (int64_t)D1 * z);
-        cplx s0 = mk(0, 0);
-#pragma unroll
-        for (int q0 = 0; q0 < 2; ++q0) {
-          if (q0 >= t0.cnt) break;
-          s0 += t0.w[q0] * wide(row[t0.idx[q0]]);
-        }
-        s1 += t1.w[q1] * s0;
-      }
-    }
-    s2 += t2.w[q2] * s1;
+    for (int q1 = 0; q1 < 2; ++q1)
+      row[q2][q1] = base + (int64_t)D0 * ((q1 < t1.cnt ? t1.idx[q1] : t1.idx[0]) + (int64_t)D1 * (zok[q2] ? z : 0));
   }
-  *o = narrow<V>(accumulate ? wide(old) + s2 : s2);
+  V* orow = xf + gf.off[C] + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
+#pragma unroll
+  for (int k = 0; k < kProlongNX; ++k) {
+    const int f0 = fx0 + 32 * k;
+    if (f0 >= F0) break;
+    const Taps t0 = prolong_taps(f0, F0, C == 0);
+    V* o = orow + f0;
+    const V old = accumulate ? *o : V{};  // issued first: overlaps the coarse gathers
+    // same contraction order as k_transfer (axis 0 innermost)
+    cplx s2 = mk(0, 0);
+#pragma unroll
+    for (int q2 = 0; q2 < 2; ++q2) {
+      if (q2 >= t2.cnt) break;
+      cplx s1 = mk(0, 0);
+      if (zok[q2]) {
+#pragma unroll
+        for (int q1 = 0; q1 < 2; ++q1) {
+          if (q1 >= t1.cnt) break;
+          cplx s0 = mk(0, 0);
+#pragma unroll
+          for (int q0 = 0; q0 < 2; ++q0) {
+            if (q0 >= t0.cnt) break;
+            s0 += t0.w[q0] * wide(row[q2][q1][t0.idx[q0]]);
+          }
+          s1 += t1.w[q1] * s0;
+        }
+      }
+      s2 += t2.w[q2] * s1;
+    }
+    *o = narrow<V>(accumulate ? wide(old) + s2 : s2);
+  }
 }
 
 // ------------------------------------------------------------------ media

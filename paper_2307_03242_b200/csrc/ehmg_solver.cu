@@ -269,7 +269,8 @@ static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, cons
     const dim3 blk(32, 8);
     for (int c = 0; c < 4; ++c) {
       const int d0 = gto.n[0] + (c == 0), d1 = gto.n[1] + (c == 1), d2 = gto.n[2] + (c == 2);
-      const dim3 grd((d0 + 31) / 32, (d1 + 7) / 8, c < 3 ? d2 : gto.n[2]);
+      const int bx = restricting ? 32 : 32 * kProlongNX;  // prolongation: kProlongNX values per thread
+      const dim3 grd((d0 + bx - 1) / bx, (d1 + 7) / 8, c < 3 ? d2 : gto.n[2]);
       if (restricting) {
         if (c == 0) k_restrict3<0, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
         else if (c == 1) k_restrict3<1, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
