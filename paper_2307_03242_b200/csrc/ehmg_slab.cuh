@@ -149,6 +149,7 @@ struct ehmg_slab_mg_s {
   std::vector<cplxf*> brepf_of;
   std::vector<std::unique_ptr<DBuf<cplxf>>> bwf, xwf;      // complex64 level-0 windows
   std::vector<void*> cx_of;  // every rank's coarsest-level solution buffer (row-partitioned solve)
+  std::vector<std::unique_ptr<Fgmres>> kin;  // K-cycle inner Krylov per distributed level
   std::vector<void*> mapped;                                // IPC mappings to close
   std::vector<std::unique_ptr<DBuf<cplx>>> bw, xw;         // level-0 windows of local slabs
   int64_t exchanged_bytes = 0;
@@ -340,7 +341,13 @@ struct ehmg_slab_mg_s {
         EC[q] = SB<V>::ec(c);
       }
       exchange(l + 1, BC);
-      for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC, r == 0);
+      if constexpr (sizeof(V) == sizeof(cplx)) {
+        if (opt.cycle == 3) kcycle(l + 1, BC, EC);
+        else
+          for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC, r == 0);
+      } else {
+        for (int r = 0; r < repeat; ++r) cycle(l + 1, BC, EC, r == 0);
+      }
       for (int q = q_lo; q < q_hi; ++q)
         launch_transfer(L[l][q]->sg.g, L[l + 1][q]->sg.g, false, (const V*)SB<V>::ec(*L[l + 1][q]), X[q], true, s);
     } else {
@@ -365,12 +372,62 @@ struct ehmg_slab_mg_s {
       V* ee = rep_e((V*)nullptr);
       CK(cudaMemsetAsync(ee, 0, sizeof(V) * gc.ndofs, s));
       CK(cudaStreamSynchronize(s));
-      for (int r = 0; r < repeat; ++r) rep->cycle_t<V>(0, bb, ee, r == 0);
+      if constexpr (sizeof(V) == sizeof(cplx)) {
+        if (opt.cycle == 3 && La + 1 < nl) rep->kcycle_top(bb, ee);
+        else
+          for (int r = 0; r < repeat; ++r) rep->cycle_t<V>(0, bb, ee, r == 0);
+      } else {
+        for (int r = 0; r < repeat; ++r) rep->cycle_t<V>(0, bb, ee, r == 0);
+      }
       CK(cudaStreamSynchronize(rep->s));
       for (int q = q_lo; q < q_hi; ++q) launch_transfer(L[l][q]->sg.g, gc, false, (const V*)ee, X[q], true, s);
     }
     for (int q = 0; q < opt.nu2; ++q) sweep_all(l, B, X);
     settle(l, X);
+  }
+
+  // K-cycle coarse correction on distributed level l1 (multigrid.hpp:217, the
+  // cycle_t K branch): inner FGMRES on this rank's window of level l1 with
+  // the distributed operator (ghost exchange, then rows) and M = the
+  // distributed cycle one level down; dot products over the owned planes,
+  // summed in rank order. One local slab (one slab per process).
+  void kcycle(int l1, const std::vector<cplx*>& BC, const std::vector<cplx*>& EC) {
+    const int q = q_lo;
+    SlabLevel& c = *L[l1][q];
+    if (!kin[l1]) kin[l1].reset(new Fgmres());
+    Fgmres& fg = *kin[l1];
+    fg.init(c.sg.g.ndofs, opt.k_inner_iterations, s);
+    fg.blas.comm = comm;
+    fg.blas.owned = owned_ranges(l1, q);
+    ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol, 0.99, 2};
+    std::vector<cplx*> VV(P_(), nullptr), WW(P_(), nullptr);
+    Fgmres::Fn A = [&](const cplx* in, cplx* out) {
+      VV[q] = const_cast<cplx*>(in);  // ghost planes are scratch
+      exchange(l1, VV);
+      launch_residual(c.sg.g, P, c.media.ref(), in, nullptr, out, s);
+    };
+    Fgmres::Fn M = [&](const cplx* in, cplx* out) {
+      VV[q] = const_cast<cplx*>(in);
+      WW[q] = out;
+      exchange(l1, VV);
+      CK(cudaMemsetAsync(out, 0, sizeof(cplx) * c.sg.g.ndofs, s));
+      cycle(l1, VV, WW, true);
+    };
+    CK(cudaMemsetAsync(EC[q], 0, sizeof(cplx) * c.sg.g.ndofs, s));
+    std::vector<double> hist;
+    fg.run(A, M, BC[q], EC[q], ko, hist);
+  }
+  // element ranges of slab q's owned planes in its level-l window
+  std::vector<std::pair<int64_t, int64_t>> owned_ranges(int l, int q) const {
+    const SlabGeo& sg = L[l][q]->sg;
+    const bool last = q + 1 == P_();
+    std::vector<std::pair<int64_t, int64_t>> o;
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ps = slab_plane(sg.g, k);
+      const int b = (k == 2 && last) ? sg.Z1 + 1 : sg.Z1;
+      o.push_back({sg.g.off[k] + (sg.Z0 - sg.g.zoff) * ps, sg.g.off[k] + (b - sg.g.zoff) * ps});
+    }
+    return o;
   }
 
   // z = M r on the level-0 windows of the local slabs (ghosts of B refreshed
@@ -450,7 +507,9 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
                                                      const ehmg_mg_options& opt, int nslabs, int agg_n2,
                                                      NodeComm* comm) {
   if (g0.nd != 3) throw Err(EHMG_EINVAL, "slab: z-slab decomposition is 3D only");
-  if (opt.cycle == 3) throw Err(EHMG_EINVAL, "slab: K-cycles need a distributed inner Krylov (not supported)");
+  if (opt.cycle == 3 && (comm ? comm->n != nslabs : nslabs != 1))
+    throw Err(EHMG_EINVAL, "slab: K-cycles need one slab per process (the inner Krylov is distributed over ranks)");
+  if (opt.cycle == 3 && opt.precision != 0) throw Err(EHMG_EINVAL, "mixed precision: K-cycles are not supported");
   if (opt.sweep != 1) throw Err(EHMG_EINVAL, "slab: only red-black sweeps decompose");
   if (opt.precision != 0 && opt.precision != 1) throw Err(EHMG_EINVAL, "slab: precision must be 0 or 1");
   if (!stencil3d_supported(g0)) throw Err(EHMG_EINVAL, "slab: needs an even x extent (TMA stencil)");
@@ -487,6 +546,7 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
   sm->L.resize(La);
   sm->pend.assign(La, 0);
   sm->xpar.assign(La, 0);
+  sm->kin.resize(La);
   for (int l = 0; l < La; ++l) {
     for (int q = 0; q < nslabs; ++q) {
       auto sl = std::make_unique<SlabLevel>();

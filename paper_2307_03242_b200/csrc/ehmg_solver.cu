@@ -786,6 +786,21 @@ struct ehmg_mg_s {
   template <class V>
   void cycle_t(int l, const V* b, V* x, bool xzero);
   void cycle_at(int l, const cplx* b, cplx* x, bool xzero = false) { cycle_t<cplx>(l, b, x, xzero); }
+  // K-cycle coarse correction on this hierarchy's level 0 (the cycle_t
+  // K branch one level up): inner FGMRES with A_0 and M = cycle_at(0, ...).
+  // The z-slab mode calls it for its first agglomerated level.
+  void kcycle_top(const cplx* b, cplx* x) {
+    Level& lv = *L[0];
+    ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol, 0.99, 2};
+    lv.inner.init(lv.g.ndofs, opt.k_inner_iterations, s);
+    CK(cudaMemsetAsync(x, 0, sizeof(cplx) * lv.g.ndofs, s));
+    std::vector<double> hist;
+    Fgmres::Fn A = [&](const cplx* in, cplx* out) {
+      launch_residual(lv.g, lv.P, lv.media.ref(), in, nullptr, out, s);
+    };
+    Fgmres::Fn M = [&](const cplx* in, cplx* out) { cycle_at(0, in, out, true); };
+    lv.inner.run(A, M, b, x, ko, hist);
+  }
   void precondition_direct(const cplx* r, cplx* z) {
     const int64_t n = L[0]->g.ndofs;
     if (prec == 0) {
