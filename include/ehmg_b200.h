@@ -153,6 +153,8 @@ int ehmg_multigrid_measure_convergence(ehmg_mg mg, uint64_t seed, const ehmg_mea
  *      levels with z extent <= agg_n2 are agglomerated (replicated). In one
  *      process all slabs live on the current device and exchange by device
  *      copies; results equal ehmg_multigrid_precondition (same options).
+ *      V/W cycles in complex128 or (opt->precision = 1) complex64; K-cycles
+ *      need one slab per process (ehmg_dist_*) or nslabs = 1.
  * plan: la = number of distributed levels, z0[0..nslabs] = level-0 slab
  *       boundaries (pure host function, no device needed). */
 typedef struct ehmg_slab_mg_s* ehmg_slab_mg;
@@ -173,7 +175,9 @@ int64_t ehmg_slab_multigrid_exchanged_bytes(ehmg_slab_mg mg);
  *      share inbox buffers through CUDA IPC (peer copies over NVLink) and
  *      sum FGMRES reductions in rank order. Media and fields are passed as
  *      full host arrays; each rank reads its window and writes back only the
- *      planes it owns. Results equal the single-process solver's. */
+ *      planes it owns. Results equal the single-process solver's. V/W/K
+ *      cycles, complex128 or complex64 hierarchy (opt->precision); the exact
+ *      coarsest solve is row-partitioned over the ranks. */
 typedef struct ehmg_dist_s* ehmg_dist;
 int ehmg_dist_create(const char* job, int rank, int nranks, int device, int ndim, const int* dims,
                      double h, const double* lambda, const double* mu, const double* rho,
