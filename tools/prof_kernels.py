@@ -1,6 +1,6 @@
 """Short driver for ncu captures of the hot kernels at the bench size.
 
-    python tools/prof_kernels.py [--n 256] [--what apply|cycle]
+    python tools/prof_kernels.py [--n 256] [--what apply|cycle|solve]
 """
 import argparse
 import math
@@ -38,8 +38,14 @@ def main():
         opt = E.MgOptions(n_levels=5 if n >= 64 else 3, cycle="v", nu1=2, nu2=2, damping=0.25,
                           vanka_mode="full", sweep="red_black")
         mg = E.Multigrid(g, med, E.OperatorParams(2 / 3, omega, 0.5), opt)
-        for _ in range(a.reps):
-            mg.precondition(r, y)
+        if a.what == "solve":  # a few FGMRES iterations (MGS passes, scale/copy, restart update)
+            D0 = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.0))
+            b = E.make_point_source(g, 0, (n // 2, n // 2, n // 2))
+            x = b * 0
+            E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=4 * a.reps))
+        else:
+            for _ in range(a.reps):
+                mg.precondition(r, y)
     torch.cuda.synchronize()
     print("ok", float(y.abs().max()))
 
