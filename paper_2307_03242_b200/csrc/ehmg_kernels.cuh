@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const V* __re
 // Prolongation(+add) for one component; each thread produces kProlongNX
 // fine values 32 apart along x, so the y/z taps and coarse row addresses
 // (most of the per-output instructions) are formed once per thread.
-constexpr int kProlongNX = 4;
+constexpr int kProlongNX = 8;
 template <int C, class V = cplx>
 __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const V* __restrict__ xc,
                                                   V* __restrict__ xf, int accumulate) {
