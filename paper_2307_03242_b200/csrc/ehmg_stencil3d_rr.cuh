@@ -308,12 +308,6 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   const R mu01 = (mc_lb + mc_l + mc_b + mc00) * Q.mu01s;
   const R mu02p = (mc_l + mp_l + mc00 + mp00) * (Q.ix * izp);  // edges (z, z+1)
   const R mu12p = (mc_b + mp_b + mc00 + mp00) * (Q.iy * izp);
-  auto spread = [](C mm, C m0_, C mp, C zm, C z0, C zp, C pm, C p0, C pp) {
-    const C a = mm + mp + R(2) * m0_;
-    const C c = pm + pp + R(2) * p0;
-    const C m_ = zm + zp + R(2) * z0;
-    return a + c + R(2) * m_;
-  };
   // mass: beta*q + the x neighbours (shuffles) + the z-1 neighbour (the older
   // carried product, whose register the new product then takes); the y
   // neighbours and z+1 follow after the barrier
@@ -326,22 +320,24 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   };
   // ---- component 0: F00 (cell, +x pair), F01 (edge01, -y pair), F02 (edge02, +z pair)
   {
-    const C vmm = V0[ui - R3_UX - 1], vm0 = V0[ui - R3_UX], vmp = V0[ui - R3_UX + 1];
-    const C v0m = V0[ui - 1], v00 = V0[ui], v0p = V0[ui + 1];
-    const C vpm = V0[ui + R3_UX - 1], vp0 = V0[ui + R3_UX], vpp = V0[ui + R3_UX + 1];
+    // own column of the new plane (rows y-1, y, y+1); the x neighbours of
+    // its column sum Sy and of the y difference D come by shuffle
+    const C vm0 = V0[ui - R3_UX], v00 = V0[ui], vp0 = V0[ui + R3_UX];
     const C u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - R3_UX];
-    const C rn0 = (vmp - vm0) + (vpp - vp0) + R(2) * (v0p - v00);
+    const C sy = vm0 + vp0 + R(2) * v00, syl = r3_up(sy), syr = r3_dn(sy);
+    const C dy = v00 - vm0;
+    const C rn0 = syr - sy;  // sum over rows of (x+1 - x) differences
     const C sz0 = (nxt.r00 + R(2) * cur.r00) + rn0;
     nxt.r00 = rn0;
     const C d00 = (beta * (u0p - u00) + w * sz0) * (IW(Q.fl00 | zA) * ih);
     o3v = d00;
     const C f0 = mc00 * d00;
     o0v = (r3_up(f0) - f0) * ih;
-    const C rn1 = (v0m - vmm) + (v0p - vmp) + R(2) * (v00 - vm0);
+    const C rn1 = r3_up(dy) + r3_dn(dy) + R(2) * dy;
     const C sz1 = (nxt.r01 + R(2) * cur.r01) + rn1;
     nxt.r01 = rn1;
     FY[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (IW(zB | Q.fl01) * ih));
-    const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
+    const C tn = syl + syr + R(2) * sy;
     nxt.f02 = mu02p * ((beta * (v00 - u00) + w * (tn - cur.t0)) * (IW(Q.i02) * ih));
     nxt.t0 = tn;
     m0 = mass_head(cur.q0, nxt.q0);
@@ -350,22 +346,22 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   }
   // ---- component 1: F11 (cell, +y pair), F10 (edge01, -x pair), F12 (edge12, +z pair)
   {
-    const C vmm = V1[ui - R3_UX - 1], vm0 = V1[ui - R3_UX], vmp = V1[ui - R3_UX + 1];
-    const C v0m = V1[ui - 1], v00 = V1[ui], v0p = V1[ui + 1];
-    const C vpm = V1[ui + R3_UX - 1], vp0 = V1[ui + R3_UX], vpp = V1[ui + R3_UX + 1];
+    const C vm0 = V1[ui - R3_UX], v00 = V1[ui], vp0 = V1[ui + R3_UX];
     const C u00 = U1[ui], up0 = U1[ui + R3_UX], u0m = U1[ui - 1];
-    const C rn0 = (vpm - v0m) + (vpp - v0p) + R(2) * (vp0 - v00);
+    const C sy = vm0 + vp0 + R(2) * v00, syl = r3_up(sy), syr = r3_dn(sy);
+    const C dy = vp0 - v00;
+    const C rn0 = r3_up(dy) + r3_dn(dy) + R(2) * dy;
     const C sz0 = (nxt.r11 + R(2) * cur.r11) + rn0;
     nxt.r11 = rn0;
     const C d11 = (beta * (up0 - u00) + w * sz0) * (IW(zB | Q.fl11) * ih);
     o3v += d11;
     FY[0][t] = mc00 * d11;
-    const C rn1 = (vm0 - vmm) + (vp0 - vpm) + R(2) * (v00 - v0m);
+    const C rn1 = sy - syl;
     const C sz1 = (nxt.r10 + R(2) * cur.r10) + rn1;
     nxt.r10 = rn1;
     const C f3 = mu01 * ((beta * (u00 - u0m) + w * sz1) * (IW(zB | Q.fl10) * ih));
     o1v = (f3 - r3_dn(f3)) * ih;
-    const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
+    const C tn = syl + syr + R(2) * sy;
     nxt.f12 = mu12p * ((beta * (v00 - u00) + w * (tn - cur.t1)) * (IW(Q.i12) * ih));
     nxt.t1 = tn;
     m1 = mass_head(cur.q1, nxt.q1);
@@ -374,20 +370,20 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   }
   // ---- component 2: F20 (edge02, -x pair), F21 (edge12, -y pair), F22 (cell, +z pair)
   {
-    const C vmm = V2[ui - R3_UX - 1], vm0 = V2[ui - R3_UX], vmp = V2[ui - R3_UX + 1];
-    const C v0m = V2[ui - 1], v00 = V2[ui], v0p = V2[ui + 1];
-    const C vpm = V2[ui + R3_UX - 1], vp0 = V2[ui + R3_UX], vpp = V2[ui + R3_UX + 1];
+    const C vm0 = V2[ui - R3_UX], v00 = V2[ui], vp0 = V2[ui + R3_UX];
     const C u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - R3_UX];
-    const C rn0 = (vm0 - vmm) + (vp0 - vpm) + R(2) * (v00 - v0m);
+    const C sy = vm0 + vp0 + R(2) * v00, syl = r3_up(sy), syr = r3_dn(sy);
+    const C dy = v00 - vm0;
+    const C rn0 = sy - syl;
     const C sz0 = (nxt.r20 + R(2) * cur.r20) + rn0;
     nxt.r20 = rn0;
     const C f4 = cur.mu02 * ((beta * (u00 - u0m) + w * sz0) * (IW(Q.fl20 | zC) * ih));
     o2v = (f4 - r3_dn(f4)) * ih;
-    const C rn1 = (v0m - vmm) + (v0p - vmp) + R(2) * (v00 - vm0);
+    const C rn1 = r3_up(dy) + r3_dn(dy) + R(2) * dy;
     const C sz1 = (nxt.r21 + R(2) * cur.r21) + rn1;
     nxt.r21 = rn1;
     FY[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (IW(Q.fl21 | zC) * ih));
-    const C tn = spread(vmm, vm0, vmp, v0m, v00, v0p, vpm, vp0, vpp);
+    const C tn = syl + syr + R(2) * sy;
     const C d22 = (beta * (v00 - u00) + w * (tn - cur.t2)) * (IW(Q.i22) * ih);  // cell (q, z)
     o3v += d22;
     nxt.f22 = mc00 * d22;  // zero-filled mu masks cells outside the box
