@@ -178,6 +178,7 @@ struct R3Carry {
   V f02, f12, f22;                 // in-plane family fluxes of the previous step
   V q0, q1, q2;                    // mass products: cur = plane z, nxt = plane z-1 -> z+1
   V p;                             // p at plane z-1 (cur) -> plane z (nxt)
+  V u0, u1, u2;                    // own u at plane z (cur) -> z+1 (nxt)
   R mu02, mu12;                    // edge averages of planes (z-1, z) (cur) -> (z, z+1) (nxt)
 };
 
@@ -323,7 +324,8 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
     // own column of the new plane (rows y-1, y, y+1); the x neighbours of
     // its column sum Sy and of the y difference D come by shuffle
     const C vm0 = V0[ui - R3_UX], v00 = V0[ui], vp0 = V0[ui + R3_UX];
-    const C u00 = U0[ui], u0p = U0[ui + 1], um0 = U0[ui - R3_UX];
+    const C u00 = cur.u0, u0p = U0[ui + 1], um0 = U0[ui - R3_UX];
+    nxt.u0 = v00;
     const C sy = vm0 + vp0 + R(2) * v00, syl = r3_up(sy), syr = r3_dn(sy);
     const C dy = v00 - vm0;
     const C rn0 = syr - sy;  // sum over rows of (x+1 - x) differences
@@ -347,7 +349,8 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   // ---- component 1: F11 (cell, +y pair), F10 (edge01, -x pair), F12 (edge12, +z pair)
   {
     const C vm0 = V1[ui - R3_UX], v00 = V1[ui], vp0 = V1[ui + R3_UX];
-    const C u00 = U1[ui], up0 = U1[ui + R3_UX], u0m = U1[ui - 1];
+    const C u00 = cur.u1, up0 = U1[ui + R3_UX], u0m = U1[ui - 1];
+    nxt.u1 = v00;
     const C sy = vm0 + vp0 + R(2) * v00, syl = r3_up(sy), syr = r3_dn(sy);
     const C dy = vp0 - v00;
     const C rn0 = r3_up(dy) + r3_dn(dy) + R(2) * dy;
@@ -371,7 +374,8 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   // ---- component 2: F20 (edge02, -x pair), F21 (edge12, -y pair), F22 (cell, +z pair)
   {
     const C vm0 = V2[ui - R3_UX], v00 = V2[ui], vp0 = V2[ui + R3_UX];
-    const C u00 = U2[ui], u0m = U2[ui - 1], um0 = U2[ui - R3_UX];
+    const C u00 = cur.u2, u0m = U2[ui - 1], um0 = U2[ui - R3_UX];
+    nxt.u2 = v00;
     const C sy = vm0 + vp0 + R(2) * v00, syl = r3_up(sy), syr = r3_dn(sy);
     const C dy = v00 - vm0;
     const C rn0 = sy - syl;
@@ -499,6 +503,7 @@ __global__ void __launch_bounds__(R3_THREADS, 1)
       const V zc = VT<V>::mk(0, 0);
       A.r00 = A.r11 = A.r01 = A.r10 = A.r20 = A.r21 = zc;
       A.t0 = A.t1 = A.t2 = A.f02 = A.f12 = A.f22 = A.q0 = A.q1 = A.q2 = A.p = zc;
+      A.u0 = A.u1 = A.u2 = zc;
       A.mu02 = A.mu12 = R(0);
       B = A;
     }
