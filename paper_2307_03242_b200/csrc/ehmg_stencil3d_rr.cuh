@@ -295,7 +295,7 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
   C(*FY)[R3_THREADS] = S.fy[z & 1];
 
   // values the row evaluation after the barrier needs (rows 1..TY only)
-  C m0, m1, m2, o0v, o1v, o2v, o3v, pt0, pt1, pt2;
+  C m0, m1, m2, o0v, o1v, o2v, o3v, pt0, pt1, pt2, f1, f2, f5;
   {
   // ---- every flux family at this position (halo rows and columns too:
   // skipping the unused families there costs more in warp imbalance at the
@@ -338,7 +338,8 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
     const C rn1 = r3_up(dy) + r3_dn(dy) + R(2) * dy;
     const C sz1 = (nxt.r01 + R(2) * cur.r01) + rn1;
     nxt.r01 = rn1;
-    FY[1][t] = mu01 * ((beta * (u00 - um0) + w * sz1) * (IW(zB | Q.fl01) * ih));
+    f2 = mu01 * ((beta * (u00 - um0) + w * sz1) * (IW(zB | Q.fl01) * ih));
+    FY[1][t] = f2;
     const C tn = syl + syr + R(2) * sy;
     nxt.f02 = mu02p * ((beta * (v00 - u00) + w * (tn - cur.t0)) * (IW(Q.i02) * ih));
     nxt.t0 = tn;
@@ -358,7 +359,8 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
     nxt.r11 = rn0;
     const C d11 = (beta * (up0 - u00) + w * sz0) * (IW(zB | Q.fl11) * ih);
     o3v += d11;
-    FY[0][t] = mc00 * d11;
+    f1 = mc00 * d11;
+    FY[0][t] = f1;
     const C rn1 = sy - syl;
     const C sz1 = (nxt.r10 + R(2) * cur.r10) + rn1;
     nxt.r10 = rn1;
@@ -386,7 +388,8 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
     const C rn1 = r3_up(dy) + r3_dn(dy) + R(2) * dy;
     const C sz1 = (nxt.r21 + R(2) * cur.r21) + rn1;
     nxt.r21 = rn1;
-    FY[2][t] = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (IW(Q.fl21 | zC) * ih));
+    f5 = cur.mu12 * ((beta * (u00 - um0) + w * sz1) * (IW(Q.fl21 | zC) * ih));
+    FY[2][t] = f5;
     const C tn = syl + syr + R(2) * sy;
     const C d22 = (beta * (v00 - u00) + w * (tn - cur.t2)) * (IW(Q.i22) * ih);  // cell (q, z)
     o3v += d22;
@@ -419,21 +422,21 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
     const int64_t o3 = o2 + (g.off[3] - g.off[2]);
     const C(*SQ)[R3_THREADS] = S.q[s0];
     const int czz = lz + hz0;
-    o0v += (FY[1][t] - FY[1][t + R3_FX]) * ih;
+    o0v += (f2 - FY[1][t + R3_FX]) * ih;
     o0v += (cur.f02 - nxt.f02) * ih;
     m0 += wn * SQ[0][t - R3_FX];
     m0 += wn * SQ[0][t + R3_FX];
     m0 += wn * nxt.q0;
     o0v -= m0 * IM(Q.mc0 + czz);
     o0v += pt0;
-    o1v += (FY[0][t - R3_FX] - FY[0][t]) * ih;
+    o1v += (FY[0][t - R3_FX] - f1) * ih;
     o1v += (cur.f12 - nxt.f12) * ih;
     m1 += wn * SQ[1][t - R3_FX];
     m1 += wn * SQ[1][t + R3_FX];
     m1 += wn * nxt.q1;
     o1v -= m1 * IM(Q.mc1 + czz);
     o1v += (pt1 - S.p[s0][ui - R3_UX]) * ih;
-    o2v += (FY[2][t] - FY[2][t + R3_FX]) * ih;
+    o2v += (f5 - FY[2][t + R3_FX]) * ih;
     o2v += (cur.f22 - nxt.f22) * ih;
     m2 += wn * SQ[2][t - R3_FX];
     m2 += wn * SQ[2][t + R3_FX];
