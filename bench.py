@@ -36,7 +36,7 @@ sys.path.insert(0, ROOT)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
 # kernel from one `ncu --set full` capture of the same residual at 256^3
 # (distinct b and x; profiles/round1/ncu_stencil3d_rr_residual.txt).
-NCU_TRAFFIC = {"residual@L0": 2871403000 + 1056070000,
+NCU_TRAFFIC = {"residual@L0": 2859076000 + 1056127000,
                "source": "profiles/round1/ncu_stencil3d_rr_residual.txt (ncu --set full, 256^3 residual)"}
 N_CELLS = 256
 LEVELS = 5  # at 256^3: coarsest level 16^3 cells (17^3 nodes), BASELINE configs[2]
@@ -435,9 +435,9 @@ def run_b200(args, ws, rank, local):
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": NCU_TRAFFIC.get(f"{kname}@L{klev}") if n == N_CELLS else None,
                      "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
-                     "limiter": ("shared-memory/shuffle (LSU) pipe: 477 B of LSU traffic per DOF vs 56 B of "
-                                 "HBM, LSU bound = 67% of the HBM roofline; ncu: LSU 74% busy, IPC 1.64, FP64 "
-                                 "pipe 44%, DRAM 38% at 8 warps x 254 registers; see DESIGN.md"),
+                     "limiter": ("shared-memory/shuffle (LSU) pipe: 418 B of LSU traffic per DOF vs 56 B of "
+                                 "HBM, LSU bound = 77% of the HBM roofline; ncu: LSU 72% busy, IPC 1.73, FP64 "
+                                 "pipe 41%, DRAM 42% at 8 warps x 255 registers; see DESIGN.md"),
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "clocks": clocks,
     }
