@@ -696,11 +696,10 @@ __global__ void k_coarse_matrix(Geo g, OpPar P, const Cell* __restrict__ m, cplx
 template <class V = cplx>
 __global__ void __launch_bounds__(kThreads) k_gemv_rows(int64_t N, const V* __restrict__ A,
                                                         const V* __restrict__ b, V* __restrict__ x,
-                                                        int64_t nrows = -1) {
-  // rows [0, nrows) of a row-major nrows x N block (nrows < 0: N x N)
+                                                        int64_t R) {
+  // rows [0, R) of a row-major R x N matrix (the whole inverse: R = N)
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  const int64_t R = nrows < 0 ? N : nrows;
   for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; row < R; row += warps) {
     const V* a = A + row * N;
     double sr = 0, si = 0;

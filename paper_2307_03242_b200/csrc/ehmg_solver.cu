@@ -871,7 +871,7 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
   if (l + 1 == nl) {
     Prof pf("coarse_solve", s);
     if (c_r1 < 0) {
-      k_gemv_rows<V><<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x);
+      k_gemv_rows<V><<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x, nco);
       CK(cudaGetLastError());
     } else {
       const int64_t rows = c_r1 - c_r0;
