@@ -304,10 +304,11 @@ __global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict_
 // it owns. Cells of one colour share no DOFs, so the in-place writes commute.
 // T = cplx or cplxf: storage and arithmetic type (the single-precision
 // hierarchy updates in float, as the reference's VankaSmoother<float>).
-template <int ND, class T = cplx>
+template <int ND, class T = cplx, bool XZERO = false>
 __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
                                                            const T* __restrict__ r, int color, double w,
-                                                           T* __restrict__ x, int xzero) {
+                                                           T* __restrict__ x) {
+  constexpr bool xzero = XZERO;  // compile-time: the regular update keeps its load schedule
   typedef typename VT<T>::R R;
   const int nu = full ? 4 : 2, cs = ND * nu + 1;
   const T zero = VT<T>::mk(0, 0);
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k
       x[fi[k][1]] = xx[k][1] + wr * du1;
     }
     x[pi] = xp + wr * dp;
-    if (xzero) {
+    if constexpr (XZERO) {
       // the x-partner (other colour): its p, and its faces on the domain
       // boundary (interior faces belong to a cell of this colour)
       int pc[3] = {c[0] ^ 1, c[1], c[2]};

@@ -403,9 +403,11 @@ struct Smoother {
     const V* cq = cache(r);
     Prof pf("vanka_update", s);
     if (g.nd == 3)
-      k_vanka_update<3, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x, xzero);
+      (xzero ? k_vanka_update<3, V, true> : k_vanka_update<3, V, false>)<<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(
+          g, vk, full, cq, r, lc, w, x);
     else
-      k_vanka_update<2, V><<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(g, vk, full, cq, r, lc, w, x, xzero);
+      (xzero ? k_vanka_update<2, V, true> : k_vanka_update<2, V, false>)<<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(
+          g, vk, full, cq, r, lc, w, x);
     CK(cudaGetLastError());
   }
 };
