@@ -1,14 +1,14 @@
-// ehmg_stencil2d.cuh -- tiled 2D operator / residual kernel.
+// ehmg_stencil2d.cuh -- 2D operator / residual kernel.
 //
 // y = H x or r = b - H x for the 2D staggered mixed operator
-// (operator.hpp:267-421 with Dim = 2), all three rows (u0, u1, p) of a 32x8
-// block of (i, j) positions per CTA. The u0 / u1 / p fields and the packed
-// cell media of the block plus a 2-wide halo are staged in shared memory
-// with coalesced loads (zero outside the arrays, the reference's ghosts);
-// every row is then evaluated from shared memory term by term in the
-// reference's accumulation order (the generic rows of ehmg_core.cuh read
-// global memory per term, which left the 2D configs latency-bound).
-// V = cplx (complex128) or cplxf (complex64 storage; arithmetic in double).
+// (operator.hpp:267-421 with Dim = 2), all three rows (u0, u1, p) per
+// position. u0 / u1 / p and the packed cell media of a block plus halo are
+// staged in shared memory with coalesced loads (zero outside the arrays, the
+// reference's ghosts); fluxes and face mass products are evaluated once per
+// position and shared through shared memory (the generic rows of
+// ehmg_core.cuh read global memory per term, which left the 2D configs
+// latency-bound). V = cplx (complex128) or cplxf (complex64 storage;
+// arithmetic in double).
 #pragma once
 
 #include <mutex>
@@ -17,8 +17,6 @@
 
 namespace ehmg {
 
-constexpr int S2_TX = 32, S2_TY = 8, S2_H = 2;
-constexpr int S2_WX = S2_TX + 2 * S2_H, S2_WY = S2_TY + 2 * S2_H, S2_WN = S2_WX * S2_WY;
 
 struct S2Params {
   double beta, omega2, alpha, w;  // w = (1 - beta) / 4
@@ -49,163 +47,7 @@ inline S2Params make_s2params(const OpPar& P) {
   return s;
 }
 
-template <class V>
-__global__ void __launch_bounds__(S2_TX * S2_TY) k_stencil2d(Geo g, S2Params P, const Cell* __restrict__ m,
-                                                             const V* __restrict__ x, const V* __restrict__ b,
-                                                             V* __restrict__ y) {
-  __shared__ cplx U0[S2_WN], U1[S2_WN], Pp[S2_WN];
-  __shared__ Cell M[S2_WN];
-  const int n0 = g.n[0], n1 = g.n[1];
-  const int i0 = blockIdx.x * S2_TX, j0 = blockIdx.y * S2_TY;
-  const int t = threadIdx.x + S2_TX * threadIdx.y;
-  const V* X0 = x + g.off[0];
-  const V* X1 = x + g.off[1];
-  const V* XP = x + g.off[2];
-  for (int e = t; e < S2_WN; e += S2_TX * S2_TY) {
-    const int wy = e / S2_WX, wx = e - wy * S2_WX;
-    const int xx = i0 - S2_H + wx, yy = j0 - S2_H + wy;
-    const bool cy = yy >= 0 && yy < n1, cx = xx >= 0 && xx < n0;
-    U0[e] = (xx >= 0 && xx <= n0 && cy) ? wide(X0[xx + (int64_t)(n0 + 1) * yy]) : mk(0, 0);
-    U1[e] = (cx && yy >= 0 && yy <= n1) ? wide(X1[xx + (int64_t)n0 * yy]) : mk(0, 0);
-    const bool cok = cx && cy;
-    Pp[e] = cok ? wide(XP[xx + (int64_t)n0 * yy]) : mk(0, 0);
-    M[e] = cok ? m[xx + (int64_t)n0 * yy] : make_double4(0, 0, 0, 0);
-  }
-  __syncthreads();
-
-  const int xo = i0 + threadIdx.x, yo = j0 + threadIdx.y;
-  const int W = S2_WX;
-  const int c0 = (threadIdx.x + S2_H) + W * (threadIdx.y + S2_H);  // window index of (xo, yo)
-  const double beta = P.beta, w = P.w, ih = g.inv_h, wn = P.wn;
-  auto cell_ok = [&](int cx, int cy) { return cx >= 0 && cx < n0 && cy >= 0 && cy < n1; };
-  // operator.hpp:267 dspread_cell, cell (cx, cy) = window index ci
-  auto dsc0 = [&](int cx, int cy, int ci) {  // k = 0: x-difference of u0, spread along y
-    cplx v = beta * (U0[ci + 1] - U0[ci]);
-    if (beta != 1.0) {
-      if (cy - 1 >= 0) v += w * (U0[ci + 1 - W] - U0[ci - W]);
-      v += (2.0 * w) * (U0[ci + 1] - U0[ci]);
-      if (cy + 1 < n1) v += w * (U0[ci + 1 + W] - U0[ci + W]);
-      v = v * P.inv_wsum[(cy - 1 >= 0) | ((cy + 1 < n1) << 1)];
-    }
-    return v * ih;
-  };
-  auto dsc1 = [&](int cx, int cy, int ci) {  // k = 1: y-difference of u1, spread along x
-    cplx v = beta * (U1[ci + W] - U1[ci]);
-    if (beta != 1.0) {
-      if (cx - 1 >= 0) v += w * (U1[ci - 1 + W] - U1[ci - 1]);
-      v += (2.0 * w) * (U1[ci + W] - U1[ci]);
-      if (cx + 1 < n0) v += w * (U1[ci + 1 + W] - U1[ci + 1]);
-      v = v * P.inv_wsum[(cx - 1 >= 0) | ((cx + 1 < n0) << 1)];
-    }
-    return v * ih;
-  };
-  // operator.hpp:306 dspread_edge at edge (ex, ey) = window index ei
-  auto dse01 = [&](int ex, int ey, int ei) {  // k = 0, j = 1: y-difference of u0, spread along x
-    cplx v = beta * (U0[ei] - U0[ei - W]);
-    if (beta != 1.0) {
-      if (ex - 1 >= 0) v += w * (U0[ei - 1] - U0[ei - 1 - W]);
-      v += (2.0 * w) * (U0[ei] - U0[ei - W]);
-      if (ex + 1 < n0 + 1) v += w * (U0[ei + 1] - U0[ei + 1 - W]);
-      v = v * P.inv_wsum[(ex - 1 >= 0) | ((ex + 1 < n0 + 1) << 1)];
-    }
-    return v * ih;
-  };
-  auto dse10 = [&](int ex, int ey, int ei) {  // k = 1, j = 0: x-difference of u1, spread along y
-    cplx v = beta * (U1[ei] - U1[ei - 1]);
-    if (beta != 1.0) {
-      if (ey - 1 >= 0) v += w * (U1[ei - W] - U1[ei - 1 - W]);
-      v += (2.0 * w) * (U1[ei] - U1[ei - 1]);
-      if (ey + 1 < n1 + 1) v += w * (U1[ei + W] - U1[ei - 1 + W]);
-      v = v * P.inv_wsum[(ey - 1 >= 0) | ((ey + 1 < n1 + 1) << 1)];
-    }
-    return v * ih;
-  };
-  // operator.hpp:108 mu on the (0,1) edge: mean of the in-range cells, summed
-  // first-axis-outer as the reference does (a = 0 for u0 rows, a = 1 for u1)
-  auto mu_e = [&](int ex, int ey, int ei, bool yfirst) {
-    double s = 0;
-    int cnt = 0;
-    if (cell_ok(ex - 1, ey - 1)) s += M[ei - 1 - W].x, ++cnt;
-    if (!yfirst) {
-      if (cell_ok(ex - 1, ey)) s += M[ei - 1].x, ++cnt;
-      if (cell_ok(ex, ey - 1)) s += M[ei - W].x, ++cnt;
-    } else {
-      if (cell_ok(ex, ey - 1)) s += M[ei - W].x, ++cnt;
-      if (cell_ok(ex - 1, ey)) s += M[ei - 1].x, ++cnt;
-    }
-    if (cell_ok(ex, ey)) s += M[ei].x, ++cnt;
-    return s / cnt;
-  };
-  // operator.hpp:132 face mass diagonal of a k-face at window index fi
-  auto mdiag = [&](int k, int fx, int fy, int fi) {
-    const int st = k == 0 ? 1 : W;
-    const int bx = fx - (k == 0), by = fy - (k == 1);
-    double sr = 0, sg = 0;
-    int cnt = 0;
-    if (cell_ok(bx, by)) sr += M[fi - st].y, sg += M[fi - st].z, ++cnt;
-    if (cell_ok(fx, fy)) sr += M[fi].y, sg += M[fi].z, ++cnt;
-    const double rho_f = sr / cnt, gam_f = sg / cnt + P.alpha;
-    return mk(P.omega2 * rho_f, -P.omega2 * gam_f * rho_f);
-  };
-  // operator.hpp:359 mass_eval on a k-face
-  auto mass = [&](int k, int fx, int fy, int fi, const cplx* Uk) {
-    const int d0 = n0 + (k == 0), d1 = n1 + (k == 1);
-    cplx v = beta * (mdiag(k, fx, fy, fi) * Uk[fi]);
-    if (beta == 1.0) return v;
-    int cnt = 0;
-    if (fx - 1 >= 0) v += wn * (mdiag(k, fx - 1, fy, fi - 1) * Uk[fi - 1]), ++cnt;
-    if (fx + 1 < d0) v += wn * (mdiag(k, fx + 1, fy, fi + 1) * Uk[fi + 1]), ++cnt;
-    if (fy - 1 >= 0) v += wn * (mdiag(k, fx, fy - 1, fi - W) * Uk[fi - W]), ++cnt;
-    if (fy + 1 < d1) v += wn * (mdiag(k, fx, fy + 1, fi + W) * Uk[fi + W]), ++cnt;
-    return v * P.inv_msum[cnt];
-  };
-
-  if (xo <= n0 && yo < n1) {  // u0 row (operator.hpp:389 / :409)
-    cplx out = mk(0, 0);
-    {
-      const cplx wm = cell_ok(xo - 1, yo) ? M[c0 - 1].x * dsc0(xo - 1, yo, c0 - 1) : mk(0, 0);
-      const cplx wp = cell_ok(xo, yo) ? M[c0].x * dsc0(xo, yo, c0) : mk(0, 0);
-      out += (wm - wp) * ih;
-    }
-    {
-      const cplx wm = mu_e(xo, yo, c0, false) * dse01(xo, yo, c0);
-      const cplx wp = mu_e(xo, yo + 1, c0 + W, false) * dse01(xo, yo + 1, c0 + W);
-      out += (wm - wp) * ih;
-    }
-    out -= mass(0, xo, yo, c0, U0);
-    out += (Pp[c0] - Pp[c0 - 1]) * ih;
-    const int64_t o = g.off[0] + xo + (int64_t)(n0 + 1) * yo;
-    y[o] = narrow<V>(b ? wide(b[o]) - out : out);
-  }
-  if (xo < n0 && yo <= n1) {  // u1 row
-    cplx out = mk(0, 0);
-    {
-      const cplx wm = mu_e(xo, yo, c0, true) * dse10(xo, yo, c0);
-      const cplx wp = mu_e(xo + 1, yo, c0 + 1, true) * dse10(xo + 1, yo, c0 + 1);
-      out += (wm - wp) * ih;
-    }
-    {
-      const cplx wm = cell_ok(xo, yo - 1) ? M[c0 - W].x * dsc1(xo, yo - 1, c0 - W) : mk(0, 0);
-      const cplx wp = cell_ok(xo, yo) ? M[c0].x * dsc1(xo, yo, c0) : mk(0, 0);
-      out += (wm - wp) * ih;
-    }
-    out -= mass(1, xo, yo, c0, U1);
-    out += (Pp[c0] - Pp[c0 - W]) * ih;
-    const int64_t o = g.off[1] + xo + (int64_t)n0 * yo;
-    y[o] = narrow<V>(b ? wide(b[o]) - out : out);
-  }
-  if (xo < n0 && yo < n1) {  // p row (operator.hpp:416)
-    cplx out = mk(0, 0);
-    out += dsc0(xo, yo, c0);
-    out += dsc1(xo, yo, c0);
-    out += M[c0].w * Pp[c0];
-    const int64_t o = g.off[2] + xo + (int64_t)n0 * yo;
-    y[o] = narrow<V>(b ? wide(b[o]) - out : out);
-  }
-}
-
-// Flux-sharing variant (the production 2D kernel): the 32x16 thread grid is
-// the flux window of a 30x14 output block. Each thread evaluates the fluxes
+// The 32x16 thread grid is the flux window of a 30x14 output block. Each thread evaluates the fluxes
 // of its own cell and edge, and the mass products of its own faces, once;
 // neighbouring rows read them from shared memory instead of re-evaluating
 // them (the term-by-term kernel above evaluated every flux twice and every
