@@ -43,6 +43,8 @@
 #pragma once
 
 #include "ehmg_stencil3d.cuh"
+#include <cstdio>
+#include <stdexcept>
 
 namespace ehmg {
 
@@ -105,7 +107,7 @@ __device__ __forceinline__ void r3_issue(R3SmemT<V>& S, const R3Maps& RM, int i0
   constexpr int ku0 = F ? 1 : 0;
   s3_expect(bar, (unsigned)(nu * (3 - ku0) * SM::CBYTES + nm * 4 * SM::MBYTES + np * SM::CBYTES +
                             (hasb && !F ? 4 * SM::BBYTES : 0)));
-  if (!F && hasb)
+  if (!F && hasb)  // complex64 b arrives by cp.async
     for (int k = 0; k < 4; ++k) s3_tma(S.bp[s3_mod3(zb_)][k], &RM.b[k], 2 * (i0 - 1), j0 - 1, zb_, bar);
   const int cx = 2 * (i0 - 2), cy = j0 - 2;
   const int mx = F ? ((i0 - 2) & ~3) : i0 - 2;  // 16-byte aligned media start (i0 is even)
@@ -134,33 +136,23 @@ template <int N>
 __device__ __forceinline__ void r3_cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-// u0 window of plane z (origin (i0-2, j0-2), 34 x 10) into dst
-__device__ __forceinline__ void r3_u0_plane(cplxf* dst, const cplxf* u0, const Geo& g, int i0, int j0, int z, int t) {
-  const int d0 = g.n[0] + 1, d1 = g.n[1], d2 = g.n[2];
-  const bool zin = z >= 0 && z < d2;
-  for (int e = t; e < R3_UN; e += R3_THREADS) {
-    const int r = e / R3_UX, c = e - r * R3_UX, x = i0 - 2 + c, yy = j0 - 2 + r;
-    const bool ok = zin && x >= 0 && x < d0 && yy >= 0 && yy < d1;
-    r3_cp8(&dst[e], ok ? u0 + ((int64_t)z * d1 + yy) * d0 + x : u0, ok);
-  }
-}
-// b rows of the thread grid (origin (i0-1, j0-1)) of plane z, all four components
-__device__ __forceinline__ void r3_b_plane(cplxf (*dst)[R3_THREADS], const cplxf* b, const Geo& g, int i0, int j0,
-                                           int z, int t) {
-  const int x = i0 - 1 + (t % R3_FX), yy = j0 - 1 + t / R3_FX;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int d0 = g.n[0] + (k == 0), d1 = g.n[1] + (k == 1), d2 = g.n[2] + (k == 2);
-    const cplxf* base = b + g.off[k];
-    const bool ok = z >= 0 && z < d2 && x >= 0 && x < d0 && yy >= 0 && yy < d1;
-    r3_cp8(&dst[k][t], ok ? base + ((int64_t)z * d1 + yy) * d0 + x : base, ok);
-  }
+// complex64 u0 window of plane z (origin (i0-2, j0-2), 34 x 10): thread t
+// copies elements t and t + 256 whose in-plane offsets and bounds were
+// formed once per item (zero outside the array).
+__device__ __forceinline__ void r3_u0_plane(cplxf* dst, const cplxf* u0, int64_t plane, int n2, int z, int t,
+                                            bool ok0, int64_t off0, bool ok1, int64_t off1) {
+  const bool zin = z >= 0 && z < n2;
+  const cplxf* base = u0 + (int64_t)z * plane;
+  r3_cp8(&dst[t], (zin && ok0) ? base + off0 : u0, zin && ok0);
+  if (t + R3_THREADS < R3_UN) r3_cp8(&dst[t + R3_THREADS], (zin && ok1) ? base + off1 : u0, zin && ok1);
 }
 
-// Per-item constants of one thread's position.
 template <class R>
 struct R3Pos {
   int ui, um, t, fy, i0, j0, zb, xg, yg;
+  // complex64 cp.async: u0 window elements t, t+256 and this position's b0 row
+  int64_t u0off0, u0off1, b0off;
+  bool u0ok0, u0ok1, b0ok;
   R ix, iy, mu01s;
   int fl00, fl11, fl01, fl10, fl20, fl21, i22, i02, i12, mc0, mc1, mc2;
   bool interior, v0, v1, v2, q0ok, q1ok, q2ok;
@@ -225,6 +217,17 @@ __device__ __forceinline__ R3Pos<typename VT<V>::R> r3_pos(const Geo& g, int t, 
   Q.q0ok = xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
   Q.q1ok = xg >= 0 && xg < n0 && yg >= 0 && yg <= n1;
   Q.q2ok = xg >= 0 && xg < n0 && yg >= 0 && yg < n1;
+  if constexpr (F) {
+    auto elem = [&](int e, bool& ok, int64_t& off) {
+      const int r = e / R3_UX, c = e - r * R3_UX, xx = i0 - 2 + c, yy = j0 - 2 + r;
+      ok = e < R3_UN && xx >= 0 && xx <= n0 && yy >= 0 && yy < n1;
+      off = (int64_t)yy * (n0 + 1) + xx;
+    };
+    elem(t, Q.u0ok0, Q.u0off0);
+    elem(t + R3_THREADS, Q.u0ok1, Q.u0off1);
+    Q.b0ok = xg >= 0 && xg <= n0 && yg >= 0 && yg < n1;
+    Q.b0off = (int64_t)yg * (n0 + 1) + xg;
+  }
   return Q;
 }
 
@@ -258,10 +261,23 @@ __device__ __forceinline__ void r3_step(R3SmemT<V>& S, const R3Maps& maps, const
     r3_issue<V>(S, maps, Q.i0, Q.j0, z + 2, 1, z + 2, 1, z + 1, 1, b != nullptr, z + 1, &S.bar[seq & 1]);
   }
   if constexpr (F) {
-    // u0 of plane z+3 and b of plane z+2 by cp.async (one group per plane,
+    // u0 of plane z+3 and b0 of plane z+2 by cp.async (one group per plane,
     // completed at the next plane's barrier)
-    r3_u0_plane(S.u0x[(z + 3) & 3], x + g.off[0], g, Q.i0, Q.j0, z + 3, t);
-    if (b) r3_b_plane(S.bp[(z + 2) & 3], b, g, Q.i0, Q.j0, z + 2, t);
+    const int64_t pl0 = (int64_t)(g.n[0] + 1) * g.n[1];
+    r3_u0_plane(S.u0x[(z + 3) & 3], x + g.off[0], pl0, g.n[2], z + 3, t, Q.u0ok0, Q.u0off0, Q.u0ok1, Q.u0off1);
+    if (b) {
+      const int zb2 = z + 2, n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+      const bool zin = zb2 >= 0 && zb2 < n2;
+      const int64_t boff = (int64_t)Q.yg * n0 + Q.xg, pl = (int64_t)n0 * n1;
+      const bool okx = Q.xg >= 0 && Q.xg < n0 && Q.yg >= 0;
+      const bool ok0 = Q.b0ok && zin, ok1 = okx && Q.yg <= n1 && zin, ok2 = okx && Q.yg < n1 && zb2 >= 0 && zb2 <= n2,
+                 ok3 = okx && Q.yg < n1 && zin;
+      cplxf(*dst)[R3_THREADS] = S.bp[zb2 & 3];
+      r3_cp8(&dst[0][t], ok0 ? b + g.off[0] + (int64_t)zb2 * pl0 + Q.b0off : b, ok0);
+      r3_cp8(&dst[1][t], ok1 ? b + g.off[1] + (int64_t)zb2 * (pl + n0) + boff : b, ok1);
+      r3_cp8(&dst[2][t], ok2 ? b + g.off[2] + (int64_t)zb2 * pl + boff : b, ok2);
+      r3_cp8(&dst[3][t], ok3 ? b + g.off[3] + (int64_t)zb2 * pl + boff : b, ok3);
+    }
     r3_cp_commit();
   }
   const int s0 = su0, s1 = su0 == 2 ? 0 : su0 + 1;
@@ -493,10 +509,13 @@ __global__ void __launch_bounds__(R3_THREADS, 1)
       r3_issue<V>(S, maps, Q.i0, Q.j0, zs, 2, zs, 2, zs, 1, false, 0, &S.bar[seq & 1]);
     }
     if constexpr (F) {  // u0 planes zs, zs+1 now, zs+2 in flight (completed at step zs's barrier)
-      r3_u0_plane(S.u0x[zs & 3], x + g.off[0], g, Q.i0, Q.j0, zs, t);
-      r3_u0_plane(S.u0x[(zs + 1) & 3], x + g.off[0], g, Q.i0, Q.j0, zs + 1, t);
+      const int64_t pl0 = (int64_t)(g.n[0] + 1) * g.n[1];
+      r3_u0_plane(S.u0x[zs & 3], x + g.off[0], pl0, g.n[2], zs, t, Q.u0ok0, Q.u0off0, Q.u0ok1, Q.u0off1);
+      r3_u0_plane(S.u0x[(zs + 1) & 3], x + g.off[0], pl0, g.n[2], zs + 1, t, Q.u0ok0, Q.u0off0, Q.u0ok1,
+                  Q.u0off1);
       r3_cp_commit();
-      r3_u0_plane(S.u0x[(zs + 2) & 3], x + g.off[0], g, Q.i0, Q.j0, zs + 2, t);
+      r3_u0_plane(S.u0x[(zs + 2) & 3], x + g.off[0], pl0, g.n[2], zs + 2, t, Q.u0ok0, Q.u0off0, Q.u0ok1,
+                  Q.u0off1);
       r3_cp_commit();
       r3_cp_wait<1>();
       __syncthreads();
@@ -559,7 +578,7 @@ inline int r3_device_init() {
 // (float for the complex64 kernel). Output planes [z_lo, z_hi) (default:
 // all, including the top u2 faces).
 template <class V>
-inline void launch_stencil3d_rr(const Geo& g, const OpPar& P, const typename VT<V>::R* media_soa, const V* x,
+inline bool launch_stencil3d_rr(const Geo& g, const OpPar& P, const typename VT<V>::R* media_soa, const V* x,
                                 const V* b, V* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
   typedef typename VT<V>::R R;
   constexpr bool F = sizeof(R) == 4;
@@ -592,21 +611,27 @@ inline void launch_stencil3d_rr(const Geo& g, const OpPar& P, const typename VT<
     e.m = media_soa;
     e.b = bkey;
     e.n[0] = n0, e.n[1] = n1, e.n[2] = n2;
+    bool ok = true;
     for (int k = F ? 1 : 0; k < 3; ++k)
-      r3_encode(&e.M.m.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_UX, R3_UY,
+      ok &= r3_encode(&e.M.m.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_UX, R3_UY,
                 es);
-    r3_encode(&e.M.m.p, x + g.off[3], 2 * n0, n1, n2, 2 * R3_UX, R3_UY, es);
+    ok &= r3_encode(&e.M.m.p, x + g.off[3], 2 * n0, n1, n2, 2 * R3_UX, R3_UY, es);
     const int64_t nc = g.ncells;
     constexpr int MX = R3SmemT<V>::MX;
-    r3_encode(&e.M.m.mu, media_soa + 0 * nc, n0, n1, n2, MX, R3_UY, es);
-    r3_encode(&e.M.m.rho, media_soa + 1 * nc, n0, n1, n2, MX, R3_UY, es);
-    r3_encode(&e.M.m.gam, media_soa + 2 * nc, n0, n1, n2, MX, R3_UY, es);
-    r3_encode(&e.M.m.ilm, media_soa + 3 * nc, n0, n1, n2, MX, R3_UY, es);
+    ok &= r3_encode(&e.M.m.mu, media_soa + 0 * nc, n0, n1, n2, MX, R3_UY, es);
+    ok &= r3_encode(&e.M.m.rho, media_soa + 1 * nc, n0, n1, n2, MX, R3_UY, es);
+    ok &= r3_encode(&e.M.m.gam, media_soa + 2 * nc, n0, n1, n2, MX, R3_UY, es);
+    ok &= r3_encode(&e.M.m.ilm, media_soa + 3 * nc, n0, n1, n2, MX, R3_UY, es);
     if (bkey) {
       for (int k = 0; k < 3; ++k)
-        r3_encode(&e.M.b[k], b + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_FX, R3_FY,
+        ok &= r3_encode(&e.M.b[k], b + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * R3_FX, R3_FY,
                   es);
-      r3_encode(&e.M.b[3], b + g.off[3], 2 * n0, n1, n2, 2 * R3_FX, R3_FY, es);
+      ok &= r3_encode(&e.M.b[3], b + g.off[3], 2 * n0, n1, n2, 2 * R3_FX, R3_FY, es);
+    }
+    if (!ok) {
+      fprintf(stderr, "ehmg: tensor map encode failed (n=%d,%d,%d F=%d x=%p b=%p)\n", n0, n1, n2, (int)F, (const void*)x,
+              (const void*)b);
+      return false;
     }
     if (cache.size() < 256) {
       cache.push_back(e);
@@ -619,24 +644,25 @@ inline void launch_stencil3d_rr(const Geo& g, const OpPar& P, const typename VT<
   }
   const R3Maps M = *Mp;
   const S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi, R3_TY, R3_TX);
-  if (sp.z_hi <= sp.z_lo) return;
+  if (sp.z_hi <= sp.z_lo) return true;
   const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
   const int grid = items < nsm ? items : nsm;
   k_stencil3d_rr<V><<<grid, R3_THREADS, sizeof(R3SmemT<V>), s>>>(M, sp, x, b, y);
+  return true;
 }
 
 inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
                              const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
-  launch_stencil3d_rr<cplx>(g, P, media_soa, x, b, y, s, z_lo, z_hi);
+  if (!launch_stencil3d_rr<cplx>(g, P, media_soa, x, b, y, s, z_lo, z_hi))
+    throw std::runtime_error("ehmg: 3D stencil tensor maps could not be encoded");
 }
 
 // complex64: the register-resident kernel needs 16-byte float media rows
 // (n0 % 4 == 0); other even widths take the cp.async 20-warp kernel.
 inline void launch_stencil3d(const Geo& g, const OpPar& P, const float* media_soa, const cplxf* x,
                              const cplxf* b, cplxf* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
-  if (g.n[0] % 4 == 0 && stencil3d_supported(g))
-    launch_stencil3d_rr<cplxf>(g, P, media_soa, x, b, y, s, z_lo, z_hi);
-  else
+  if (!(g.n[0] % 4 == 0 && stencil3d_supported(g) &&
+        launch_stencil3d_rr<cplxf>(g, P, media_soa, x, b, y, s, z_lo, z_hi)))
     launch_stencil3d_ca(g, P, media_soa, x, b, y, s, z_lo, z_hi);
 }
 
