@@ -572,61 +572,98 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo gf, Geo gc, const V* __re
   xc[gc.off[C] + o0 + (int64_t)D0 * (o1 + (int64_t)D1 * o2)] = narrow<V>(s2);
 }
 
-// Prolongation(+add) for one component; each thread produces kProlongNX
-// fine values 32 apart along x, so the y/z taps and coarse row addresses
-// (most of the per-output instructions) are formed once per thread.
-constexpr int kProlongNX = 8;
+// Prolongation(+add) for one component. A thread owns one fine (x, y)
+// column and marches a chunk of `zc` fine planes: the x/y contraction of a
+// coarse plane (s1, the inner two sums of k_transfer's axis-0-innermost
+// order) is formed once and kept in registers for the (up to four) fine
+// planes whose z taps read it, so a fine value costs one z combination
+// instead of the full 2x2x2 gather. Same operations in the same order as
+// k_transfer, hence bit-identical results.
+constexpr int kProlongG = 4;
 template <int C, class V = cplx>
 __global__ void __launch_bounds__(256) k_prolong3(Geo gf, Geo gc, const V* __restrict__ xc,
-                                                  V* __restrict__ xf, int accumulate) {
-  const int fx0 = blockIdx.x * (32 * kProlongNX) + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y, f2 = blockIdx.z;
-  const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1);
-  if (fx0 >= F0 || f1 >= F1) return;
+                                                  V* __restrict__ xf, int accumulate, int zc) {
+  const int f0 = blockIdx.x * 32 + threadIdx.x, f1 = blockIdx.y * 8 + threadIdx.y;
+  const int F0 = gf.n[0] + (C == 0), F1 = gf.n[1] + (C == 1), F2 = gf.n[2] + (C == 2);
+  if (f0 >= F0 || f1 >= F1) return;
+  const int za = blockIdx.z * zc, zb = za + zc < F2 ? za + zc : F2;
   const int D0 = gc.n[0] + (C == 0), D1 = gc.n[1] + (C == 1), D2 = gc.n[2] + (C == 2);
+  const Taps t0 = prolong_taps(f0, F0, C == 0);
   const Taps t1 = prolong_taps(f1, F1, C == 1);
-  const Taps t2 = prolong_taps(f2 + gf.zoff, gf.gn2 + (C == 2), C == 2);
   const V* base = xc + gc.off[C];
-  // coarse rows (q2, q1) and whether the z tap lies in this coarse window
-  const V* row[2][2];
-  bool zok[2];
-#pragma unroll
-  for (int q2 = 0; q2 < 2; ++q2) {
-    const int z = (q2 < t2.cnt ? t2.idx[q2] : t2.idx[0]) - gc.zoff;
-    zok[q2] = q2 < t2.cnt && z >= 0 && z < D2;
+  const int64_t r0 = (int64_t)D0 * t1.idx[0], r1 = (int64_t)D0 * (t1.cnt > 1 ? t1.idx[1] : t1.idx[0]);
+  const int64_t pl = (int64_t)D0 * D1;
+  // raw coarse taps of global coarse plane c (zero outside this coarse
+  // window), loaded one coarse plane before their contraction is needed
+  struct Raw {
+    V v[2][2];
+    bool ok;
+  };
+  auto load_raw = [&](int c) -> Raw {
+    Raw r;
+    const int z = c - gc.zoff;
+    r.ok = z >= 0 && z < D2;
+    const V* p = base + pl * (r.ok ? z : 0);
 #pragma unroll
     for (int q1 = 0; q1 < 2; ++q1)
-      row[q2][q1] = base + (int64_t)D0 * ((q1 < t1.cnt ? t1.idx[q1] : t1.idx[0]) + (int64_t)D1 * (zok[q2] ? z : 0));
-  }
-  V* orow = xf + gf.off[C] + (int64_t)F0 * (f1 + (int64_t)F1 * f2);
 #pragma unroll
-  for (int k = 0; k < kProlongNX; ++k) {
-    const int f0 = fx0 + 32 * k;
-    if (f0 >= F0) break;
-    const Taps t0 = prolong_taps(f0, F0, C == 0);
-    V* o = orow + f0;
-    const V old = accumulate ? *o : V{};  // issued first: overlaps the coarse gathers
-    // same contraction order as k_transfer (axis 0 innermost)
-    cplx s2 = mk(0, 0);
-#pragma unroll
-    for (int q2 = 0; q2 < 2; ++q2) {
-      if (q2 >= t2.cnt) break;
-      cplx s1 = mk(0, 0);
-      if (zok[q2]) {
-#pragma unroll
-        for (int q1 = 0; q1 < 2; ++q1) {
-          if (q1 >= t1.cnt) break;
-          cplx s0 = mk(0, 0);
-#pragma unroll
-          for (int q0 = 0; q0 < 2; ++q0) {
-            if (q0 >= t0.cnt) break;
-            s0 += t0.w[q0] * wide(row[q2][q1][t0.idx[q0]]);
-          }
-          s1 += t1.w[q1] * s0;
-        }
+      for (int q0 = 0; q0 < 2; ++q0) {
+        r.v[q1][q0] = V{};
+        if (r.ok && q1 < t1.cnt && q0 < t0.cnt) r.v[q1][q0] = p[(q1 ? r1 : r0) + t0.idx[q0]];
       }
-      s2 += t2.w[q2] * s1;
+    return r;
+  };
+  // s1 = the x/y contraction, k_transfer's order
+  auto contract = [&](const Raw& r) -> cplx {
+    cplx s1 = mk(0, 0);
+    if (!r.ok) return s1;
+#pragma unroll
+    for (int q1 = 0; q1 < 2; ++q1) {
+      if (q1 >= t1.cnt) break;
+      cplx s0 = mk(0, 0);
+#pragma unroll
+      for (int q0 = 0; q0 < 2; ++q0) {
+        if (q0 >= t0.cnt) break;
+        s0 += t0.w[q0] * wide(r.v[q1][q0]);
+      }
+      s1 += t1.w[q1] * s0;
     }
-    *o = narrow<V>(accumulate ? wide(old) + s2 : s2);
+    return s1;
+  };
+  auto s1_of = [&](int c) -> cplx { return contract(load_raw(c)); };
+  const int G2 = gf.gn2 + (C == 2);
+  int c = (za + gf.zoff) >> 1;  // coarse plane of tap 0 (global)
+  cplx P = s1_of(c - 1), Q = s1_of(c), R = s1_of(c + 1);
+  Raw NR = load_raw(c + 2);
+  V* __restrict__ col = xf + gf.off[C] + f0 + (int64_t)F0 * f1;
+  const int64_t fpl = (int64_t)F0 * F1;
+  // groups of kProlongG planes: their fine values are loaded up front so
+  // several HBM reads per thread are in flight
+  for (int fz = za; fz < zb; fz += kProlongG) {
+    V old[kProlongG];
+#pragma unroll
+    for (int k = 0; k < kProlongG; ++k) {
+      old[k] = V{};
+      if (accumulate && fz + k < zb) old[k] = col[fpl * (fz + k)];
+    }
+#pragma unroll
+    for (int k = 0; k < kProlongG; ++k) {
+      const int f2 = fz + k;
+      if (f2 >= zb) break;
+      const int g2 = f2 + gf.zoff;
+      if ((g2 >> 1) != c) {  // next coarse plane (uniform across the block)
+        ++c;
+        P = Q;
+        Q = R;
+        R = contract(NR);
+        NR = load_raw(c + 2);
+      }
+      const Taps t2 = prolong_taps(g2, G2, C == 2);
+      cplx s2 = mk(0, 0);
+      s2 += t2.w[0] * Q;
+      if (t2.cnt > 1) s2 += t2.w[1] * (t2.idx[1] < c ? P : R);
+      col[fpl * f2] = narrow<V>(accumulate ? wide(old[k]) + s2 : s2);
+    }
   }
 }
 

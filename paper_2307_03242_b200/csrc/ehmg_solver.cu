@@ -269,18 +269,19 @@ static void launch_transfer(const Geo& gf, const Geo& gc, bool restricting, cons
     const dim3 blk(32, 8);
     for (int c = 0; c < 4; ++c) {
       const int d0 = gto.n[0] + (c == 0), d1 = gto.n[1] + (c == 1), d2 = gto.n[2] + (c == 2);
-      const int bx = restricting ? 32 : 32 * kProlongNX;  // prolongation: kProlongNX values per thread
-      const dim3 grd((d0 + bx - 1) / bx, (d1 + 7) / 8, c < 3 ? d2 : gto.n[2]);
+      // prolongation: zc fine planes per thread (fewer on small levels, to keep the SMs busy)
+      const int zc = d2 >= 128 ? 16 : 4;
+      const dim3 grd((d0 + 31) / 32, (d1 + 7) / 8, restricting ? d2 : (d2 + zc - 1) / zc);
       if (restricting) {
         if (c == 0) k_restrict3<0, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
         else if (c == 1) k_restrict3<1, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
         else if (c == 2) k_restrict3<2, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
         else k_restrict3<3, V><<<grd, blk, 0, s>>>(gf, gc, in, out);
       } else {
-        if (c == 0) k_prolong3<0, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
-        else if (c == 1) k_prolong3<1, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
-        else if (c == 2) k_prolong3<2, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
-        else k_prolong3<3, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate);
+        if (c == 0) k_prolong3<0, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate, zc);
+        else if (c == 1) k_prolong3<1, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate, zc);
+        else if (c == 2) k_prolong3<2, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate, zc);
+        else k_prolong3<3, V><<<grd, blk, 0, s>>>(gf, gc, in, out, accumulate, zc);
       }
     }
   } else {
