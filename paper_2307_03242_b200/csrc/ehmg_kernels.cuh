@@ -848,13 +848,14 @@ __global__ void __launch_bounds__(kThreads) k_reduce(int mode, int64_t n, const 
 // then accumulate |w|^2 (want_norm) and <y, w> (y != null) over the updated w.
 // Per element the arithmetic equals the separate axpy-then-dot passes; the
 // reduction tree is the deterministic one of k_reduce. Results: out_norm[0],
-// out_dot[0..1]; coef[0..1] = -<y,w> for the next pass.
+// out_dot[0..1]; coef[0..1] = -<y,w> for the next pass; hacc += <y,w>
+// (re-orthogonalisation passes).
 __global__ void __launch_bounds__(kThreads) k_mgs(int64_t n, const double* __restrict__ ap,
                                                   const cplx* __restrict__ xa, cplx* __restrict__ w,
                                                   const cplx* __restrict__ y, int want_norm,
                                                   double* __restrict__ partial, unsigned* __restrict__ counter,
                                                   double* __restrict__ out_norm, double* __restrict__ out_dot,
-                                                  double* __restrict__ coef) {
+                                                  double* __restrict__ coef, double* __restrict__ hacc = nullptr) {
   const cplx a = xa ? mk(ap[0], ap[1]) : mk(0, 0);
   double sn = 0, sr = 0, si = 0;
   GRID_STRIDE(i, n) {
@@ -912,6 +913,10 @@ __global__ void __launch_bounds__(kThreads) k_mgs(int64_t n, const double* __res
     if (coef) {
       coef[0] = -t1;
       coef[1] = -t2;
+    }
+    if (hacc) {
+      hacc[0] += t1;
+      hacc[1] += t2;
     }
     *counter = 0;
   }

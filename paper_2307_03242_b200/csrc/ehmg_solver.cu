@@ -584,11 +584,25 @@ struct Fgmres {
         const double wpre = std::sqrt(hbuf[4]);
         double wn = std::sqrt(hbuf[6]);
         if (wn < 0.70710678 * wpre) {  // one re-orthogonalisation pass
-          for (int i = 0; i <= j; ++i) {
-            blas.reduce(0, n, V[i]->p, w.p, blas.res(), blas.coef(), blas.hcol(i));
-            blas.axpy(n, mk(0, 0), blas.coef(), V[i]->p, w.p);
+          if (blas.owned.empty()) {
+            // pipelined like the first pass; the corrections accumulate into H
+            double* cf[2] = {blas.coef(), blas.res()};
+            for (int i = 0; i <= j + 1; ++i) {
+              k_mgs<<<kRedBlocks, kThreads, 0, s>>>(n, i > 0 ? cf[(i - 1) & 1] : nullptr,
+                                                    i > 0 ? V[i - 1]->p : nullptr, w.p,
+                                                    i <= j ? V[i]->p : nullptr, i == j + 1, blas.partial3.p,
+                                                    blas.counter.p, i == j + 1 ? blas.wn() : nullptr,
+                                                    i <= j ? blas.hcol(m + 1) : nullptr, i <= j ? cf[i & 1] : nullptr,
+                                                    i <= j ? blas.hcol(i) : nullptr);
+              CK(cudaGetLastError());
+            }
+          } else {
+            for (int i = 0; i <= j; ++i) {
+              blas.reduce(0, n, V[i]->p, w.p, blas.res(), blas.coef(), blas.hcol(i));
+              blas.axpy(n, mk(0, 0), blas.coef(), V[i]->p, w.p);
+            }
+            blas.reduce(1, n, w.p, nullptr, blas.wn(), nullptr, nullptr);
           }
-          blas.reduce(1, n, w.p, nullptr, blas.wn(), nullptr, nullptr);
           CK(cudaMemcpyAsync(hbuf.data(), blas.scal.p, sizeof(double) * (8 + 2 * (j + 1)),
                              cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
