@@ -381,11 +381,12 @@ def run_b200(args, ws, rank, local):
         x = torch.zeros(N, dtype=torch.complex128, device="cuda")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+        res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it, orthogonalization=args.orth))
         torch.cuda.synchronize()
         ts = time.perf_counter() - t0
         solve = {"status": res.status, "iterations": res.iterations, "relres": res.relres,
-                 "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5)}
+                 "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5),
+                 "orthogonalization": args.orth}
 
     # the reference's "precision": "mixed" mode (experiments.hpp:241): complex64
     # hierarchy behind the complex128 FGMRES -- reported beside the headline
@@ -409,7 +410,7 @@ def run_b200(args, ws, rank, local):
             x = torch.zeros(N, dtype=torch.complex128, device="cuda")
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            res = E.fgmres(D0, mgm, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+            res = E.fgmres(D0, mgm, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it, orthogonalization=args.orth))
             torch.cuda.synchronize()
             ts = time.perf_counter() - t0
             mixed["gmres_time_to_1e-6"] = {"status": res.status, "iterations": res.iterations,
@@ -525,7 +526,7 @@ def run_b200_slabs(args, ws, rank, local):
     if args.solve:
         b = E.make_point_source(g, 0, (n // 2, n // 2, n // 2))
         t0 = time.perf_counter()
-        _, res = d.solve(b, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+        _, res = d.solve(b, E.KrylovOptions(restart=10, max_iterations=args.max_it, orthogonalization=args.orth))
         ts = max_over_ranks(ws, time.perf_counter() - t0)
         solve = {"status": res.status, "iterations": res.iterations, "relres": res.relres,
                  "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5)}
@@ -583,7 +584,7 @@ def run_b200_sources(args, ws, rank, local):
     for p in mine:
         b = torch.from_numpy(E.make_point_source(g, 2, p)).cuda()
         x.zero_()
-        res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it))
+        res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it, orthogonalization=args.orth))
         its.append(res.iterations)
     torch.cuda.synchronize()
     secs = max_over_ranks(ws, time.perf_counter() - t0)
@@ -630,6 +631,8 @@ def main():
     ap.add_argument("--solve", type=int, default=1)
     ap.add_argument("--mixed", type=int, default=1, help="also time the complex64-hierarchy mode")
     ap.add_argument("--max-it", type=int, default=600)
+    ap.add_argument("--orth", choices=["classical", "modified"], default="classical",
+                    help="FGMRES Arnoldi variant (modified = the reference's MGS order)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sources", type=int, default=32, help="--mode sources: number of point sources")
     ap.add_argument("--mode", choices=["slabs", "replicas", "sources"], default="slabs",

@@ -205,6 +205,13 @@ typedef struct {
   double rtol;
   double stall_factor;
   int stall_cycles;
+  /* B200 addition (not in krylov.hpp:45): Arnoldi orthogonalisation.
+   * 0 = classical Gram-Schmidt passes (all projections of a step in one HBM
+   *     pass, the update + norm in a second; with the reference's
+   *     re-orthogonalisation criterion this is CGS2) -- the default;
+   * 1 = modified Gram-Schmidt in the reference's order (krylov.hpp:115).
+   * Distributed (z-slab) solves always use 1. */
+  int orthogonalization;
 } ehmg_krylov_options;
 
 typedef struct {

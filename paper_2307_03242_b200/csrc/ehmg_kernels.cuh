@@ -922,6 +922,131 @@ __global__ void __launch_bounds__(kThreads) k_mgs(int64_t n, const double* __res
   }
 }
 
+// Classical Gram-Schmidt passes for the Arnoldi step (krylov.hpp:115-128
+// with the projections taken against one w instead of one at a time):
+// k_gs_dots takes every <V_i, w> (and optionally |w|^2) in ONE pass over w
+// and the NV basis vectors; k_gs_update applies w -= sum_i h_i V_i (in the
+// reference's i order) and takes |w|^2 of the result in a second pass. Per
+// Arnoldi step that is 16 (2j + 5) B/DOF of HBM traffic against
+// 16 (4j + 5) for the pipelined MGS passes; the reference's
+// re-orthogonalisation criterion then makes the pair CGS2 (the second pass
+// corrects the first pass's loss of orthogonality, as the re-orthogonalised
+// MGS does). Deterministic reductions: per-block partials in a fixed grid,
+// summed in block order by the last block.
+constexpr int kGsMax = 16;
+struct GsVecs {
+  const cplx* v[kGsMax];
+};
+
+template <int NV>
+__global__ void __launch_bounds__(kThreads) k_gs_dots(int64_t n, GsVecs P, const cplx* __restrict__ w,
+                                                      double* __restrict__ partial, unsigned* __restrict__ counter,
+                                                      double* __restrict__ out_norm, double* __restrict__ out_dots,
+                                                      double* __restrict__ hacc) {
+  constexpr int NR = 2 * NV + 1;  // dots (re, im) ..., |w|^2
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0;
+  GRID_STRIDE(i, n) {
+    const cplx v = w[i];
+    cplx y[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) y[q] = P.v[q][i];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      acc[2 * q] += y[q].x * v.x + y[q].y * v.y;
+      acc[2 * q + 1] += y[q].x * v.y - y[q].y * v.x;
+    }
+    acc[2 * NV] += v.x * v.x + v.y * v.y;
+  }
+  __shared__ double sh[NR][kThreads / 32];
+  __shared__ bool last;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const double s = warp_sum(acc[q]);
+    if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x / 32] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NR) {
+    double t = 0;
+    for (int q = 0; q < kThreads / 32; ++q) t += sh[threadIdx.x][q];
+    partial[(size_t)NR * blockIdx.x + threadIdx.x] = t;
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last && threadIdx.x < NR) {
+    __threadfence();
+    const volatile double* pp = (const volatile double*)partial;
+    double t = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += pp[(size_t)NR * b + threadIdx.x];
+    if (threadIdx.x == 2 * NV) {
+      if (out_norm) out_norm[0] = t;
+    } else {
+      out_dots[threadIdx.x] = t;
+      if (hacc) hacc[threadIdx.x] += t;
+    }
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) *counter = 0;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(kThreads) k_gs_update(int64_t n, GsVecs P, const double* __restrict__ h,
+                                                        cplx* __restrict__ w, double* __restrict__ partial,
+                                                        unsigned* __restrict__ counter, double* __restrict__ out_norm) {
+  cplx c[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) c[q] = mk(-h[2 * q], -h[2 * q + 1]);
+  double sn = 0;
+  GRID_STRIDE(i, n) {
+    cplx y[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) y[q] = P.v[q][i];
+    cplx v = w[i];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v += c[q] * y[q];
+    w[i] = v;
+    sn += v.x * v.x + v.y * v.y;
+  }
+  __shared__ double sh[kThreads / 32];
+  __shared__ bool last;
+  sn = warp_sum(sn);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = sn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int q = 0; q < kThreads / 32; ++q) t += sh[q];
+    partial[blockIdx.x] = t;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* pp = (const volatile double*)partial;
+    double t = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += pp[b];
+    out_norm[0] = t;
+    *counter = 0;
+  }
+}
+
+// Launch helpers: NV = 1 .. kGsMax basis vectors.
+template <int NV>
+inline void gs_launch(bool dots, int nv, int64_t n, const GsVecs& P, cplx* w, const double* h, double* partial,
+                      unsigned* counter, double* out_norm, double* out_dots, double* hacc, cudaStream_t s) {
+  if constexpr (NV <= kGsMax) {
+    if (nv != NV)
+      return gs_launch<NV + 1>(dots, nv, n, P, w, h, partial, counter, out_norm, out_dots, hacc, s);
+    if (dots)
+      k_gs_dots<NV><<<kRedBlocks, kThreads, 0, s>>>(n, P, w, partial, counter, out_norm, out_dots, hacc);
+    else
+      k_gs_update<NV><<<kRedBlocks, kThreads, 0, s>>>(n, P, h, w, partial, counter, out_norm);
+  }
+}
+
 // x += sum_i c_i Z_i (krylov.hpp:176), accumulated in the reference's order.
 struct MultiAxpy {
   int m;

@@ -420,10 +420,14 @@ struct Blas {
   DBuf<unsigned> counter;
   DBuf<double> scal;  // [0..1] last result, [2..3] coef, [4..] hessenberg column
   DBuf<double> partial3;
+  DBuf<double> partialN;  // classical Gram-Schmidt passes: 2 kGsMax + 1 per block
+  DBuf<double> corr;      // re-orthogonalisation corrections of one Arnoldi step
   void init(cudaStream_t s_, int ncol) {
     s = s_;
     partial.alloc(kRedBlocks);
     partial3.alloc(3 * kRedBlocks);
+    partialN.alloc((2 * kGsMax + 1) * kRedBlocks);
+    corr.alloc(2 * kGsMax);
     counter.alloc(1);
     counter.zero(s);
     scal.alloc(8 + 2 * (ncol + 2));
@@ -558,7 +562,19 @@ struct Fgmres {
       while (j < m && res.iterations < opt.max_iterations) {
         M(V[j]->p, Z[j]->p);
         A(Z[j]->p, w.p);
-        if (blas.owned.empty()) {
+        const bool cgs = blas.owned.empty() && opt.orthogonalization == 0 && j + 1 <= kGsMax;
+        GsVecs gv{};
+        if (cgs) {
+          // classical passes: all <V[i], w> and |w|^2 in one pass, then
+          // w -= sum_i h_i V[i] and |w|^2
+          for (int i = 0; i <= j; ++i) gv.v[i] = V[i]->p;
+          gs_launch<1>(true, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, blas.wpre(),
+                       blas.hcol(0), nullptr, s);
+          CK(cudaGetLastError());
+          gs_launch<1>(false, j + 1, n, gv, w.p, blas.hcol(0), blas.partialN.p, blas.counter.p, blas.wn(),
+                       nullptr, nullptr, s);
+          CK(cudaGetLastError());
+        } else if (blas.owned.empty()) {
           // pipelined MGS: pass i applies the projection on V[i-1] and takes <V[i], w>
           double* cf[2] = {blas.coef(), blas.res()};
           for (int i = 0; i <= j + 1; ++i) {
@@ -584,7 +600,15 @@ struct Fgmres {
         const double wpre = std::sqrt(hbuf[4]);
         double wn = std::sqrt(hbuf[6]);
         if (wn < 0.70710678 * wpre) {  // one re-orthogonalisation pass
-          if (blas.owned.empty()) {
+          if (cgs) {
+            // corrections c_i = <V[i], w> in one pass (H += c), w -= sum_i c_i V[i]
+            gs_launch<1>(true, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, nullptr, blas.corr.p,
+                         blas.hcol(0), s);
+            CK(cudaGetLastError());
+            gs_launch<1>(false, j + 1, n, gv, w.p, blas.corr.p, blas.partialN.p, blas.counter.p, blas.wn(), nullptr,
+                         nullptr, s);
+            CK(cudaGetLastError());
+          } else if (blas.owned.empty()) {
             // pipelined like the first pass; the corrections accumulate into H
             double* cf[2] = {blas.coef(), blas.res()};
             for (int i = 0; i <= j + 1; ++i) {
@@ -808,7 +832,8 @@ struct ehmg_mg_s {
   // The z-slab mode calls it for its first agglomerated level.
   void kcycle_top(const cplx* b, cplx* x) {
     Level& lv = *L[0];
-    ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol, 0.99, 2};
+    // inner K-cycle solves keep the reference's MGS order (few, small vectors)
+    ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol, 0.99, 2, 1};
     lv.inner.init(lv.g.ndofs, opt.k_inner_iterations, s);
     CK(cudaMemsetAsync(x, 0, sizeof(cplx) * lv.g.ndofs, s));
     std::vector<double> hist;
@@ -929,7 +954,7 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
         throw Err(EHMG_EINVAL, "mixed precision: K-cycles are not supported");
       } else {
         ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol,
-                               0.99, 2};
+                               0.99, 2, 1};
         nxt.inner.init(nxt.g.ndofs, opt.k_inner_iterations, s);
         CK(cudaMemsetAsync(nec, 0, sizeof(V) * nxt.g.ndofs, s));  // the inner solve's initial guess
         std::vector<double> hist;

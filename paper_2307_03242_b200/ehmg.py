@@ -60,7 +60,7 @@ class _MRes(C.Structure):
 
 class _KOpts(C.Structure):
     _fields_ = [("restart", C.c_int), ("max_iterations", C.c_int), ("rtol", C.c_double),
-                ("stall_factor", C.c_double), ("stall_cycles", C.c_int)]
+                ("stall_factor", C.c_double), ("stall_cycles", C.c_int), ("orthogonalization", C.c_int)]
 
 
 class _KRes(C.Structure):
@@ -801,7 +801,8 @@ class DistributedSlabSolver:
         opt = opt or KrylovOptions()
         b = np.ascontiguousarray(b, np.complex128)
         x = np.zeros(self.n, np.complex128)
-        ko = _KOpts(opt.restart, opt.max_iterations, opt.rtol, opt.stall_factor, opt.stall_cycles)
+        ko = _KOpts(opt.restart, opt.max_iterations, opt.rtol, opt.stall_factor, opt.stall_cycles,
+                    _ORTH[opt.orthogonalization])
         kr = _KRes()
         cap = opt.max_iterations + opt.max_iterations // max(1, opt.restart) + 8
         hist = np.zeros(cap, np.float64)
@@ -820,8 +821,12 @@ class KrylovOptions:
     rtol: float = 1e-6
     stall_factor: float = 0.99
     stall_cycles: int = 2
+    # B200 addition: "classical" (CGS passes, re-orthogonalised as the
+    # reference decides; fewer HBM passes) or "modified" (krylov.hpp:115 order)
+    orthogonalization: str = "classical"
 
 
+_ORTH = {"classical": 0, "modified": 1}
 _STATUS = {0: "converged", 1: "max_iterations", 2: "breakdown", 3: "stalled"}
 
 
@@ -842,7 +847,8 @@ def fgmres(A: OpData, M: Optional[Multigrid], b, x, opt: KrylovOptions = KrylovO
     px, wx = _ptr(x, n, writable=True)
     if wb != wx:
         raise ValueError("b and x must both be host arrays or both device tensors")
-    ko = _KOpts(opt.restart, opt.max_iterations, opt.rtol, opt.stall_factor, opt.stall_cycles)
+    ko = _KOpts(opt.restart, opt.max_iterations, opt.rtol, opt.stall_factor, opt.stall_cycles,
+                    _ORTH[opt.orthogonalization])
     kr = _KRes()
     cap = opt.max_iterations + opt.max_iterations // max(1, opt.restart) + 8
     hist = np.zeros(cap, np.float64)

@@ -141,7 +141,11 @@ def test_kcycle_and_wcycle_vs_oracle():
             assert np.array_equal(mg.precondition(b), z)
 
 
-def test_fgmres_iterations_vs_oracle_2d():
+@pytest.mark.parametrize("orth", ["classical", "modified"])
+def test_fgmres_iterations_vs_oracle_2d(orth):
+    """Both Arnoldi variants: the reference's MGS order and the default
+    classical passes (CGS2 under the reference's re-orthogonalisation test)
+    reach the oracle's iteration count +-1 and its solution."""
     dims = (128, 128)
     g = E.StaggeredGrid(dims, 1 / 128)
     sp = E.SpongeConfig(16)
@@ -156,7 +160,7 @@ def test_fgmres_iterations_vs_oracle_2d():
     mg = E.Multigrid(g, med, E.OperatorParams(2 / 3, omega, 0.5), opt)
     D0 = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.0))
     x = np.zeros(g.n_dofs(), complex)
-    res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=400))
+    res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=400, orthogonalization=orth))
     om = O.MG(dims, 1 / 128, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.5, n_levels=4, cycle="v",
               nu1=2, nu2=2, damping=0.25)
     xr, info = om.solve(O.Op(dims, 1 / 128, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.0), b,
