@@ -825,6 +825,10 @@ class KrylovOptions:
     # reference decides; fewer HBM passes) or "modified" (krylov.hpp:115 order)
     orthogonalization: str = "classical"
 
+    def __post_init__(self):
+        if self.orthogonalization not in _ORTH:
+            raise ValueError(f"krylov: unknown orthogonalization '{self.orthogonalization}'")
+
 
 _ORTH = {"classical": 0, "modified": 1}
 _STATUS = {0: "converged", 1: "max_iterations", 2: "breakdown", 3: "stalled"}

@@ -72,3 +72,22 @@ def test_host_validation_mirrors_reference_messages():
 
 def test_graft_entry_has_build_and_smoke():
     assert callable(__graft_entry__.build) and callable(__graft_entry__.smoke)
+
+
+def test_krylov_options_struct_matches_header():
+    """The ctypes mirror of ehmg_krylov_options carries every header field
+    (incl. the B200 orthogonalization switch) and rejects unknown variants."""
+    import ctypes
+    import paper_2307_03242_b200 as E
+    from paper_2307_03242_b200 import ehmg as H
+    src = open(HEADER).read()
+    body = src[:src.index("} ehmg_krylov_options;")]
+    body = body[body.rindex("typedef struct {"):]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"^\s*(?:int|double)\s+([a-z_]+);", body, re.M)
+    assert [f for f, _ in H._KOpts._fields_] == fields
+    assert ctypes.sizeof(H._KOpts) == 32  # int int double double int int
+    assert E.KrylovOptions().orthogonalization == "classical"
+    assert H._ORTH == {"classical": 0, "modified": 1}
+    with pytest.raises(ValueError, match="unknown orthogonalization"):
+        E.KrylovOptions(orthogonalization="householder")
