@@ -1846,6 +1846,8 @@ int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int wher
   return guard([&] {
     const int64_t n = A->g.ndofs;
     if (M && M->L[0]->g.ndofs != n) throw Err(EHMG_EINVAL, "fgmres: operator/preconditioner size mismatch");
+    if (opt->orthogonalization != 0 && opt->orthogonalization != 1)
+      throw Err(EHMG_EINVAL, "krylov: unknown orthogonalization");
     cudaStream_t s = M ? M->s : A->s;
     // keep the operator on the solver stream
     const cplx* db;
