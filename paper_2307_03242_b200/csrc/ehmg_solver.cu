@@ -768,6 +768,11 @@ struct ehmg_mg_s {
   std::vector<std::unique_ptr<Level>> L;
   DBuf<cplx> ainv;  // row-major inverse of the coarsest operator
   int64_t nco = 0;
+  // FGMRES workspace of solves preconditioned by this hierarchy (2m+3
+  // level-0 vectors), kept between solves so the basis buffers -- and the
+  // CUDA graphs of the cycle, keyed by (r, z) -- are reused; released with
+  // the handle
+  std::unique_ptr<Fgmres> solve_ws;
   DBuf<cplx> hx, hy;
   // precision 1: the hierarchy holds complex64 fields, caches and coarsest
   // inverse (experiments.hpp:241 MixedPrecondition); r and z stay complex128.
@@ -1861,7 +1866,9 @@ int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int wher
       CK(cudaMemcpyAsync(sx.p, x, sizeof(cplx) * n, cudaMemcpyHostToDevice, s));
       dx = sx.p;
     }
-    Fgmres fg;
+    Fgmres local;
+    if (M && !M->solve_ws) M->solve_ws.reset(new Fgmres());
+    Fgmres& fg = M ? *M->solve_ws : local;
     fg.init(n, opt->restart, s);
     Fgmres::Fn Af = [&](const cplx* in, cplx* out) {
       launch_residual(A->g, A->P, A->media.ref(), in, nullptr, out, s);
