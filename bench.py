@@ -587,7 +587,8 @@ def run_b200_sources(args, ws, rank, local):
     mine = [p for k, p in enumerate(pos) if k % ws == rank]
     x = torch.zeros(N, dtype=torch.complex128, device="cuda")
     warm = torch.from_numpy(E.make_point_source(g, 2, pos[0])).cuda()
-    E.fgmres(D0, mg, warm, x, E.KrylovOptions(restart=10, max_iterations=3))  # graphs, lazy setup
+    # warm-up: workspace on the handle + the cycle's graphs for all basis buffers
+    E.fgmres(D0, mg, warm, x, E.KrylovOptions(restart=10, max_iterations=20, orthogonalization=args.orth))
     barrier(ws)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
