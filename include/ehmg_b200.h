@@ -221,6 +221,9 @@ typedef struct {
   int n_history;
 } ehmg_krylov_result;
 
+/* The FGMRES workspace (2 restart + 3 level-0 vectors) stays on M between
+ * solves (released by ehmg_multigrid_destroy); M == NULL solves unpreconditioned
+ * with a per-call workspace. */
 int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int where,
                       const ehmg_krylov_options* opt, ehmg_krylov_result* res, double* history,
                       int history_cap);
