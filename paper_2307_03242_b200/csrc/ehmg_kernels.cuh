@@ -992,14 +992,23 @@ __global__ void __launch_bounds__(kThreads) k_gs_dots(int64_t n, GsVecs P, const
   if (last && threadIdx.x == 0) *counter = 0;
 }
 
-template <int NV>
+// DOTS: the same pass also takes <V_i, w_new> over the updated values --
+// exactly the projections a re-orthogonalisation pass would take first
+// (same per-element operations, same reduction tree), so when the
+// reference's test asks for one, only its update pass remains.
+// Results: out[0 .. 2NV) = <V_i, w_new> (DOTS), out_norm[0] = |w_new|^2.
+template <int NV, bool DOTS>
 __global__ void __launch_bounds__(kThreads) k_gs_update(int64_t n, GsVecs P, const double* __restrict__ h,
                                                         cplx* __restrict__ w, double* __restrict__ partial,
-                                                        unsigned* __restrict__ counter, double* __restrict__ out_norm) {
+                                                        unsigned* __restrict__ counter, double* __restrict__ out_norm,
+                                                        double* __restrict__ out_dots) {
+  constexpr int NR = DOTS ? 2 * NV + 1 : 1;  // (dots,) |w|^2 last
   cplx c[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) c[q] = mk(-h[2 * q], -h[2 * q + 1]);
-  double sn = 0;
+  double acc[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) acc[q] = 0;
   GRID_STRIDE(i, n) {
     cplx y[NV];
 #pragma unroll
@@ -1008,42 +1017,59 @@ __global__ void __launch_bounds__(kThreads) k_gs_update(int64_t n, GsVecs P, con
 #pragma unroll
     for (int q = 0; q < NV; ++q) v += c[q] * y[q];
     w[i] = v;
-    sn += v.x * v.x + v.y * v.y;
+    if constexpr (DOTS) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        acc[2 * q] += y[q].x * v.x + y[q].y * v.y;
+        acc[2 * q + 1] += y[q].x * v.y - y[q].y * v.x;
+      }
+    }
+    acc[NR - 1] += v.x * v.x + v.y * v.y;
   }
-  __shared__ double sh[kThreads / 32];
+  __shared__ double sh[NR][kThreads / 32];
   __shared__ bool last;
-  sn = warp_sum(sn);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = sn;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0;
-    for (int q = 0; q < kThreads / 32; ++q) t += sh[q];
-    partial[blockIdx.x] = t;
-    __threadfence();
-    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const double sv = warp_sum(acc[q]);
+    if ((threadIdx.x & 31) == 0) sh[q][threadIdx.x / 32] = sv;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (threadIdx.x < NR) {
+    double t = 0;
+    for (int q = 0; q < kThreads / 32; ++q) t += sh[threadIdx.x][q];
+    partial[(size_t)NR * blockIdx.x + threadIdx.x] = t;
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last && threadIdx.x < NR) {
     __threadfence();
     const volatile double* pp = (const volatile double*)partial;
     double t = 0;
-    for (unsigned b = 0; b < gridDim.x; ++b) t += pp[b];
-    out_norm[0] = t;
-    *counter = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += pp[(size_t)NR * b + threadIdx.x];
+    if (threadIdx.x == NR - 1) out_norm[0] = t;
+    else out_dots[threadIdx.x] = t;
   }
+  __syncthreads();
+  if (last && threadIdx.x == 0) *counter = 0;
 }
 
-// Launch helpers: NV = 1 .. kGsMax basis vectors.
+// Launch helpers: NV = 1 .. kGsMax basis vectors. mode 0: dots pass;
+// 1: update pass; 2: update pass that also takes the projections of the
+// updated w (into out_dots).
 template <int NV>
-inline void gs_launch(bool dots, int nv, int64_t n, const GsVecs& P, cplx* w, const double* h, double* partial,
+inline void gs_launch(int mode, int nv, int64_t n, const GsVecs& P, cplx* w, const double* h, double* partial,
                       unsigned* counter, double* out_norm, double* out_dots, double* hacc, cudaStream_t s) {
   if constexpr (NV <= kGsMax) {
     if (nv != NV)
-      return gs_launch<NV + 1>(dots, nv, n, P, w, h, partial, counter, out_norm, out_dots, hacc, s);
-    if (dots)
+      return gs_launch<NV + 1>(mode, nv, n, P, w, h, partial, counter, out_norm, out_dots, hacc, s);
+    if (mode == 0)
       k_gs_dots<NV><<<kRedBlocks, kThreads, 0, s>>>(n, P, w, partial, counter, out_norm, out_dots, hacc);
+    else if (mode == 1)
+      k_gs_update<NV, false><<<kRedBlocks, kThreads, 0, s>>>(n, P, h, w, partial, counter, out_norm, nullptr);
     else
-      k_gs_update<NV><<<kRedBlocks, kThreads, 0, s>>>(n, P, h, w, partial, counter, out_norm);
+      k_gs_update<NV, true><<<kRedBlocks, kThreads, 0, s>>>(n, P, h, w, partial, counter, out_norm, out_dots);
   }
 }
 

@@ -550,7 +550,7 @@ struct Fgmres {
     auto HH = [&](int i, int j) -> cplx& { return H[(size_t)i * m + j]; };
     std::vector<double> gc(m, 0.0);
     std::vector<cplx> gs(m, mk(0, 0)), g(m + 1, mk(0, 0)), y(m, mk(0, 0));
-    std::vector<double> hbuf(8 + 2 * (m + 2));
+    std::vector<double> hbuf(8 + 2 * (m + 2)), hcorr(2 * kGsMax);
     double prev_cycle = beta;
     int stall = 0;
     while (res.iterations < opt.max_iterations) {
@@ -566,13 +566,15 @@ struct Fgmres {
         GsVecs gv{};
         if (cgs) {
           // classical passes: all <V[i], w> and |w|^2 in one pass, then
-          // w -= sum_i h_i V[i] and |w|^2
+          // w -= sum_i h_i V[i] and |w|^2 -- the update pass also takes the
+          // projections <V[i], w> of the updated w, which a
+          // re-orthogonalisation pass would otherwise take first
           for (int i = 0; i <= j; ++i) gv.v[i] = V[i]->p;
-          gs_launch<1>(true, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, blas.wpre(),
+          gs_launch<1>(0, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, blas.wpre(),
                        blas.hcol(0), nullptr, s);
           CK(cudaGetLastError());
-          gs_launch<1>(false, j + 1, n, gv, w.p, blas.hcol(0), blas.partialN.p, blas.counter.p, blas.wn(),
-                       nullptr, nullptr, s);
+          gs_launch<1>(2, j + 1, n, gv, w.p, blas.hcol(0), blas.partialN.p, blas.counter.p, blas.wn(),
+                       blas.corr.p, nullptr, s);
           CK(cudaGetLastError());
         } else if (blas.owned.empty()) {
           // pipelined MGS: pass i applies the projection on V[i-1] and takes <V[i], w>
@@ -601,13 +603,12 @@ struct Fgmres {
         double wn = std::sqrt(hbuf[6]);
         if (wn < 0.70710678 * wpre) {  // one re-orthogonalisation pass
           if (cgs) {
-            // corrections c_i = <V[i], w> in one pass (H += c), w -= sum_i c_i V[i]
-            gs_launch<1>(true, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, nullptr, blas.corr.p,
-                         blas.hcol(0), s);
-            CK(cudaGetLastError());
-            gs_launch<1>(false, j + 1, n, gv, w.p, blas.corr.p, blas.partialN.p, blas.counter.p, blas.wn(), nullptr,
+            // corrections c_i = <V[i], w> came with the update pass:
+            // w -= sum_i c_i V[i] (H += c on the host below)
+            gs_launch<1>(1, j + 1, n, gv, w.p, blas.corr.p, blas.partialN.p, blas.counter.p, blas.wn(), nullptr,
                          nullptr, s);
             CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(hcorr.data(), blas.corr.p, sizeof(double) * 2 * (j + 1), cudaMemcpyDeviceToHost, s));
           } else if (blas.owned.empty()) {
             // pipelined like the first pass; the corrections accumulate into H
             double* cf[2] = {blas.coef(), blas.res()};
@@ -631,6 +632,8 @@ struct Fgmres {
                              cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
           wn = std::sqrt(hbuf[6]);
+          if (cgs)  // H += c, the addition the device-side accumulation performed
+            for (int i = 0; i < 2 * (j + 1); ++i) hbuf[8 + i] += hcorr[i];
         }
         for (int i = 0; i <= j; ++i) HH(i, j) = mk(hbuf[8 + 2 * i], hbuf[9 + 2 * i]);
         HH(j + 1, j) = mk(wn, 0);
