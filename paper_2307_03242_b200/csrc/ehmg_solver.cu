@@ -566,15 +566,16 @@ struct Fgmres {
         GsVecs gv{};
         if (cgs) {
           // classical passes: all <V[i], w> and |w|^2 in one pass, then
-          // w -= sum_i h_i V[i] and |w|^2 -- the update pass also takes the
-          // projections <V[i], w> of the updated w, which a
-          // re-orthogonalisation pass would otherwise take first
+          // w -= sum_i h_i V[i] and |w|^2. (Taking the projections of the
+          // updated w in the same pass -- mode 2 -- saves the first pass of a
+          // re-orthogonalisation but slows every update pass 0.98 -> 1.10 ms
+          // at 256^3 under ncu, and the test rarely fires: not used.)
           for (int i = 0; i <= j; ++i) gv.v[i] = V[i]->p;
           gs_launch<1>(0, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, blas.wpre(),
                        blas.hcol(0), nullptr, s);
           CK(cudaGetLastError());
-          gs_launch<1>(2, j + 1, n, gv, w.p, blas.hcol(0), blas.partialN.p, blas.counter.p, blas.wn(),
-                       blas.corr.p, nullptr, s);
+          gs_launch<1>(1, j + 1, n, gv, w.p, blas.hcol(0), blas.partialN.p, blas.counter.p, blas.wn(),
+                       nullptr, nullptr, s);
           CK(cudaGetLastError());
         } else if (blas.owned.empty()) {
           // pipelined MGS: pass i applies the projection on V[i-1] and takes <V[i], w>
@@ -603,8 +604,11 @@ struct Fgmres {
         double wn = std::sqrt(hbuf[6]);
         if (wn < 0.70710678 * wpre) {  // one re-orthogonalisation pass
           if (cgs) {
-            // corrections c_i = <V[i], w> came with the update pass:
-            // w -= sum_i c_i V[i] (H += c on the host below)
+            // corrections c_i = <V[i], w> in one pass, w -= sum_i c_i V[i]
+            // (H += c on the host below)
+            gs_launch<1>(0, j + 1, n, gv, w.p, nullptr, blas.partialN.p, blas.counter.p, nullptr, blas.corr.p,
+                         nullptr, s);
+            CK(cudaGetLastError());
             gs_launch<1>(1, j + 1, n, gv, w.p, blas.corr.p, blas.partialN.p, blas.counter.p, blas.wn(), nullptr,
                          nullptr, s);
             CK(cudaGetLastError());
