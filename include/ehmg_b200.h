@@ -13,6 +13,12 @@
  * (EHMG_HOST: copied to/from HBM inside the call) or device memory that the
  * caller keeps resident in HBM (EHMG_DEVICE).
  *
+ * Ordering of EHMG_DEVICE buffers: the library runs its kernels on its own
+ * non-blocking CUDA streams, so a device input must be complete before the
+ * call (synchronise the stream that produced it; the Python binding does this
+ * for torch's current stream). Device outputs are complete when the call
+ * returns (the library synchronises its stream).
+ *
  * Media are cell-sized float64 arrays, axis-0-fastest (media.hpp:13).
  * Errors: every call returns 0 on success or a negative EHMG_E* code; the
  * message (mirroring the reference's exception text) is available from
@@ -87,9 +93,19 @@ int ehmg_layered_media(int ndim, const int* dims, double gamma_phys, uint64_t se
 
 /* ---- multigrid: multigrid.hpp:34 MgOptions, :75 Multigrid, :133 cycle,
  *      :136 precondition --------------------------------------------------
- * cycle: 0 two_grid, 1 v, 2 w, 3 k. coarse: the coarsest level is solved
- * exactly (CoarseSolverKind::lu, multigrid.hpp:97) by an LU-derived inverse
- * held in HBM. */
+ * cycle: 0 two_grid, 1 v, 2 w, 3 k.
+ * coarse (multigrid.hpp:22 CoarseSolverKind): 0 automatic, 1 lu, 2 kaczmarz.
+ * automatic and lu solve the coarsest level exactly (CoarseSolverKind::lu,
+ * multigrid.hpp:97) by an LU-derived inverse held in HBM; the reference's
+ * automatic picks Kaczmarz-FGMRES in 3D (multigrid.hpp:93-95), which is not on
+ * the B200 path: coarse = 2 returns EHMG_EINVAL. lu_dof_budget
+ * (multigrid.hpp:42; 0 = the reference default 4000000) bounds the coarsest
+ * DOF count: EHMG_ERANGE "assemble_sparse: grid exceeds DOF budget of N"
+ * (assemble.hpp:209-211). The dense inverse also needs 2 N^2 complex of free
+ * HBM during set-up (EHMG_ERANGE otherwise; N ~ 60000 on an idle B200).
+ * kz_* (multigrid.hpp:45-49) are accepted and validated for ABI parity; they
+ * only matter to the Kaczmarz solve. Zero-initialise the struct and set
+ * the fields you use: zero kz_* values are read as the reference defaults. */
 typedef struct {
   int n_levels;
   int cycle;
@@ -103,6 +119,13 @@ typedef struct {
    * precondition()/cycle() calls (experiments.hpp:241 MixedPrecondition,
    * config "precision": "mixed"; V/W/two-grid cycles, red-black sweeps) */
   int precision;
+  int coarse;
+  int64_t lu_dof_budget;
+  int kz_sweeps_per_apply;
+  double kz_damping;
+  double kz_rtol;
+  int kz_max_iterations;
+  int kz_restart;
 } ehmg_mg_options;
 
 int ehmg_multigrid_create(int ndim, const int* dims, double h, const double* lambda,

@@ -17,6 +17,8 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <chrono>
+#include <stdexcept>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -25,7 +27,11 @@ constexpr int kCommMaxRanks = 16;
 constexpr int kCommRedSlots = 64;
 constexpr int kCommBlob = 4096;
 
+constexpr int kCommReady = 0x45484d47;  // "EHMG"
+
 struct CommShm {
+  std::atomic<int> ready;     // kCommReady once rank 0 initialised this segment
+  std::atomic<int> failed;    // a rank gave up: every barrier throws, close() skips its barrier
   std::atomic<int> arrived;
   std::atomic<int> sense;
   std::atomic<int> attached;
@@ -38,29 +44,117 @@ struct NodeComm {
   std::string name;
   CommShm* shm = nullptr;
   int local_sense = 0;
+  double timeout_s = 120.0;
 
+  static CommShm* map_fd(int fd) {
+    void* p = mmap(nullptr, sizeof(CommShm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    ::close(fd);
+    return p == MAP_FAILED ? nullptr : static_cast<CommShm*>(p);
+  }
+  void deadline_check(const std::chrono::steady_clock::time_point& t0, const char* what) {
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+      throw std::runtime_error(std::string("comm: timed out waiting for ") + what + " (" + name + ")");
+  }
+
+  // Rank 0 invalidates any segment a crashed job left under this name
+  // (ready = 0, failed = 1), unlinks it and creates a fresh one exclusively;
+  // the other ranks attach only to a segment whose ready flag is set and
+  // start over if it is invalidated while they wait for the others.
   void open(const std::string& job, int r, int nranks) {
     if (nranks < 1 || nranks > kCommMaxRanks) throw std::runtime_error("comm: 1..16 ranks");
+    if (r < 0 || r >= nranks) throw std::runtime_error("comm: rank out of range");
     rank = r;
     n = nranks;
     name = "/ehmg_" + job;
-    int fd = shm_open(name.c_str(), O_CREAT | O_RDWR, 0600);
-    if (fd < 0) throw std::runtime_error("comm: shm_open failed for " + name);
-    if (ftruncate(fd, sizeof(CommShm)) != 0) {
-      ::close(fd);
-      throw std::runtime_error("comm: ftruncate failed");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (rank == 0) {
+      int ofd = shm_open(name.c_str(), O_RDWR, 0600);
+      if (ofd >= 0) {
+        struct stat st;
+        if (fstat(ofd, &st) == 0 && st.st_size >= (off_t)sizeof(CommShm)) {
+          if (CommShm* old = map_fd(ofd)) {
+            old->ready.store(0);
+            old->failed.store(1);
+            munmap(old, sizeof(CommShm));
+          }
+        } else {
+          ::close(ofd);
+        }
+        shm_unlink(name.c_str());
+      }
+      int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+      if (fd < 0) throw std::runtime_error("comm: shm_open failed for " + name);
+      if (ftruncate(fd, sizeof(CommShm)) != 0) {
+        ::close(fd);
+        shm_unlink(name.c_str());
+        throw std::runtime_error("comm: ftruncate failed");
+      }
+      shm = map_fd(fd);
+      if (!shm) throw std::runtime_error("comm: mmap failed");
+      shm->failed.store(0);
+      shm->arrived.store(0);
+      shm->sense.store(0);
+      shm->attached.store(1);
+      shm->ready.store(kCommReady);
+      while (shm->attached.load() < n) {
+        if (shm->failed.load()) throw std::runtime_error("comm: a peer rank failed during open");
+        deadline_check(t0, "ranks to attach");
+        std::this_thread::yield();
+      }
+      return;
     }
-    void* p = mmap(nullptr, sizeof(CommShm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-    ::close(fd);
-    if (p == MAP_FAILED) throw std::runtime_error("comm: mmap failed");
-    shm = static_cast<CommShm*>(p);
-    // a fresh segment is zero-filled: arrived = sense = attached = 0
-    shm->attached.fetch_add(1);
-    while (shm->attached.load() < n) std::this_thread::yield();
+    for (;;) {
+      deadline_check(t0, "rank 0's segment");
+      int fd = shm_open(name.c_str(), O_RDWR, 0600);
+      if (fd < 0) {
+        std::this_thread::yield();
+        continue;
+      }
+      struct stat st;
+      if (fstat(fd, &st) != 0 || st.st_size < (off_t)sizeof(CommShm)) {
+        ::close(fd);
+        std::this_thread::yield();
+        continue;
+      }
+      CommShm* p = map_fd(fd);
+      if (!p) throw std::runtime_error("comm: mmap failed");
+      if (p->ready.load() != kCommReady || p->failed.load()) {
+        munmap(p, sizeof(CommShm));
+        std::this_thread::yield();
+        continue;
+      }
+      p->attached.fetch_add(1);
+      bool stale = false;
+      while (p->attached.load() < n) {
+        if (p->ready.load() != kCommReady) { stale = true; break; }
+        if (p->failed.load()) {
+          munmap(p, sizeof(CommShm));
+          throw std::runtime_error("comm: a peer rank failed during open");
+        }
+        deadline_check(t0, "ranks to attach");
+        std::this_thread::yield();
+      }
+      if (stale) {  // attached to a segment rank 0 has just replaced
+        munmap(p, sizeof(CommShm));
+        continue;
+      }
+      shm = p;
+      return;
+    }
+  }
+  // Mark the job failed: peers blocked in a barrier throw instead of pairing
+  // this rank's teardown barrier with their exchange barriers.
+  void fail() {
+    if (shm) shm->failed.store(1);
   }
   void close() {
     if (!shm) return;
-    barrier();
+    if (!shm->failed.load()) {
+      try {
+        barrier();
+      } catch (...) {
+      }
+    }
     const int left = shm->attached.fetch_sub(1) - 1;
     munmap(shm, sizeof(CommShm));
     shm = nullptr;
@@ -77,7 +171,10 @@ struct NodeComm {
       shm->arrived.store(0);
       shm->sense.store(local_sense);
     } else {
-      while (shm->sense.load() != local_sense) std::this_thread::yield();
+      while (shm->sense.load() != local_sense) {
+        if (shm->failed.load()) throw std::runtime_error("comm: a peer rank failed");
+        std::this_thread::yield();
+      }
     }
   }
   // v[0..k) <- sum over ranks (rank order), identical on every rank

@@ -399,7 +399,8 @@ struct ehmg_slab_mg_s {
     fg.init(c.sg.g.ndofs, opt.k_inner_iterations, s);
     fg.blas.comm = comm;
     fg.blas.owned = owned_ranges(l1, q);
-    ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol, 0.99, 2};
+    // inner K-cycle solves keep the reference's MGS order (orthogonalization = 1)
+    ehmg_krylov_options ko{opt.k_inner_iterations, opt.k_inner_iterations, opt.k_inner_rtol, 0.99, 2, 1};
     std::vector<cplx*> VV(P_(), nullptr), WW(P_(), nullptr);
     Fgmres::Fn A = [&](const cplx* in, cplx* out) {
       VV[q] = const_cast<cplx*>(in);  // ghost planes are scratch

@@ -512,15 +512,20 @@ struct Fgmres {
 
   void init(int64_t n_, int m_, cudaStream_t s) {
     if (n == n_ && m == m_) return;
-    n = n_;
-    m = m_;
+    // marked initialised only once every buffer exists: a failed cudaMalloc
+    // part-way (2m+3 level-0 vectors) leaves n = m = 0, so the next call
+    // allocates again instead of indexing missing buffers
+    n = 0;
+    m = 0;
     V.clear();
     Z.clear();
-    for (int i = 0; i <= m; ++i) V.emplace_back(new DBuf<cplx>(n));
-    for (int i = 0; i < m; ++i) Z.emplace_back(new DBuf<cplx>(n));
-    r.alloc(n);
-    w.alloc(n);
-    blas.init(s, m + 1);
+    for (int i = 0; i <= m_; ++i) V.emplace_back(new DBuf<cplx>(n_));
+    for (int i = 0; i < m_; ++i) Z.emplace_back(new DBuf<cplx>(n_));
+    r.alloc(n_);
+    w.alloc(n_);
+    blas.init(s, m_ + 1);
+    n = n_;
+    m = m_;
   }
 
   using Fn = std::function<void(const cplx*, cplx*)>;
@@ -1210,6 +1215,16 @@ static void measure_t(ehmg_mg_s& mg, uint64_t seed, const ehmg_measure_options& 
 }
 
 // ------------------------------------------------------------------ C ABI
+// krylov.hpp:45 KrylovOptions sanity: a restart of 0 would never grow the
+// iteration count (the outer loop would spin), so it is rejected up front.
+static void check_krylov_args(const ehmg_krylov_options* opt, const ehmg_krylov_result* res) {
+  if (!opt || !res) throw Err(EHMG_EINVAL, "fgmres: null options or result");
+  if (opt->restart < 1) throw Err(EHMG_EINVAL, "fgmres: restart must be >= 1");
+  if (opt->max_iterations < 0) throw Err(EHMG_EINVAL, "fgmres: max_iterations must be >= 0");
+  if (opt->orthogonalization != 0 && opt->orthogonalization != 1)
+    throw Err(EHMG_EINVAL, "krylov: unknown orthogonalization");
+}
+
 extern "C" {
 
 const char* ehmg_last_error(void) { return g_last_error.c_str(); }
@@ -1437,6 +1452,25 @@ int ehmg_attenuation_profile(int nd, const int* dims, double gamma_phys, int L, 
   });
 }
 
+// multigrid.hpp:40-50 coarsest-solver options. automatic and lu take the
+// exact solve (the reference's automatic picks Kaczmarz-FGMRES in 3D,
+// multigrid.hpp:93-95, a strictly sequential row-projection sweep with no
+// B200 counterpart: DESIGN.md "Coarsest solve"); kaczmarz is rejected. The
+// reference's lu_dof_budget is honoured with its own length_error text
+// (assemble.hpp:209-211); 0 means the reference default of 4M DOFs.
+static void check_coarse_options(const Geo& fine, const ehmg_mg_options* opt) {
+  if (opt->coarse == 2)
+    throw Err(EHMG_EINVAL,
+              "multigrid: coarse solver 'kaczmarz' is not on the B200 path (use 'lu' or 'automatic')");
+  if (opt->coarse != 0 && opt->coarse != 1) throw Err(EHMG_EINVAL, "config: unknown coarse solver");
+  if (opt->lu_dof_budget < 0) throw Err(EHMG_EINVAL, "multigrid: lu_dof_budget must be >= 0");
+  const int64_t budget = opt->lu_dof_budget > 0 ? opt->lu_dof_budget : (int64_t)4000000;
+  Geo t = fine;
+  for (int l = 0; l + 1 < opt->n_levels; ++l) t = coarse_geo(t);
+  if (t.ndofs > budget)
+    throw Err(EHMG_ERANGE, "assemble_sparse: grid exceeds DOF budget of " + std::to_string(budget));
+}
+
 int ehmg_multigrid_create(int nd, const int* dims, double h, const double* lambda,
                           const double* mu, const double* rho, const double* gamma, double beta,
                           double omega, double alpha, const ehmg_mg_options* opt, ehmg_mg* out) {
@@ -1445,7 +1479,6 @@ int ehmg_multigrid_create(int nd, const int* dims, double h, const double* lambd
     if (opt->cycle == 0 && opt->n_levels != 2)
       throw Err(EHMG_EINVAL, "multigrid: two_grid cycle requires exactly 2 levels");
     validate_grid(nd, dims, h);
-    check_device();
     int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
     Geo g = make_geo(nd, d, h);
     validate_media(g.ncells, lambda, mu, rho, gamma);
@@ -1459,6 +1492,8 @@ int ehmg_multigrid_create(int nd, const int* dims, double h, const double* lambd
         t = coarse_geo(t);
       }
     }
+    check_coarse_options(g, opt);
+    check_device();
     const OpPar P{beta, omega * omega, alpha};
     const double* f[4] = {lambda, mu, rho, gamma};
     *out = build_mg(g, f, nullptr, P, *opt, opt->n_levels).release();
@@ -1495,6 +1530,7 @@ int ehmg_slab_multigrid_create(int nd, const int* dims, double h, const double* 
         t = coarse_geo(t);
       }
     }
+    check_coarse_options(g, opt);
     const OpPar P{beta, omega * omega, alpha};
     const double* f[4] = {lambda, mu, rho, gamma};
     *out = build_slab_mg(g, f, P, *opt, nslabs, agg_n2, nullptr).release();
@@ -1589,12 +1625,27 @@ int ehmg_dist_create(const char* job, int rank, int nranks, int device, int nd, 
     int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
     Geo g = make_geo(nd, d, h);
     validate_media(g.ncells, lambda, mu, rho, gamma);
+    {
+      Geo t = g;
+      for (int l = 0; l + 1 < opt->n_levels; ++l) {
+        for (int a = 0; a < nd; ++a)
+          if (t.n[a] % 2 != 0 || t.n[a] / 2 < 2)
+            throw Err(EHMG_EINVAL, "multigrid: grid cannot support requested levels");
+        t = coarse_geo(t);
+      }
+    }
+    check_coarse_options(g, opt);
     auto dd = std::make_unique<ehmg_dist_s>();
     dd->comm.open(job, rank, nranks);
     const OpPar P{beta, omega * omega, alpha};
     dd->P0 = OpPar{beta, omega * omega, 0.0};
     const double* f[4] = {lambda, mu, rho, gamma};
-    dd->mg = build_slab_mg(g, f, P, *opt, nranks, agg_n2, &dd->comm);
+    try {
+      dd->mg = build_slab_mg(g, f, P, *opt, nranks, agg_n2, &dd->comm);
+    } catch (...) {
+      dd->comm.fail();  // peers' barriers throw; no teardown barrier pairs with theirs
+      throw;
+    }
     *out = dd.release();
   });
 }
@@ -1658,6 +1709,8 @@ int64_t ehmg_dist_exchanged_bytes(ehmg_dist d) { return d ? d->mg->exchanged_byt
 int ehmg_dist_solve(ehmg_dist d, const double* b, double* x, const ehmg_krylov_options* opt,
                     ehmg_krylov_result* res, double* history, int history_cap) {
   return guard([&] {
+    check_krylov_args(opt, res);
+    if (!d) throw Err(EHMG_EINVAL, "fgmres: null distributed handle");
     ehmg_slab_mg_s& mg = *d->mg;
     const int q = d->comm.rank;
     SlabLevel& me = d->me();
@@ -1856,10 +1909,10 @@ int ehmg_fgmres_solve(ehmg_op A, ehmg_mg M, const double* b, double* x, int wher
                       const ehmg_krylov_options* opt, ehmg_krylov_result* res, double* history,
                       int history_cap) {
   return guard([&] {
+    check_krylov_args(opt, res);
+    if (!A) throw Err(EHMG_EINVAL, "fgmres: null operator");
     const int64_t n = A->g.ndofs;
     if (M && M->L[0]->g.ndofs != n) throw Err(EHMG_EINVAL, "fgmres: operator/preconditioner size mismatch");
-    if (opt->orthogonalization != 0 && opt->orthogonalization != 1)
-      throw Err(EHMG_EINVAL, "krylov: unknown orthogonalization");
     cudaStream_t s = M ? M->s : A->s;
     // keep the operator on the solver stream
     const cplx* db;

@@ -45,7 +45,9 @@ class _MgOpts(C.Structure):
     _fields_ = [("n_levels", C.c_int), ("cycle", C.c_int), ("nu1", C.c_int), ("nu2", C.c_int),
                 ("damping", C.c_double), ("vanka_mode", C.c_int), ("sweep", C.c_int),
                 ("k_inner_iterations", C.c_int), ("k_inner_rtol", C.c_double),
-                ("precision", C.c_int)]
+                ("precision", C.c_int), ("coarse", C.c_int), ("lu_dof_budget", C.c_int64),
+                ("kz_sweeps_per_apply", C.c_int), ("kz_damping", C.c_double), ("kz_rtol", C.c_double),
+                ("kz_max_iterations", C.c_int), ("kz_restart", C.c_int)]
 
 
 class _MOpts(C.Structure):
@@ -178,6 +180,10 @@ def _ptr(a, n: int, writable: bool = False):
         import torch
         if a.dtype != torch.complex128 or not a.is_contiguous() or a.numel() != n:
             raise ValueError("device field must be a contiguous complex128 tensor of n_dofs")
+        # the library runs on its own non-blocking streams: whatever torch
+        # still has queued on this tensor must land first (ehmg_b200.h,
+        # "Ordering of EHMG_DEVICE buffers")
+        torch.cuda.current_stream(a.device).synchronize()
         return C.c_void_p(a.data_ptr()), DEVICE
     if not isinstance(a, np.ndarray) or a.dtype != np.complex128 or not a.flags.c_contiguous:
         raise ValueError("host field must be a C-contiguous complex128 numpy array")
@@ -528,9 +534,30 @@ class MgOptions:
     damping: float = 0.75
     vanka_mode: str = ECONOMIC
     sweep: str = LEXICOGRAPHIC
-    coarse: str = "lu"
+    # multigrid.hpp:22/:40-50. "automatic" and "lu" take the exact coarsest
+    # solve; "kaczmarz" is rejected by the library
+    coarse: str = "automatic"
+    lu_dof_budget: int = 4_000_000
+    kz_sweeps_per_apply: int = 5
+    kz_damping: float = 0.8
+    kz_rtol: float = 0.01
+    kz_max_iterations: int = 150
+    kz_restart: int = 40
     k_inner_iterations: int = 2
     k_inner_rtol: float = 0.25
+
+
+_COARSE = {"automatic": 0, "lu": 1, "kaczmarz": 2}
+
+
+def _mg_opts(opt: "MgOptions", precision: str) -> _MgOpts:
+    if opt.coarse not in _COARSE:
+        raise ValueError(f"config: unknown coarse solver '{opt.coarse}'")
+    return _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
+                   0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
+                   opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0,
+                   _COARSE[opt.coarse], int(opt.lu_dof_budget), opt.kz_sweeps_per_apply,
+                   opt.kz_damping, opt.kz_rtol, opt.kz_max_iterations, opt.kz_restart)
 
 
 @dataclasses.dataclass
@@ -563,14 +590,10 @@ class Multigrid:
         self.precision = precision
         if opt.cycle not in _CYCLES:
             raise ValueError(f"config: unknown cycle '{opt.cycle}'")
-        if opt.coarse not in ("lu", "automatic"):
-            raise ValueError("only the exact coarsest solve (lu) runs on the B200 path")
         if par.periodic:
             raise ValueError("periodic hierarchies are LFA-probe only (out of scope)")
         self.grid, self.par, self.opt = grid, par, opt
-        o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
-                    0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
-                    opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0)
+        o = _mg_opts(opt, precision)
         arrs = media.arrays(grid)
         h = C.c_void_p()
         _check(lib().ehmg_multigrid_create(grid.ndim, _dims_arr(grid.dims), grid.h,
@@ -697,9 +720,7 @@ class SlabMultigrid:
                  opt: MgOptions, nslabs: int, agg_n2: int = 64, precision: str = "double"):
         if precision not in ("double", "mixed"):
             raise ValueError(f"config: unknown precision '{precision}'")
-        o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
-                    0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
-                    opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0)
+        o = _mg_opts(opt, precision)
         arrs = media.arrays(grid)
         h = C.c_void_p()
         _check(lib().ehmg_slab_multigrid_create(grid.ndim, _dims_arr(grid.dims), grid.h,
@@ -745,9 +766,7 @@ class DistributedSlabSolver:
                  precision: str = "double"):
         if precision not in ("double", "mixed"):
             raise ValueError(f"config: unknown precision '{precision}'")
-        o = _MgOpts(opt.n_levels, _CYCLES[opt.cycle], opt.nu1, opt.nu2, opt.damping,
-                    0 if opt.vanka_mode == FULL else 1, 1 if opt.sweep == RED_BLACK else 0,
-                    opt.k_inner_iterations, opt.k_inner_rtol, 1 if precision == "mixed" else 0)
+        o = _mg_opts(opt, precision)
         arrs = media.arrays(grid)
         h = C.c_void_p()
         _check(lib().ehmg_dist_create(job.encode(), rank, nranks, device, grid.ndim,
@@ -826,6 +845,10 @@ class KrylovOptions:
     orthogonalization: str = "classical"
 
     def __post_init__(self):
+        if self.restart < 1:
+            raise ValueError("fgmres: restart must be >= 1")
+        if self.max_iterations < 0:
+            raise ValueError("fgmres: max_iterations must be >= 0")
         if self.orthogonalization not in _ORTH:
             raise ValueError(f"krylov: unknown orthogonalization '{self.orthogonalization}'")
 
