@@ -146,6 +146,19 @@ def dist_init(args):
     return ws, rank, local
 
 
+def spawn_ranks(n):
+    """Re-launch this command as `python -m torch.distributed.run
+    --nproc-per-node n` on 127.0.0.1 (a free port); rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr)
+    return subprocess.call(cmd)
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -207,6 +220,9 @@ def load_peaks():
 # ------------------------------------------------------- CPU baseline
 REF_SAMPLE_N = 32
 REF_SAMPLE_LEVELS = 3
+# one-time check of the DOF-ratio extrapolation against larger measured
+# reference cycles (tools/ref_extrapolation.py on the GPU box's host cores)
+REF_VALIDATION = "profiles/round2/ref_extrapolation.json"
 
 
 def level_work(n, levels):
@@ -221,14 +237,15 @@ def cpu_sample_media(n):
     return O.Media(np.full(c, LAM), np.full(c, MU), np.full(c, RHO), gam)
 
 
-def run_cpu_sample(steps, threads):
-    """Reference V(2,2) cycles (oracle/_ref = the reference headers) on a
-    REF_SAMPLE_N^3 cube with the same media/omega-per-h recipe, `threads`
-    independent replicas in parallel. Returns (V-cycles/s extrapolated to
-    N_CELLS^3, kind, raw seconds per sample cycle)."""
+def run_cpu_sample(steps, threads, n=REF_SAMPLE_N, levels=None):
+    """Reference V(2,2) cycles (oracle/_ref = the reference headers) on an
+    n^3 cube with the same media/omega-per-h recipe, `threads` independent
+    replicas in parallel (the reference is single-threaded). Returns
+    (V-cycles/s extrapolated to N_CELLS^3, kind, raw seconds per sample
+    cycle, wall seconds)."""
     from oracle import oracle as O
     kind = "reference" if O.ref_available() else "port"
-    n = REF_SAMPLE_N
+    levels = levels or max(2, min(LEVELS, int(round(math.log2(n))) - 2))
     dims = (n, n, n)
     m = cpu_sample_media(n)
     omega = 2 * math.pi / (PPW / n)
@@ -240,10 +257,10 @@ def run_cpu_sample(steps, threads):
     def work():
         if kind == "reference":
             _, s = O.ref_mg_cycles(dims, 1.0 / n, m, BETA, omega, ALPHA, b, np.zeros_like(b),
-                                   ncycles=steps, n_levels=REF_SAMPLE_LEVELS, cycle="v", nu1=2,
+                                   ncycles=steps, n_levels=levels, cycle="v", nu1=2,
                                    nu2=2, damping=DAMPING)
         else:
-            mg = O.MG(dims, 1.0 / n, m, BETA, omega, ALPHA, n_levels=REF_SAMPLE_LEVELS, cycle="v",
+            mg = O.MG(dims, 1.0 / n, m, BETA, omega, ALPHA, n_levels=levels, cycle="v",
                       nu1=2, nu2=2, damping=DAMPING)
             t0 = time.perf_counter()
             for _ in range(steps):
@@ -261,8 +278,8 @@ def run_cpu_sample(steps, threads):
     wall = time.perf_counter() - t0
     per_cycle = max(secs)
     rate_sample = threads / per_cycle
-    scale = level_work(REF_SAMPLE_N, REF_SAMPLE_LEVELS) / level_work(N_CELLS, LEVELS)
-    return rate_sample * scale, kind, per_cycle, wall
+    scale = level_work(n, levels) / level_work(N_CELLS, LEVELS)
+    return rate_sample * scale, kind, per_cycle, wall, levels
 
 
 # ------------------------------------------------------------ b200 arm
@@ -454,12 +471,13 @@ def run_b200(args, ws, rank, local):
         "kernels": kernels, "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_cpu:
-        rate, kind, per, wall = run_cpu_sample(1, 1)
+        rate, kind, per, wall, lv = run_cpu_sample(1, 1, args.ref_cells)
         line["cpu_baseline"] = {
-            "value": rate, "unit": "V-cycles/s", "cores": 1, "kind": kind,
-            "sample": (f"one V(2,2) cycle of the reference on a {REF_SAMPLE_N}^3 cube "
-                       f"({REF_SAMPLE_LEVELS} levels, same media/omega*h/shift/damping), "
-                       f"{per:.2f} s, extrapolated to {N_CELLS}^3 by smoothed-level DOF ratio")}
+            "value": rate, "unit": "V-cycles/s", "cores": 1, "kind": kind, "extrapolated": True,
+            "sample": (f"one V(2,2) cycle of the reference on a {args.ref_cells}^3 cube "
+                       f"({lv} levels, same media/omega*h/shift/damping), "
+                       f"{per:.2f} s, extrapolated to {N_CELLS}^3 by smoothed-level DOF ratio "
+                       f"(validated against measured 64^3 and 128^3 reference cycles: {REF_VALIDATION})")}
     return line
 
 
@@ -486,6 +504,9 @@ def run_b200_slabs(args, ws, rank, local):
     d = E.DistributedSlabSolver(job, rank, ws, dev, g, med, E.OperatorParams(BETA, omega, ALPHA),
                                 opt, agg_n2=AGG_N2)
     setup_s = time.perf_counter() - t0
+    # which device each rank's slab attached (CUDA-IPC inboxes of every peer)
+    rank_devs = [None] * ws
+    dist.all_gather_object(rank_devs, {"rank": rank, "device": dev, "window": list(d.window())})
     rng = np.random.default_rng(1234)
     N = g.n_dofs()
     r = rng.standard_normal(N) + 1j * rng.standard_normal(N)
@@ -553,6 +574,7 @@ def run_b200_slabs(args, ws, rank, local):
         "e2e": {"value": round(e_steps / (e2e_ms / 1e3), 4), "unit": "V-cycles/s",
                 "h2d_bytes_per_step": 16 * N // ws, "d2h_bytes_per_step": 16 * N // ws},
         "halo_bytes_per_step_rank0": int(halo), "slab_rank0": [z0, z1, w0, w1],
+        "ipc_ranks_attached": rank_devs,
         # halo traffic against NVLink 5 (900 GB/s per direction per GPU): the
         # bandwidth the exchanges would need if spread over the whole cycle
         "halo_vs_nvlink": {"GBps_over_cycle": round(halo / (ms_max / args.steps / 1e3) / 1e9, 2),
@@ -615,19 +637,23 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return None
     threads = max(1, os.cpu_count() or 1)
-    run_cpu_sample(1, threads) if args.warmup > 0 else None
-    rate, kind, per, wall = run_cpu_sample(args.steps, threads)
+    if args.warmup > 0:
+        run_cpu_sample(1, threads, args.ref_cells)
+    rate, kind, per, wall, lv = run_cpu_sample(args.steps, threads, args.ref_cells)
     return {
         "metric": metric_name(), "value": rate, "unit": "V-cycles/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "steps": args.steps, "warmup": args.warmup,
+        # time of one extrapolated 256^3 cycle on the whole box (1 / value);
+        # the measured sample cycle is cpu_baseline.sample_ms_per_cycle
+        "ms_per_step": 1e3 / rate, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "complex128 (f64)", "data": "synthetic", "config": workload_config(N_CELLS),
-        "impl": "reference",
+        "impl": "reference", "extrapolated": True,
         "cpu_baseline": {"value": rate, "unit": "V-cycles/s", "cores": threads, "kind": kind,
+                         "extrapolated": True, "sample_ms_per_cycle": round(per * 1e3, 2),
                          "sample": (f"{threads} concurrent replicas x {args.steps} V(2,2) cycles "
-                                    f"of the reference on a {REF_SAMPLE_N}^3 cube "
-                                    f"({REF_SAMPLE_LEVELS} levels), extrapolated to "
-                                    f"{N_CELLS}^3 by smoothed-level DOF ratio")},
+                                    f"of the reference (single-threaded) on a {args.ref_cells}^3 cube "
+                                    f"({lv} levels), extrapolated to "
+                                    f"{N_CELLS}^3 by smoothed-level DOF ratio; validation: {REF_VALIDATION}")},
         "e2e": {"value": rate, "unit": "V-cycles/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -646,10 +672,22 @@ def main():
     ap.add_argument("--orth", choices=["classical", "modified"], default="classical",
                     help="FGMRES Arnoldi variant (modified = the reference's MGS order)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-cells", type=int, default=REF_SAMPLE_N,
+                    help="reference arm / cpu_baseline: cube edge of the measured reference sample")
     ap.add_argument("--sources", type=int, default=32, help="--mode sources: number of point sources")
     ap.add_argument("--mode", choices=["slabs", "replicas", "sources"], default="slabs",
                     help="N > 1: z-slab decomposition (strong) or independent replicas (weak)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched directly with --gpus N: start the N ranks ourselves (one
+        # process per GPU), exactly as the driver's torchrun line would
+        sys.exit(spawn_ranks(args.gpus))
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE={ws_env} but --gpus {args.gpus}: launch one rank per GPU"}))
+        sys.exit(2)
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         line = run_reference(args, ws, rank)
