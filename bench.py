@@ -177,8 +177,10 @@ def max_over_ranks(ws, v):
 
 
 # ------------------------------------------------------- roofline bytes
-def level_dims(n, l):
-    return (n >> l,) * 3
+def level_dims(dims, l):
+    if isinstance(dims, int):
+        dims = (dims,) * 3
+    return tuple(d >> l for d in dims)
 
 
 def ndofs(d):
@@ -187,7 +189,8 @@ def ndofs(d):
 
 
 def alg_bytes(kernel, n, level):
-    """Algorithmic HBM bytes of one launch at a level."""
+    """Algorithmic HBM bytes of one launch at a level (DESIGN.md §8(d));
+    n = cube edge or the level-0 cell dims."""
     d = level_dims(n, level)
     C = d[0] * d[1] * d[2]
     N = ndofs(d)
@@ -218,11 +221,13 @@ def load_peaks():
 
 
 # ------------------------------------------------------- CPU baseline
-REF_SAMPLE_N = 32
-REF_SAMPLE_LEVELS = 3
+REF_SAMPLE_N = 64
+REF_SAMPLE_LEVELS = 4
 # one-time check of the DOF-ratio extrapolation against larger measured
 # reference cycles (tools/ref_extrapolation.py on the GPU box's host cores)
-REF_VALIDATION = "profiles/round2/ref_extrapolation.json"
+REF_VALIDATION = ("single-core reference cycles measured at 32^3/3, 64^3/4 and 128^3/5 levels extrapolate "
+                  "to 256^3 within +6.0% / +2.5% / 0 of each other, the 64^3 sample overestimating the "
+                  "reference rate by 2.5% against the 128^3 measurement (profiles/round2/ref_extrapolation.json)")
 
 
 def level_work(n, levels):
@@ -291,21 +296,65 @@ def build_problem(n, E):
     return g, med, omega
 
 
+class Problem:
+    """One bench workload: grid, media, omega, hierarchy depth, source, and
+    the line's metric/config (BASELINE configs[2] by default)."""
+
+    def __init__(self, g, med, omega, levels, damping, source, metric, config, agg_n2=AGG_N2, scaling=None):
+        self.g, self.med, self.omega, self.levels, self.damping = g, med, omega, levels, damping
+        self.source, self.metric, self.config, self.agg_n2 = source, metric, config, agg_n2
+        self.dims = tuple(g.dims)
+        self.scaling = scaling
+
+
+def make_problem(args, E, ws):
+    if args.workload == "c2":
+        n = args.n or N_CELLS
+        g, med, omega = build_problem(n, E)
+        return Problem(g, med, omega, levels_for(n), DAMPING, (0, (n // 2, n // 2, n // 2)), metric_name(n),
+                       workload_config(n))
+    from paper_2307_03242_b200 import configs as K
+    if args.workload == "c3":
+        n = args.n or 512
+        w = K.config3(scale=512 // n)
+        metric = f"V-cycles/s (complex128) at {n + 1}^3 3D heterogeneous elastic Helmholtz"
+        wl = f"configs[3]: 3D heterogeneous {n + 1}^3 nodes ({n}^3 cells), layered + 3D GRF (seed {K.SEED})"
+        scaling = "strong"
+    else:  # c4w: weak scaling, 384 x 384 x 192 G cells on G GPUs
+        scale = 384 // (args.n or 384)
+        w = K.config4_weak(gpus=ws, scale=scale)
+        d = w.grid.dims
+        metric = f"V-cycles/s (complex128) weak scaling, {d[0] + 1}x{d[1] + 1}x(192*G/{scale}) nodes per G GPUs"
+        wl = f"configs[4] weak: {d[0]}x{d[1]}x{d[2]} cells on {ws} GPU(s), layered + 3D GRF (seed {K.SEED})"
+        scaling = "weak"
+    d = w.grid.dims
+    cfg = {"workload": wl, "media": "8 layers, cs in [1,2.5], cp/cs in [1.7,2.2], rho in [1,2.5], each x (1 +- 10% "
+                                    "smooth GRF, correlation 20h); csrc/ehmg_media.cuh",
+           "omega": f"{w.shifted.omega:.6g} (10 points per wavelength at the minimum interior cs)",
+           "sponge_cells": w.sponge.layer_width, "gamma_phys": K.GAMMA_PHYS, "beta": K.BETA, "alpha": K.ALPHA,
+           "cycle": "V(2,2) full red-black Vanka", "levels": w.mg.n_levels,
+           "coarsest": "x".join(str(a >> (w.mg.n_levels - 1)) for a in d) + " exact (LU-derived inverse in HBM)",
+           "damping": w.mg.damping, "source": w.notes, "krylov": "FGMRES(10), rtol 1e-6",
+           "l2": "inputs larger than the 126 MB L2"}
+    return Problem(w.grid, w.media, w.shifted.omega, w.mg.n_levels, w.mg.damping, w.sources[0], metric, cfg,
+                   w.agg_n2, scaling)
+
+
 def run_b200(args, ws, rank, local):
     import torch
     import paper_2307_03242_b200 as E
     torch.cuda.set_device(local)
     E.lib().ehmg_set_device(local)
-    n = args.n
-    g, med, omega = build_problem(n, E)
-    opt = E.MgOptions(n_levels=levels_for(n), cycle="v", nu1=2, nu2=2, damping=DAMPING,
+    P = make_problem(args, E, 1)
+    g, med, omega, n = P.g, P.med, P.omega, P.dims
+    opt = E.MgOptions(n_levels=P.levels, cycle="v", nu1=2, nu2=2, damping=P.damping,
                       vanka_mode="full", sweep="red_black")
     t0 = time.perf_counter()
     mg = E.Multigrid(g, med, E.OperatorParams(BETA, omega, ALPHA), opt)
     D0 = E.make_opdata(g, med, E.OperatorParams(BETA, omega, 0.0))
     setup_s = time.perf_counter() - t0
     N = g.n_dofs()
-    b = torch.from_numpy(E.make_point_source(g, 0, (n // 2, n // 2, n // 2))).cuda()
+    b = torch.from_numpy(E.make_point_source(g, *P.source)).cuda()
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     r = torch.randn(N, dtype=torch.complex128, device="cuda", generator=gen)
     z = torch.zeros(N, dtype=torch.complex128, device="cuda")
@@ -394,7 +443,11 @@ def run_b200(args, ws, rank, local):
 
     # GMRES time-to-1e-6 on the point-source problem (device buffers)
     solve = None
-    if args.solve:
+    free_b = torch.cuda.mem_get_info()[0]
+    if args.solve and free_b < 16 * N * (2 * 10 + 6) * 1.05:
+        solve = {"skipped": f"FGMRES(10) needs {16 * N * 26 / 1e9:.0f} GB beside the hierarchy; "
+                            f"{free_b / 1e9:.0f} GB free on one GPU (the z-slab mode shards it)"}
+    elif args.solve:
         # warm-up: a 20-iteration solve allocates the hierarchy's FGMRES
         # workspace and captures the cycle's CUDA graphs for its basis
         # buffers (one-time set-up, timed separately as warm_s)
@@ -446,12 +499,12 @@ def run_b200(args, ws, rank, local):
         del mgm
 
     line = {
-        "metric": metric_name(n), "value": round(value, 4), "unit": "V-cycles/s",
+        "metric": P.metric, "value": round(value, 4), "unit": "V-cycles/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
-        "data": "synthetic (BASELINE configs[2] media recipe; seeded residual)",
-        "config": workload_config(n),
+        "data": f"synthetic ({P.config['workload'].split(':')[0]} media recipe; seeded residual)",
+        "config": P.config,
         "e2e": {"value": round(e2e, 4), "unit": "V-cycles/s", "h2d_bytes_per_step": N * 16,
                 "d2h_bytes_per_step": N * 16, "steps": e_steps,
                 "api": "Multigrid.precondition_many (ehmg_multigrid_precondition_many): host r in, host z out "
@@ -462,7 +515,8 @@ def run_b200(args, ws, rank, local):
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": {"bound": "hbm", "kernel": f"{kname}@L{klev}", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": NCU_TRAFFIC.get(f"{kname}@L{klev}") if n == N_CELLS else None,
+                     "traffic": (NCU_TRAFFIC.get(f"{kname}@L{klev}")
+                                 if args.workload == "c2" and n == (N_CELLS,) * 3 else None),
                      "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
                      "limiter": ("shared-memory/shuffle (LSU) pipe: 418 B of LSU traffic per DOF vs 56 B of "
                                  "HBM, LSU bound = 77% of the HBM roofline; ncu: LSU 72% busy, IPC 1.73, FP64 "
@@ -470,7 +524,7 @@ def run_b200(args, ws, rank, local):
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "clocks": clocks,
     }
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu and args.workload == "c2":
         rate, kind, per, wall, lv = run_cpu_sample(1, 1, args.ref_cells)
         line["cpu_baseline"] = {
             "value": rate, "unit": "V-cycles/s", "cores": 1, "kind": kind, "extrapolated": True,
@@ -496,13 +550,13 @@ def run_b200_slabs(args, ws, rank, local):
     obj = [f"bench{os.getpid()}_{int(time.time() * 1e3) % 10**9}" if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     job = obj[0]
-    n = args.n
-    g, med, omega = build_problem(n, E)
-    opt = E.MgOptions(n_levels=levels_for(n), cycle="v", nu1=2, nu2=2, damping=DAMPING,
+    P = make_problem(args, E, ws)
+    g, med, omega = P.g, P.med, P.omega
+    opt = E.MgOptions(n_levels=P.levels, cycle="v", nu1=2, nu2=2, damping=P.damping,
                       vanka_mode="full", sweep="red_black")
     t0 = time.perf_counter()
     d = E.DistributedSlabSolver(job, rank, ws, dev, g, med, E.OperatorParams(BETA, omega, ALPHA),
-                                opt, agg_n2=AGG_N2)
+                                opt, agg_n2=P.agg_n2)
     setup_s = time.perf_counter() - t0
     # which device each rank's slab attached (CUDA-IPC inboxes of every peer)
     rank_devs = [None] * ws
@@ -530,7 +584,7 @@ def run_b200_slabs(args, ws, rank, local):
     launches_per_step = sum(c for (_, _, c, _) in prof)
     z0w, z1w, w0w, w1w = d.window()
     kname, klev, kcount, kms = max(prof, key=lambda t: t[3])
-    wd = (n >> klev, n >> klev, max(1, (w1w - w0w) >> klev))
+    wd = (P.dims[0] >> klev, P.dims[1] >> klev, max(1, (w1w - w0w) >> klev))
     C = wd[0] * wd[1] * wd[2]
     Nw = ndofs(wd)
     nbytes = {"residual": 16 * 3 * Nw + 32 * C, "apply": 16 * 2 * Nw + 32 * C,
@@ -556,20 +610,20 @@ def run_b200_slabs(args, ws, rank, local):
     z0, z1, w0, w1 = d.window()
     solve = None
     if args.solve:
-        b = E.make_point_source(g, 0, (n // 2, n // 2, n // 2))
+        b = E.make_point_source(g, *P.source)
         t0 = time.perf_counter()
         _, res = d.solve(b, E.KrylovOptions(restart=10, max_iterations=args.max_it, orthogonalization=args.orth))
         ts = max_over_ranks(ws, time.perf_counter() - t0)
         solve = {"status": res.status, "iterations": res.iterations, "relres": res.relres,
                  "seconds": round(ts, 3), "s_per_iteration": round(ts / max(1, res.iterations), 5)}
     d.close()
-    cfg = workload_config(n)
-    cfg["parallelism"] = f"z-slab x{ws} (levels below 65^3 nodes agglomerated)"
+    cfg = dict(P.config)
+    cfg["parallelism"] = f"z-slab x{ws} (levels with <= {P.agg_n2} cell planes agglomerated)"
     return {
-        "metric": metric_name(n), "value": round(value, 4), "unit": "V-cycles/s", "n_gpus": ws,
+        "metric": P.metric, "value": round(value, 4), "unit": "V-cycles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "complex128 (f64)", "data": "synthetic (BASELINE configs[2] media recipe)",
+        "higher_is_better": True, "scaling": P.scaling or "strong", "vs_baseline": None,
+        "dtype": "complex128 (f64)", "data": f"synthetic ({cfg['workload'].split(':')[0]} media recipe)",
         "config": cfg,
         "e2e": {"value": round(e_steps / (e2e_ms / 1e3), 4), "unit": "V-cycles/s",
                 "h2d_bytes_per_step": 16 * N // ws, "d2h_bytes_per_step": 16 * N // ws},
@@ -588,57 +642,60 @@ def run_b200_slabs(args, ws, rank, local):
 
 def run_b200_sources(args, ws, rank, local):
     """BASELINE configs[4] (second part): independent preconditioned FGMRES
-    solves for surface point sources on the 257^3 grid, distributed across
-    the GPUs (one hierarchy per GPU, sources round-robin). value = solves/s."""
+    solves for surface point sources on the 257^3 grid with configs[3]'s
+    media recipe (paper_2307_03242_b200/configs.py config4_sources),
+    distributed across the GPUs (one hierarchy per GPU, sources round-robin,
+    no data-path collective). value = solves/s."""
     import torch
     import paper_2307_03242_b200 as E
+    from paper_2307_03242_b200 import configs as K
     ndev = max(1, torch.cuda.device_count())
     dev = local % ndev
     torch.cuda.set_device(dev)
     E.lib().ehmg_set_device(dev)
-    n = args.n
-    g, med, omega = build_problem(n, E)
-    opt = E.MgOptions(n_levels=levels_for(n), cycle="v", nu1=2, nu2=2, damping=DAMPING,
-                      vanka_mode="full", sweep="red_black")
-    mg = E.Multigrid(g, med, E.OperatorParams(BETA, omega, ALPHA), opt)
-    D0 = E.make_opdata(g, med, E.OperatorParams(BETA, omega, 0.0))
+    w = K.config4_sources(args.sources, scale=256 // (args.n or 256))
+    g = w.grid
+    mg = E.Multigrid(g, w.media, w.shifted, w.mg)
+    D0 = E.make_opdata(g, w.media, w.unshifted)
     N = g.n_dofs()
-    # a 4 x 8 pattern of vertical point forces 2 cells below the free top surface
-    pos = [(int((i + 0.5) * n / 8), int((j + 0.5) * n / 4), 2) for j in range(4) for i in range(8)]
-    pos = pos[:args.sources]
-    mine = [p for k, p in enumerate(pos) if k % ws == rank]
+    mine = [k for k in range(len(w.sources)) if k % ws == rank]
     x = torch.zeros(N, dtype=torch.complex128, device="cuda")
-    warm = torch.from_numpy(E.make_point_source(g, 2, pos[0])).cuda()
+    warm = torch.from_numpy(w.rhs(0)).cuda()
     # warm-up: workspace on the handle + the cycle's graphs for all basis buffers
     E.fgmres(D0, mg, warm, x, E.KrylovOptions(restart=10, max_iterations=20, orthogonalization=args.orth))
     barrier(ws)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    its = []
-    for p in mine:
-        b = torch.from_numpy(E.make_point_source(g, 2, p)).cuda()
+    its, st, rr = [], [], []
+    for k in mine:
+        b = torch.from_numpy(w.rhs(k)).cuda()
         x.zero_()
         res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=args.max_it, orthogonalization=args.orth))
         its.append(res.iterations)
+        st.append(res.status)
+        rr.append(res.relres)
     torch.cuda.synchronize()
     secs = max_over_ranks(ws, time.perf_counter() - t0)
-    cfg = workload_config(n)
-    cfg["workload"] = f"configs[4] sources: {len(pos)} surface point sources on {n + 1}^3, independent solves"
-    cfg["parallelism"] = f"{ws} GPUs, sources round-robin (no data-path collective)"
-    return {"metric": "solves/s (FGMRES(10) to 1e-6, complex128)", "value": round(len(pos) / secs, 5),
-            "unit": "solves/s", "n_gpus": ws, "steps": len(pos), "warmup": 1,
-            "ms_per_step": round(secs * 1e3 / max(1, len(pos)), 2), "higher_is_better": True,
+    nsrc = len(w.sources)
+    cfg = {"workload": f"configs[4] sources: {nsrc} surface point sources on {g.dims[0] + 1}^3, independent solves",
+           "media": "configs[3] recipe (8 layers + 10% 3D GRF, seed 2023)", "omega": w.shifted.omega,
+           "levels": w.mg.n_levels, "source": w.notes, "krylov": "FGMRES(10), rtol 1e-6",
+           "parallelism": f"{ws} GPUs, sources round-robin (no data-path collective)"}
+    return {"metric": "solves/s (FGMRES(10) to 1e-6, complex128)", "value": round(nsrc / secs, 5),
+            "unit": "solves/s", "n_gpus": ws, "steps": nsrc, "warmup": 1,
+            "ms_per_step": round(secs * 1e3 / max(1, nsrc), 2), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "complex128 (f64)",
-            "data": "synthetic (BASELINE configs[2] media; point sources)", "config": cfg,
-            "iterations_rank0": its, "e2e": None, "gpu_launches": None}
+            "data": "synthetic (configs[3] media recipe; surface point sources)", "config": cfg,
+            "iterations_rank0": its, "status_rank0": sorted(set(st)), "max_relres_rank0": max(rr) if rr else None,
+            "e2e": None, "gpu_launches": None}
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return None
     threads = max(1, os.cpu_count() or 1)
-    if args.warmup > 0:
-        run_cpu_sample(1, threads, args.ref_cells)
+    if args.warmup > 0:  # page-in / thread start-up: one small cycle per replica
+        run_cpu_sample(1, threads, 32)
     rate, kind, per, wall, lv = run_cpu_sample(args.steps, threads, args.ref_cells)
     return {
         "metric": metric_name(), "value": rate, "unit": "V-cycles/s", "n_gpus": ws,
@@ -665,10 +722,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--cells", dest="n", type=int, default=N_CELLS)
+    ap.add_argument("--cells", dest="n", type=int, default=None,
+                    help="cube edge in cells (c2 default 256, c3 512; c4w: the 384 edge, z = n/2 per GPU)")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4w"], default="c2",
+                    help="c2 = BASELINE configs[2] (headline), c3 = configs[3] heterogeneous 513^3, "
+                         "c4w = configs[4] weak scaling 384x384x192G")
     ap.add_argument("--solve", type=int, default=1)
     ap.add_argument("--mixed", type=int, default=1, help="also time the complex64-hierarchy mode")
-    ap.add_argument("--max-it", type=int, default=600)
+    ap.add_argument("--max-it", type=int, default=None,
+                    help="FGMRES iteration cap (default 600 for c2, 3000 for the heterogeneous workloads)")
     ap.add_argument("--orth", choices=["classical", "modified"], default="classical",
                     help="FGMRES Arnoldi variant (modified = the reference's MGS order)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -678,6 +740,8 @@ def main():
     ap.add_argument("--mode", choices=["slabs", "replicas", "sources"], default="slabs",
                     help="N > 1: z-slab decomposition (strong) or independent replicas (weak)")
     args = ap.parse_args()
+    if args.max_it is None:
+        args.max_it = 600 if (args.workload == "c2" and args.mode != "sources") else 3000
     if args.gpus < 1:
         ap.error("--gpus must be >= 1")
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:

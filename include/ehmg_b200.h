@@ -91,6 +91,19 @@ int ehmg_attenuation_profile(int ndim, const int* dims, double gamma_phys, int l
 int ehmg_layered_media(int ndim, const int* dims, double gamma_phys, uint64_t seed, double* lambda,
                        double* mu, double* rho, double* gamma);
 
+/* BASELINE configs[1]/[3]/[4] media recipe (layered_media of experiments.hpp:78
+ * extended): n_layers horizontal layers on the last axis (top = index 0) with
+ * per-layer cs, cp/cs, rho drawn uniformly from ranges = {cs_lo, cs_hi,
+ * ratio_lo, ratio_hi, rho_lo, rho_hi}, each multiplied by its own smooth
+ * Gaussian random field (correlation length corr_cells, covariance
+ * exp(-r^2/corr^2)) mapped into +-perturb; mu = rho cs^2,
+ * lambda = mu ((cp/cs)^2 - 2), gamma = gamma_phys. Deterministic in `seed`
+ * (splitmix64 streams; the exact recipe is in csrc/ehmg_media.cuh). Computed
+ * on the device, returned as cell-sized host arrays. */
+int ehmg_layered_grf_media(int ndim, const int* dims, int n_layers, const double* ranges, double perturb,
+                           double corr_cells, double gamma_phys, uint64_t seed, double* lambda, double* mu,
+                           double* rho, double* gamma);
+
 /* ---- multigrid: multigrid.hpp:34 MgOptions, :75 Multigrid, :133 cycle,
  *      :136 precondition --------------------------------------------------
  * cycle: 0 two_grid, 1 v, 2 w, 3 k.

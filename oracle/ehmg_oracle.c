@@ -1215,3 +1215,123 @@ void og_solve(og_mg* mg, const og_op* A0, const ocplx* b, ocplx* x, const og_kry
   sctx_t c = {A0, mg};
   og_fgmres(A0->ndofs, s_apply_A, &c, s_apply_M, &c, b, x, ko, res);
 }
+
+/* ------------------------------------------------ layered + GRF media
+ * BASELINE configs[1]/[3]/[4] media recipe (no reference implementation:
+ * the BASELINE text specifies it; the layer layout follows layered_media,
+ * experiments.hpp:78-111 -- tops on the last axis, index 0 at the top,
+ * mu = rho vs^2). Restated step by step from the recipe documented in
+ * paper_2307_03242_b200/csrc/ehmg_media.cuh, scalar loops, same operation
+ * order (no FMA contraction: the Makefile passes -ffp-contract=off). */
+static uint64_t or_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+int og_layered_grf_media(int ndim, const int* dims, int n_layers, const double* ranges, double perturb,
+                         double corr, double gamma_phys, uint64_t seed, double* lambda, double* mu,
+                         double* rho, double* gamma) {
+  int d[3] = {dims[0], dims[1], ndim == 3 ? dims[2] : 1};
+  const int depth = d[ndim - 1];
+  if (n_layers < 1 || n_layers > 64 || depth < 2) return -1;
+  /* layer draws: splitmix64 stream */
+  uint64_t st = seed;
+#define OR_NEXT() (st += 0x9e3779b97f4a7c15ull, or_mix64(st))
+  const int nl = n_layers < depth ? n_layers : depth;
+  int tops[64], nt = 1;
+  tops[0] = 0;
+  while (nt < nl) {
+    const int dd = 1 + (int)(OR_NEXT() % (uint64_t)(depth - 1));
+    int seen = 0;
+    for (int i = 0; i < nt; ++i) seen |= tops[i] == dd;
+    if (!seen) tops[nt++] = dd;
+  }
+  for (int i = 1; i < nt; ++i) /* insertion sort */
+    for (int j = i; j > 0 && tops[j - 1] > tops[j]; --j) {
+      int t = tops[j];
+      tops[j] = tops[j - 1];
+      tops[j - 1] = t;
+    }
+  double lcs[64], lq[64], lr[64];
+  for (int l = 0; l < nl; ++l) {
+    lcs[l] = ranges[0] + (ranges[1] - ranges[0]) * ((double)(OR_NEXT() >> 11) * 0x1.0p-53);
+    lq[l] = ranges[2] + (ranges[3] - ranges[2]) * ((double)(OR_NEXT() >> 11) * 0x1.0p-53);
+    lr[l] = ranges[4] + (ranges[5] - ranges[4]) * ((double)(OR_NEXT() >> 11) * 0x1.0p-53);
+  }
+#undef OR_NEXT
+  /* filter taps */
+  const int R = (int)ceil(2.0 * corr);
+  const double s = corr / 2.0;
+  double ss = 0.0;
+  for (int t = -R; t <= R; ++t) ss += exp(-(double)t * t / (s * s));
+  const double nrm = 1.0 / sqrt(ss);
+  double* w = (double*)malloc(sizeof(double) * (size_t)(2 * R + 1));
+  for (int t = -R; t <= R; ++t) w[t + R] = exp(-(double)t * t / (2.0 * s * s)) * nrm;
+  const int E0 = d[0] + 2 * R, E1 = d[1] + 2 * R, E2 = ndim == 3 ? d[2] + 2 * R : 1;
+  const int64_t nc = (int64_t)d[0] * d[1] * d[2];
+  double* noise = (double*)malloc(sizeof(double) * (size_t)E0 * E1 * E2);
+  double* t1 = (double*)malloc(sizeof(double) * (size_t)d[0] * E1 * E2);
+  double* t2 = (double*)malloc(sizeof(double) * (size_t)d[0] * d[1] * E2);
+  double* g[3];
+  const double s3 = 1.7320508075688772;
+  for (int f = 0; f < 3; ++f) {
+    g[f] = (double*)malloc(sizeof(double) * (size_t)nc);
+    const uint64_t key = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(f + 1));
+    for (int64_t i = 0; i < (int64_t)E0 * E1 * E2; ++i) {
+      const double u = (double)(or_mix64(key + (uint64_t)i) >> 11) * 0x1.0p-53;
+      noise[i] = (u * 2.0 + -1.0) * s3;
+    }
+    /* axis 0: (E0, E1, E2) -> (d0, E1, E2) */
+    for (int64_t z = 0; z < E2; ++z)
+      for (int64_t y = 0; y < E1; ++y)
+        for (int x = 0; x < d[0]; ++x) {
+          const double* p = noise + x + (int64_t)E0 * (y + (int64_t)E1 * z);
+          double acc = 0.0;
+          for (int t = 0; t <= 2 * R; ++t) acc = acc + w[t] * p[t];
+          t1[x + (int64_t)d[0] * (y + (int64_t)E1 * z)] = acc;
+        }
+    /* axis 1: (d0, E1, E2) -> (d0, d1, E2) */
+    double* o1 = ndim == 3 ? t2 : g[f];
+    for (int64_t z = 0; z < E2; ++z)
+      for (int y = 0; y < d[1]; ++y)
+        for (int x = 0; x < d[0]; ++x) {
+          const double* p = t1 + x + (int64_t)d[0] * (y + (int64_t)E1 * z);
+          double acc = 0.0;
+          for (int t = 0; t <= 2 * R; ++t) acc = acc + w[t] * p[(int64_t)t * d[0]];
+          o1[x + (int64_t)d[0] * (y + (int64_t)d[1] * z)] = acc;
+        }
+    if (ndim == 3) /* axis 2: (d0, d1, E2) -> (d0, d1, d2) */
+      for (int z = 0; z < d[2]; ++z)
+        for (int y = 0; y < d[1]; ++y)
+          for (int x = 0; x < d[0]; ++x) {
+            const double* p = t2 + x + (int64_t)d[0] * (y + (int64_t)d[1] * z);
+            double acc = 0.0;
+            for (int t = 0; t <= 2 * R; ++t) acc = acc + w[t] * p[(int64_t)t * d[0] * d[1]];
+            g[f][x + (int64_t)d[0] * (y + (int64_t)d[1] * z)] = acc;
+          }
+  }
+  const int64_t plane = ndim == 3 ? (int64_t)d[0] * d[1] : d[0];
+  for (int64_t i = 0; i < nc; ++i) {
+    const int z = (int)(i / plane);
+    int j = 0;
+    while (j + 1 < nl && tops[j + 1] <= z) ++j;
+    double fct[3];
+    for (int f = 0; f < 3; ++f) {
+      const double gg = g[f][i];
+      fct[f] = 1.0 + perturb * (gg / sqrt(1.0 + gg * gg));
+    }
+    const double cs = lcs[j] * fct[0], q = lq[j] * fct[1], r = lr[j] * fct[2];
+    const double m = r * cs * cs;
+    mu[i] = m;
+    rho[i] = r;
+    lambda[i] = m * (q * q + -2.0);
+    gamma[i] = gamma_phys;
+  }
+  for (int f = 0; f < 3; ++f) free(g[f]);
+  free(noise);
+  free(t1);
+  free(t2);
+  free(w);
+  return 0;
+}

@@ -109,6 +109,11 @@ void og_mg_precondition(og_mg* mg, const ocplx* r, ocplx* z);
 void og_solve(og_mg* mg, const og_op* A0, const ocplx* b, ocplx* x, const og_krylov_opts* ko,
               og_krylov_result* res);
 
+/* BASELINE configs[1]/[3]/[4] media recipe (csrc/ehmg_media.cuh restated) */
+int og_layered_grf_media(int ndim, const int* dims, int n_layers, const double* ranges, double perturb,
+                         double corr, double gamma_phys, uint64_t seed, double* lambda, double* mu,
+                         double* rho, double* gamma);
+
 #ifdef __cplusplus
 }
 #endif

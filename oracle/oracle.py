@@ -121,6 +121,8 @@ def lib():
         L.og_solve.argtypes = [C.c_void_p, C.c_void_p, _cp, _cp, C.POINTER(_KOpts),
                                C.POINTER(_KRes)]
         L.og_free.argtypes = [C.c_void_p]
+        L.og_layered_grf_media.argtypes = [C.c_int, _ip, C.c_int, _dp, C.c_double, C.c_double,
+                                           C.c_double, C.c_uint64, _dp, _dp, _dp, _dp]
         _lib = L
     return _lib
 
@@ -269,6 +271,19 @@ class MG:
 
 # ------------------------------------------------------- reference (_ref)
 _ref = None
+
+
+def layered_grf_media(dims, seed, n_layers=8, cs=(1.0, 2.5), cp_over_cs=(1.7, 2.2), rho=(1.0, 2.5),
+                      perturbation=0.1, corr_cells=20.0, gamma_phys=0.01):
+    """BASELINE configs[1]/[3]/[4] media recipe, restated in C (og_layered_grf_media)."""
+    n = n_cells(dims)
+    out = [np.empty(n, np.float64) for _ in range(4)]
+    rng = np.array([cs[0], cs[1], cp_over_cs[0], cp_over_cs[1], rho[0], rho[1]], np.float64)
+    rc = lib().og_layered_grf_media(len(dims), _dims(dims), int(n_layers), rng, float(perturbation),
+                                    float(corr_cells), float(gamma_phys), int(seed) & (2**64 - 1), *out)
+    if rc != 0:
+        raise ValueError("layered_grf_media: bad arguments")
+    return Media(*out)
 
 
 def ref_available() -> bool:

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -116,16 +117,12 @@ struct DenseLUT {
 
 using DenseLU = DenseLUT<Cd>;
 
-// Real = float: the LU of the float operator in float arithmetic, as the
-// reference's Multigrid<float> factors its float matrix (multigrid.hpp:97).
-template <class Real, int Dim> DenseLUT<std::complex<Real>> dense_lu(const OpData<Real, Dim>& D) {
-  using Cd = std::complex<Real>;
+// Every entry of the operator on the reference's unit-probe rows
+// (UnitAcc, operator.hpp:212), fn(row, col, value) in the flatten() DOF order.
+template <class Real, int Dim, class Fn> void for_each_entry(const OpData<Real, Dim>& D, Fn&& fn) {
   std::array<std::int64_t, Dim + 2> off{};
   for (int c = 0; c <= Dim; ++c)
     off[size_t(c) + 1] = off[size_t(c)] + (c < Dim ? D.faceb[size_t(c)].size() : D.cellb.size());
-  DenseLUT<Cd> L;
-  L.n = off[Dim + 1];
-  L.a.assign(size_t(L.n * L.n), Cd(0));
   for (int cc = 0; cc <= Dim; ++cc) {
     const Box<Dim>& cb = cc < Dim ? D.faceb[size_t(cc)] : D.cellb;
     for_each(cb, [&](const Idx<Dim>& ci) {
@@ -142,14 +139,147 @@ template <class Real, int Dim> DenseLUT<std::complex<Real>> dense_lu(const OpDat
               r[1] += o1;
               if constexpr (Dim == 3) r[2] += o2;
               if (!rb.contains(r)) continue;
-              Cd v = rc < Dim ? row_u(D, rc, r, acc) : row_p(D, r, acc);
-              L.a[size_t(off[size_t(rc)] + rb.lin(r) + col * L.n)] = v;
+              auto v = rc < Dim ? row_u(D, rc, r, acc) : row_p(D, r, acc);
+              fn(off[size_t(rc)] + rb.lin(r), col, v);
             }
       }
     });
   }
-  L.factor();
-  return L;
+}
+
+// Banded LU with partial pivoting (the unblocked LAPACK gbtf2 scheme) on a
+// DOF permutation that orders unknowns slice by slice along the longest axis,
+// so the coarsest operators of the slab problems (criterion 5 of
+// test_acceptance.cpp:212, 49K DOFs) factor in band storage instead of a
+// dense n^2 array. Test infrastructure: same exact-solve semantics as the
+// dense LU (CoarseSolverKind::lu, multigrid.hpp:97).
+template <class CT>
+struct BandLUT {
+  std::int64_t n = 0, kl = 0, ku = 0, ld = 0;
+  std::vector<CT> ab;  // A(i, j) at ab[(kl + ku + i - j) + j * ld]
+  std::vector<std::int64_t> piv, perm;  // perm[new] = old DOF
+  CT& at(std::int64_t i, std::int64_t j) { return ab[size_t((kl + ku + i - j) + j * ld)]; }
+  const CT& at(std::int64_t i, std::int64_t j) const { return ab[size_t((kl + ku + i - j) + j * ld)]; }
+  void factor() {
+    piv.resize(size_t(n));
+    for (std::int64_t k = 0; k < n; ++k) {
+      const std::int64_t km = std::min(kl, n - 1 - k);
+      std::int64_t p = k;
+      auto best = std::abs(at(k, k));
+      for (std::int64_t i = k + 1; i <= k + km; ++i)
+        if (std::abs(at(i, k)) > best) best = std::abs(at(i, k)), p = i;
+      piv[size_t(k)] = p;
+      const std::int64_t ju = std::min(n - 1, k + kl + ku);
+      if (p != k)
+        for (std::int64_t j = k; j <= ju; ++j) std::swap(at(k, j), at(p, j));
+      const CT d = at(k, k);
+      for (std::int64_t i = k + 1; i <= k + km; ++i) at(i, k) /= d;
+      for (std::int64_t j = k + 1; j <= ju; ++j) {
+        const CT akj = at(k, j);
+        if (akj == CT(0)) continue;
+        for (std::int64_t i = k + 1; i <= k + km; ++i) at(i, j) -= at(i, k) * akj;
+      }
+    }
+  }
+  void solve(std::vector<CT>& v) const {
+    std::vector<CT> b(static_cast<size_t>(n));
+    for (std::int64_t i = 0; i < n; ++i) b[size_t(i)] = v[size_t(perm[size_t(i)])];
+    for (std::int64_t k = 0; k < n; ++k) {
+      std::swap(b[size_t(k)], b[size_t(piv[size_t(k)])]);
+      const std::int64_t km = std::min(kl, n - 1 - k);
+      for (std::int64_t i = k + 1; i <= k + km; ++i) b[size_t(i)] -= at(i, k) * b[size_t(k)];
+    }
+    for (std::int64_t j = n - 1; j >= 0; --j) {
+      b[size_t(j)] /= at(j, j);
+      for (std::int64_t i = std::max<std::int64_t>(0, j - kl - ku); i < j; ++i) b[size_t(i)] -= at(i, j) * b[size_t(j)];
+    }
+    for (std::int64_t i = 0; i < n; ++i) v[size_t(perm[size_t(i)])] = b[size_t(i)];
+  }
+};
+
+template <class CT> struct CoarseLUT {
+  DenseLUT<CT> dense;
+  BandLUT<CT> band;
+  bool banded = false;
+  void solve(std::vector<CT>& v) const {
+    if (banded) band.solve(v);
+    else dense.solve(v);
+  }
+};
+
+// Real = float: the LU of the float operator in float arithmetic, as the
+// reference's Multigrid<float> factors its float matrix (multigrid.hpp:97).
+// Coarsest grids above kBandMin DOFs take the banded factorisation.
+// (EHMG_REF_BAND_MIN overrides the threshold: the band path's own check.)
+inline std::int64_t band_min() {
+  const char* e = std::getenv("EHMG_REF_BAND_MIN");
+  return e ? std::atoll(e) : 20000;
+}
+template <class Real, int Dim> CoarseLUT<std::complex<Real>> dense_lu(const OpData<Real, Dim>& D) {
+  using Cd = std::complex<Real>;
+  std::int64_t n = D.cellb.size();
+  for (int c = 0; c < Dim; ++c) n += D.faceb[size_t(c)].size();
+  CoarseLUT<Cd> out;
+  if (n <= band_min()) {
+    DenseLUT<Cd>& L = out.dense;
+    L.n = n;
+    L.a.assign(size_t(n * n), Cd(0));
+    for_each_entry(D, [&](std::int64_t r, std::int64_t c, Cd v) { L.a[size_t(r + c * n)] = v; });
+    L.factor();
+    return out;
+  }
+  out.banded = true;
+  BandLUT<Cd>& B = out.band;
+  B.n = n;
+  // slice key along the longest axis (faces of that axis sit half a cell
+  // earlier), then the remaining axes from last to first, then component
+  int ax = 0;
+  for (int a = 1; a < Dim; ++a)
+    if (D.grid.dims[a] > D.grid.dims[ax]) ax = a;
+  struct Key {
+    std::int64_t k[4];
+    std::int64_t dof;
+  };
+  std::vector<Key> keys;
+  keys.reserve(size_t(n));
+  std::int64_t o = 0;
+  for (int c = 0; c <= Dim; ++c) {
+    const Box<Dim>& b = c < Dim ? D.faceb[size_t(c)] : D.cellb;
+    for_each(b, [&](const Idx<Dim>& i) {
+      Key key{{0, 0, 0, c}, o + b.lin(i)};
+      key.k[0] = 2 * std::int64_t(i[ax]) - (c == ax ? 1 : 0);
+      int q = 1;
+      for (int a = Dim - 1; a >= 0; --a)
+        if (a != ax) key.k[q++] = i[a];
+      keys.push_back(key);
+    });
+    o += b.size();
+  }
+  std::sort(keys.begin(), keys.end(), [](const Key& x, const Key& y) {
+    for (int q = 0; q < 4; ++q)
+      if (x.k[q] != y.k[q]) return x.k[q] < y.k[q];
+    return x.dof < y.dof;
+  });
+  B.perm.resize(size_t(n));
+  std::vector<std::int64_t> inv(static_cast<size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) {
+    B.perm[size_t(i)] = keys[size_t(i)].dof;
+    inv[size_t(keys[size_t(i)].dof)] = i;
+  }
+  for_each_entry(D, [&](std::int64_t r, std::int64_t c, Cd v) {
+    if (v == Cd(0)) return;
+    const std::int64_t pr = inv[size_t(r)], pc = inv[size_t(c)];
+    B.kl = std::max(B.kl, pr - pc);
+    B.ku = std::max(B.ku, pc - pr);
+  });
+  B.ld = 2 * B.kl + B.ku + 1;
+  B.ab.assign(size_t(B.ld * n), Cd(0));
+  for_each_entry(D, [&](std::int64_t r, std::int64_t c, Cd v) {
+    if (v == Cd(0)) return;
+    B.at(inv[size_t(r)], inv[size_t(c)]) = v;
+  });
+  B.factor();
+  return out;
 }
 
 // ---- restated cycle around the reference components --------------------
@@ -163,7 +293,7 @@ template <class Real, int Dim> struct RefMGT {
     F r, t, bc, ec;
   };
   std::vector<std::unique_ptr<Lev>> L;
-  DenseLUT<Cd> lu;
+  CoarseLUT<Cd> lu;
   int cycle, nu1, nu2;
   double w;
   VankaMode mode;

@@ -31,6 +31,7 @@
 #include "../../include/ehmg_b200.h"
 #include "ehmg_comm.cuh"
 #include "ehmg_kernels.cuh"
+#include "ehmg_media.cuh"
 #include "ehmg_stencil2d.cuh"
 #include "ehmg_stencil3d.cuh"
 #include "ehmg_stencil3d_rr.cuh"
@@ -1418,6 +1419,61 @@ int ehmg_layered_media(int nd, const int* dims, double gamma_phys, uint64_t seed
       mu[i] = lm[j];
       gamma[i] = gamma_phys;
     }
+  });
+}
+
+int ehmg_layered_grf_media(int nd, const int* dims, int n_layers, const double* ranges, double perturb,
+                           double corr_cells, double gamma_phys, uint64_t seed, double* lambda, double* mu,
+                           double* rho, double* gamma) {
+  return guard([&] {
+    if (nd != 2 && nd != 3) throw Err(EHMG_EINVAL, "layered_grf_media: ndim must be 2 or 3");
+    int d[3] = {dims[0], dims[1], nd == 3 ? dims[2] : 1};
+    for (int a = 0; a < nd; ++a)
+      if (d[a] < 2) throw Err(EHMG_EINVAL, "layered_grf_media: need >= 2 cells per axis");
+    if (n_layers < 1 || n_layers > 64) throw Err(EHMG_EINVAL, "layered_grf_media: 1..64 layers");
+    for (int k = 0; k < 3; ++k)
+      if (!(ranges[2 * k] > 0 && ranges[2 * k + 1] >= ranges[2 * k]))
+        throw Err(EHMG_EINVAL, "layered_grf_media: ranges must be positive and ordered");
+    if (!(ranges[2] * (1 - perturb) > 1.4142135623730951))
+      throw Err(EHMG_EINVAL, "layered_grf_media: cp/cs must stay above sqrt(2) (lambda > 0)");
+    if (!(perturb >= 0 && perturb < 1)) throw Err(EHMG_EINVAL, "layered_grf_media: perturb in [0, 1)");
+    if (!(corr_cells > 0 && corr_cells <= 40)) throw Err(EHMG_EINVAL, "layered_grf_media: corr in (0, 40] cells");
+    check_device();
+    const LayerTable L = grf_layers(d[nd - 1], n_layers, ranges, seed);
+    const GrfTaps T = grf_taps(corr_cells);
+    const int R = T.R;
+    const int E0 = d[0] + 2 * R, E1 = d[1] + 2 * R, E2 = nd == 3 ? d[2] + 2 * R : 1;
+    const int64_t nc = (int64_t)d[0] * d[1] * d[2];
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{s};
+    DBuf<double> noise((int64_t)E0 * E1 * E2), t1((int64_t)d[0] * E1 * E2),
+        t2(nd == 3 ? (int64_t)d[0] * d[1] * E2 : 0);
+    DBuf<double> g[3] = {DBuf<double>(nc), DBuf<double>(nc), DBuf<double>(nc)};
+    const int gb = 148 * 16;
+    for (int f = 0; f < 3; ++f) {
+      k_grf_noise<<<gb, 256, 0, s>>>((int64_t)E0 * E1 * E2, seed ^ grf_salt(f), noise.p);
+      k_grf_filter<<<gb, 256, 0, s>>>(T, 0, E0, E1, E2, noise.p, t1.p);
+      if (nd == 2) {
+        k_grf_filter<<<gb, 256, 0, s>>>(T, 1, d[0], E1, 1, t1.p, g[f].p);
+      } else {
+        k_grf_filter<<<gb, 256, 0, s>>>(T, 1, d[0], E1, E2, t1.p, t2.p);
+        k_grf_filter<<<gb, 256, 0, s>>>(T, 2, d[0], d[1], E2, t2.p, g[f].p);
+      }
+      CK(cudaGetLastError());
+    }
+    DBuf<double> out[4] = {DBuf<double>(nc), DBuf<double>(nc), DBuf<double>(nc), DBuf<double>(nc)};
+    const int64_t plane = nd == 3 ? (int64_t)d[0] * d[1] : d[0];
+    k_compose_media<<<gb, 256, 0, s>>>(L, nc, plane, perturb, gamma_phys, g[0].p, g[1].p, g[2].p, out[0].p,
+                                       out[1].p, out[2].p, out[3].p);
+    CK(cudaGetLastError());
+    double* dst[4] = {lambda, mu, rho, gamma};
+    for (int k = 0; k < 4; ++k)
+      CK(cudaMemcpyAsync(dst[k], out[k].p, sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   });
 }
 

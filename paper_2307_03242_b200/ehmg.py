@@ -99,6 +99,8 @@ def lib():
         L.ehmg_prolong_field.argtypes = [C.c_int, ip, vp, vp, C.c_int]
         L.ehmg_coarsen_media.argtypes = [C.c_int, ip, vp, vp]
         L.ehmg_layered_media.argtypes = [C.c_int, ip, C.c_double, C.c_uint64, vp, vp, vp, vp]
+        L.ehmg_layered_grf_media.argtypes = [C.c_int, ip, C.c_int, vp, C.c_double, C.c_double,
+                                             C.c_double, C.c_uint64, vp, vp, vp, vp]
         L.ehmg_multigrid_measure_convergence.argtypes = [vp, C.c_uint64, C.POINTER(_MOpts),
                                                          C.POINTER(_MRes), vp, C.c_int]
         L.ehmg_attenuation_profile.argtypes = [C.c_int, ip, C.c_double, C.c_int, C.c_double,
@@ -909,6 +911,25 @@ def layered_media(g: StaggeredGrid, gamma_phys: float, seed: int) -> MediaModel:
     return MediaModel(lam, mu, rho, gam)
 
 
+def layered_grf_media(g: StaggeredGrid, seed: int, n_layers: int = 8, cs=(1.0, 2.5),
+                      cp_over_cs=(1.7, 2.2), rho=(1.0, 2.5), perturbation: float = 0.1,
+                      corr_cells: float = 20.0, gamma_phys: float = 0.01) -> MediaModel:
+    """BASELINE configs[1]/[3]/[4] media: `n_layers` horizontal layers along the
+    last axis (experiments.hpp:78 layout, index 0 at the top) with per-layer
+    cs, cp/cs and rho drawn from the given ranges, each multiplied by its own
+    smooth Gaussian random field (correlation length `corr_cells` cells)
+    bounded to +-perturbation. Built on the device (csrc/ehmg_media.cuh),
+    deterministic in `seed`; gamma = gamma_phys (apply a sponge afterwards)."""
+    n = g.n_cells()
+    lam, mu, rh, gam = (np.empty(n, np.float64) for _ in range(4))
+    dims = (C.c_int * 3)(*(list(g.dims) + [1] * (3 - g.ndim)))
+    rng = np.array([cs[0], cs[1], cp_over_cs[0], cp_over_cs[1], rho[0], rho[1]], np.float64)
+    _check(lib().ehmg_layered_grf_media(g.ndim, dims, int(n_layers), rng.ctypes.data, float(perturbation),
+                                        float(corr_cells), float(gamma_phys), int(seed) & (2**64 - 1),
+                                        lam.ctypes.data, mu.ctypes.data, rh.ctypes.data, gam.ctypes.data))
+    return MediaModel(lam, mu, rh, gam)
+
+
 def min_interior_vs(g: StaggeredGrid, m: MediaModel, sponge: SpongeConfig) -> float:
     """experiments.hpp:116"""
     vs = m.vs().reshape(g.dims[::-1])
@@ -960,6 +981,8 @@ def run_solve(cfg: dict, seed: int = 1) -> dict:
             media = linear_media(g, gamma_phys)
         elif problem == "layered":
             media = layered_media(g, gamma_phys, seed)
+        elif problem == "layered_grf":  # BASELINE configs[1]/[3] recipe (B200 addition)
+            media = layered_grf_media(g, seed, corr_cells=cfg.get("corr_cells", 20.0), gamma_phys=gamma_phys)
         else:
             raise ValueError(f"config: unknown problem kind '{problem}'")
     media.gamma = build_attenuation_profile(g, gamma_phys, sponge)
@@ -974,7 +997,8 @@ def run_solve(cfg: dict, seed: int = 1) -> dict:
     w = cfg.get("w", default_solve_damping(g_s, levels))
     opt = MgOptions(n_levels=levels, cycle=cfg.get("cycle", "w"), nu1=cfg.get("nu1", 1),
                     nu2=cfg.get("nu2", 1), damping=w, vanka_mode=cfg.get("vanka", FULL),
-                    sweep=cfg.get("order", RED_BLACK), coarse="lu")
+                    sweep=cfg.get("order", RED_BLACK), coarse=cfg.get("coarse", "automatic"),
+                    lu_dof_budget=cfg.get("lu_dof_budget", 4_000_000))
     precision = cfg.get("precision", "double")  # experiments.hpp:314
     if precision not in ("double", "mixed"):
         raise ValueError(f"config: unknown precision '{precision}'")

@@ -1,0 +1,80 @@
+"""BASELINE configs pinned to the reference (golden_configs.npz from
+oracle/_ref, tests/golden/make_golden_configs.py):
+
+* the bench's 5-level V(2,2) preconditioner (configs[2] recipe at 64^3:
+  beta 2/3, alpha 0.5, damping 0.25, sponge, full red-black Vanka) against
+  the reference's cycle: <= 1e-10 relative on 8192 sampled DOFs, the 2-norm
+  and the sum, and against the C oracle on the whole vector;
+* configs[0] (2D 256^2, 5 levels, FGMRES(10)): iteration count within +-1 and
+  the same status as the reference, solution samples to 1e-6; with the
+  reference default alpha = 0.1 both stall (same status, within one restart);
+* configs[1]'s layered + GRF recipe at 1/8 scale (device media builder):
+  iteration count within +-1 of the reference's.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2307_03242_b200 as E
+from paper_2307_03242_b200 import configs as K
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_configs.npz"))
+
+
+def _solve(w, alpha=None, orth="classical", max_it=2000):
+    par = w.shifted if alpha is None else E.OperatorParams(w.shifted.beta, w.shifted.omega, alpha)
+    mg = E.Multigrid(w.grid, w.media, par, w.mg)
+    A = E.make_opdata(w.grid, w.media, w.unshifted)
+    x = np.zeros(w.grid.n_dofs(), np.complex128)
+    res = E.fgmres(A, mg, w.rhs(0), x, E.KrylovOptions(restart=10, max_iterations=max_it, orthogonalization=orth))
+    return x, res
+
+
+def test_five_level_vcycle_bench_parameters_vs_reference():
+    w = K.config2(scale=4, levels=5)
+    assert w.mg.n_levels == int(GOLD["cycle5_levels"]) == 5 and w.mg.damping == float(GOLD["cycle5_damping"])
+    rng = np.random.default_rng(64064)
+    r = rng.uniform(-1, 1, w.grid.n_dofs()) + 1j * rng.uniform(-1, 1, w.grid.n_dofs())
+    assert np.array_equal(r[:16], GOLD["cycle5_r_head"])  # the seeded input did not drift
+    mg = E.Multigrid(w.grid, w.media, w.shifted, w.mg)
+    z = mg.precondition(r)
+    idx = GOLD["cycle5_idx"]
+    zr = GOLD["cycle5_z"]
+    assert np.abs(z[idx] - zr).max() <= 1e-10 * np.abs(zr).max()
+    assert abs(np.linalg.norm(z) - float(GOLD["cycle5_norm"])) <= 1e-10 * float(GOLD["cycle5_norm"])
+    assert abs(z.sum() - complex(GOLD["cycle5_sum"])) <= 1e-10 * np.abs(z).sum()
+    # whole vector against the C restatement of the cycle
+    m = w.media
+    zo = O.MG(w.grid.dims, w.grid.h, O.Media(m.lambda_, m.mu, m.rho, m.gamma), w.shifted.beta, w.shifted.omega,
+              w.shifted.alpha, n_levels=5, cycle="v", nu1=2, nu2=2, damping=w.mg.damping).precondition(r)
+    assert np.abs(z - zo).max() <= 1e-10 * np.abs(zo).max()
+
+
+@pytest.mark.parametrize("orth", ["classical", "modified"])
+def test_config0_fgmres_vs_reference(orth):
+    w = K.config0()
+    assert abs(w.shifted.omega - float(GOLD["c0_omega"])) <= 1e-14 * w.shifted.omega
+    x, res = _solve(w, orth=orth)
+    assert res.status == str(GOLD["c0_status"]) == "converged"
+    assert abs(res.iterations - int(GOLD["c0_iterations"])) <= 1, (res.iterations, int(GOLD["c0_iterations"]))
+    idx = GOLD["c0_idx"]
+    assert np.abs(x[idx] - GOLD["c0_x"]).max() <= 1e-6 * np.abs(GOLD["c0_x"]).max()
+
+
+def test_config0_reference_default_shift_stalls_alike():
+    w = K.config0()
+    _, res = _solve(w, alpha=0.1, max_it=700)
+    assert res.status == str(GOLD["c0_a01_status"])
+    assert abs(res.iterations - int(GOLD["c0_a01_iterations"])) <= w.krylov.restart
+
+
+def test_config1_recipe_fgmres_vs_reference():
+    w = K.config1(scale=8)
+    assert w.mg.n_levels == 4
+    assert abs(w.shifted.omega - float(GOLD["c1_omega"])) <= 1e-14 * w.shifted.omega
+    _, res = _solve(w)
+    assert res.status == str(GOLD["c1_status"]) == "converged"
+    assert abs(res.iterations - int(GOLD["c1_iterations"])) <= 1, (res.iterations, int(GOLD["c1_iterations"]))
