@@ -295,6 +295,8 @@ template <class Real, int Dim> struct RefMGT {
   std::vector<std::unique_ptr<Lev>> L;
   CoarseLUT<Cd> lu;
   int cycle, nu1, nu2;
+  int k_it = 2;          // MgOptions::k_inner_iterations default (multigrid.hpp:52)
+  double k_rtol = 0.25;  // MgOptions::k_inner_rtol default
   double w;
   VankaMode mode;
   SweepOrder order;
@@ -333,8 +335,24 @@ template <class Real, int Dim> struct RefMGT {
     axpy(Cd(-1), lev.t, lev.r);
     nx.bc = restrict_field(lev.g, nx.g, lev.r, false);
     nx.ec.set_zero();
-    cyc(l + 1, nx.bc, nx.ec);
-    if (cycle == 2 && l + 2 != nl) cyc(l + 1, nx.bc, nx.ec);
+    if (cycle == 3 && l + 2 != nl) {
+      // K-cycle (multigrid.hpp:238-253): the coarse correction is an inner
+      // FGMRES on the next level (the reference's own fgmres), preconditioned
+      // by one cycle from zero
+      KrylovOptions ko;
+      ko.restart = k_it;
+      ko.max_iterations = k_it;
+      ko.rtol = k_rtol;
+      auto A = [&](const F& in, F& out) { apply_mixed_operator(nx.D, in, out); };
+      auto M = [&](const F& in, F& out) {
+        out.set_zero();
+        cyc(l + 1, in, out);
+      };
+      fgmres(A, M, nx.bc, nx.ec, ko);
+    } else {
+      cyc(l + 1, nx.bc, nx.ec);
+      if (cycle == 2 && l + 2 != nl) cyc(l + 1, nx.bc, nx.ec);
+    }
     F corr = prolong_field(lev.g, nx.g, nx.ec, false);
     axpy(Cd(1), corr, x);
     for (int s = 0; s < nu2; ++s) lev.sm.sweep(lev.D, b, x, w, order);

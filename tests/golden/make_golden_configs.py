@@ -15,7 +15,9 @@ Writes tests/golden/golden_configs.npz:
             alpha 0.5 (status, iterations, relres, sampled solution) and with
             the reference default alpha 0.1 (status, iterations: it stalls);
   c1_*      configs[1]'s layered + GRF recipe at 1/8 scale (128^2, 4 levels,
-            correlation 2.5 cells, 4-cell sponge), FGMRES(10) to 1e-6.
+            correlation 2.5 cells, 4-cell sponge), FGMRES(10) to 1e-6;
+  c3s_*     configs[3]'s 3D recipe at 1/16 scale (32^3, 3 levels, 8^3
+            coarsest, correlation 1.25 cells, 2-cell sponge), FGMRES(10).
 The media of c1 come from the C restatement of the recipe
 (oracle og_layered_grf_media), which the GPU tests pin bit for bit to the
 device builder.
@@ -48,6 +50,8 @@ def workload(which):
         return K.config0()
     if which == "c1":
         return K.config1(scale=8)
+    if which == "c3s":
+        return K.config3(scale=16, levels=3)
     return K.config2(scale=4, levels=5)
 
 
@@ -102,8 +106,10 @@ def run(job):
 
 
 if __name__ == "__main__":
-    jobs = [("cycle5", None), ("c0", None), ("c0", 0.1), ("c1", None)]
-    res = {}
+    jobs = [("cycle5", None), ("c0", None), ("c0", 0.1), ("c1", None), ("c3s", None)]
+    if len(sys.argv) > 1:  # regenerate only the named jobs, keep the others
+        jobs = [j for j in jobs if j[0] in sys.argv[1:]]
+    res = dict(np.load(OUT)) if os.path.exists(OUT) and len(sys.argv) > 1 else {}
     with ProcessPoolExecutor(len(jobs)) as ex:
         for d in ex.map(run, jobs):
             res.update(d)

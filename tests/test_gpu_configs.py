@@ -78,3 +78,11 @@ def test_config1_recipe_fgmres_vs_reference():
     _, res = _solve(w)
     assert res.status == str(GOLD["c1_status"]) == "converged"
     assert abs(res.iterations - int(GOLD["c1_iterations"])) <= 1, (res.iterations, int(GOLD["c1_iterations"]))
+
+
+def test_config3_recipe_fgmres_vs_reference():
+    w = K.config3(scale=16, levels=3)
+    assert abs(w.shifted.omega - float(GOLD["c3s_omega"])) <= 1e-14 * w.shifted.omega
+    _, res = _solve(w)
+    assert res.status == str(GOLD["c3s_status"]) == "converged"
+    assert abs(res.iterations - int(GOLD["c3s_iterations"])) <= 1, (res.iterations, int(GOLD["c3s_iterations"]))

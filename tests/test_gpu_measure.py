@@ -55,11 +55,12 @@ def test_three_level_cycles_contract(cyc):
     mg = E.Multigrid(g, med, par, E.MgOptions(n_levels=3, cycle=cyc, damping=0.55))
     res = mg.measure_convergence_factor(5)
     assert not res.diverged and res.factor < 0.9
-    if cyc != "k":  # the reference-side driver restates V/W (K needs its inner Krylov)
-        ref = O.ref_measure((32, 16), g.h, om, 2 / 3, TAU * 32 / 10, 0.3, 5, n_levels=3, cycle=cyc,
-                            damping=0.55)
-        assert res.cycles == ref["cycles"]
-        assert abs(res.factor - ref["factor"]) <= 1e-9 * ref["factor"]
+    # the reference-side driver restates V/W and the K-cycle's inner FGMRES
+    # (multigrid.hpp:238-253) around the reference's own fgmres
+    ref = O.ref_measure((32, 16), g.h, om, 2 / 3, TAU * 32 / 10, 0.3, 5, n_levels=3, cycle=cyc,
+                        damping=0.55)
+    assert res.cycles == ref["cycles"]
+    assert abs(res.factor - ref["factor"]) <= (1e-9 if cyc != "k" else 1e-7) * ref["factor"]
 
 
 @pytest.mark.parametrize("sweep", ["lexicographic", "red_black"])

@@ -203,3 +203,23 @@ def test_oracle_matches_reference_randomized():
             x = rng.uniform(-1, 1, O.n_dofs(dims)) + 1j * rng.uniform(-1, 1, O.n_dofs(dims))
             y = O.Op(dims, 0.1, m, beta, 7.0, 0.2).apply(x)
             assert rel(y, O.ref_apply(dims, 0.1, m, beta, 7.0, 0.2, x)) < 1e-14
+
+
+@pytest.mark.parametrize("dims,levels", [((32, 16), 3), ((8, 8, 8), 3)])
+def test_oracle_kcycle_equals_reference_kcycle(dims, levels):
+    """K-cycle (multigrid.hpp:238-253): the C restatement against the
+    reference's own components with the reference's fgmres as the inner
+    solve (oracle/_ref, ref_driver.cpp RefMGT::cyc)."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(31)
+    n = O.n_cells(dims)
+    m = O.Media(3 * rng.uniform(.5, 2, n), rng.uniform(.5, 2, n), rng.uniform(.5, 2, n),
+                0.05 * rng.uniform(.5, 2, n))
+    h = 1.0 / dims[0]
+    om = 2 * np.pi * dims[0] / 10
+    b = rng.uniform(-1, 1, O.n_dofs(dims)) + 1j * rng.uniform(-1, 1, O.n_dofs(dims))
+    z, _ = O.ref_mg_cycles(dims, h, m, 2 / 3, om, 0.3, b, np.zeros_like(b), ncycles=1, n_levels=levels,
+                           cycle="k", nu1=1, nu2=1, damping=0.55)
+    zo = O.MG(dims, h, m, 2 / 3, om, 0.3, n_levels=levels, cycle="k", damping=0.55).precondition(b)
+    assert np.abs(z - zo).max() <= 1e-12 * np.abs(zo).max()
