@@ -205,8 +205,8 @@ def alg_bytes(kernel, n, level):
         return 16 * N + 16 * ndofs(level_dims(n, level + 1))
     if kernel == "prolong_add":
         return 16 * ndofs(level_dims(n, level + 1)) + 2 * 16 * N
-    if kernel == "coarse_solve":
-        return 16 * N * N + 32 * N
+    if kernel == "coarse_solve":  # S^-1 GEMV over the displacement DOFs + the rhs / pressure passes
+        return 16 * Nu * Nu + 16 * (3 * N + Nu)
     return 0
 
 

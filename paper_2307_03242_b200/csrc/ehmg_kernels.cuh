@@ -754,6 +754,127 @@ __global__ void __launch_bounds__(kThreads) k_gemv_rows(int64_t N, const V* __re
   }
 }
 
+// ---- coarsest solve with the pressure eliminated ---------------------------
+// The p-row of the mixed operator has one pressure entry, its diagonal
+// 1/(lambda+mu) (operator.hpp:416 row_p), so the exact solve of
+// [Auu Aup; Apu Dpp] [u; p] = [bu; bp] is
+//   u = S^-1 (bu - Aup Dpp^-1 bp),   p = Dpp^-1 (bp - Apu u),
+//   S = Auu - Aup Dpp^-1 Apu  (the displacement Schur complement the reference
+//   forms for its Kaczmarz coarse solve, multigrid.hpp:104-123, :270-299).
+// Only S^-1 (Nu^2, 58% of the full inverse at 16^3) is applied densely; the
+// gradient (2 entries per u row) and divergence (<= 54 per p row) entries are
+// taken from the assembled matrix at set-up.
+constexpr int kSchurDiv = 64;  // max u entries of one p row
+
+// u row f: the (<= 2) nonzero p columns of A[f, Nu:N]; one warp per row
+__global__ void k_schur_extract_grad(int64_t N, int64_t Nu, const cplx* __restrict__ A, int* __restrict__ gcol,
+                                     cplx* __restrict__ gval, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t f = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; f < Nu; f += warps) {
+    const cplx* a = A + f * N + Nu;
+    int cnt = 0;
+    for (int64_t c0 = 0; c0 < N - Nu; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const cplx v = c < N - Nu ? a[c] : mk(0, 0);
+      const unsigned m = __ballot_sync(0xffffffffu, v.x != 0.0 || v.y != 0.0);
+      if (v.x != 0.0 || v.y != 0.0) {
+        const int slot = cnt + __popc(m & ((1u << lane) - 1u));
+        if (slot < 2) {
+          gcol[2 * f + slot] = (int)c;
+          gval[2 * f + slot] = v;
+        } else {
+          atomicExch(err, 1);
+        }
+      }
+      cnt += __popc(m);
+    }
+    if (lane < 2 && lane >= cnt) {
+      gcol[2 * f + lane] = -1;
+      gval[2 * f + lane] = mk(0, 0);
+    }
+  }
+}
+
+// p row c: the nonzero u columns of A[Nu + c, 0:Nu] (ascending) and the
+// diagonal 1/Dpp; one warp per row
+__global__ void k_schur_extract_div(int64_t N, int64_t Nu, const cplx* __restrict__ A, int* __restrict__ dcnt,
+                                    int* __restrict__ dcol, cplx* __restrict__ dval, cplx* __restrict__ rdp,
+                                    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t Np = N - Nu;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; c < Np; c += warps) {
+    const cplx* a = A + (Nu + c) * N;
+    int cnt = 0;
+    for (int64_t j0 = 0; j0 < Nu; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const cplx v = j < Nu ? a[j] : mk(0, 0);
+      const unsigned m = __ballot_sync(0xffffffffu, v.x != 0.0 || v.y != 0.0);
+      if (v.x != 0.0 || v.y != 0.0) {
+        const int slot = cnt + __popc(m & ((1u << lane) - 1u));
+        if (slot < kSchurDiv) {
+          dcol[c * kSchurDiv + slot] = (int)j;
+          dval[c * kSchurDiv + slot] = v;
+        } else {
+          atomicExch(err, 1);
+        }
+      }
+      cnt += __popc(m);
+    }
+    // the pressure block must be diagonal (operator.hpp:419)
+    for (int64_t j0 = 0; j0 < Np; j0 += 32) {
+      const int64_t j = j0 + lane;
+      if (j < Np && j != c) {
+        const cplx v = a[Nu + j];
+        if (v.x != 0.0 || v.y != 0.0) atomicExch(err, 2);
+      }
+    }
+    if (lane == 0) {
+      dcnt[c] = cnt < kSchurDiv ? cnt : kSchurDiv;
+      rdp[c] = cdiv(mk(1, 0), a[Nu + c]);
+    }
+  }
+}
+
+// Y = Dpp^-1 Aup^T (Np x Nu, column-major, ld Np) from the column-major view
+// of the row-major A (M = A^T, ld N): Y[i, j] = M[Nu + i, j] * rdp[i]
+__global__ void k_schur_scale_rows(int64_t N, int64_t Nu, const cplx* __restrict__ A, const cplx* __restrict__ rdp,
+                                   cplx* __restrict__ Y) {
+  const int64_t Np = N - Nu;
+  GRID_STRIDE(t, Np * Nu) {
+    const int64_t i = t % Np, j = t / Np;
+    Y[t] = A[Nu + i + j * N] * rdp[i];
+  }
+}
+
+// bu'(f) = bu(f) - sum_k Aup(f, c_k) * bp(c_k) / Dpp(c_k)
+template <class V>
+__global__ void k_schur_rhs(int64_t Nu, const V* __restrict__ b, const int* __restrict__ gcol,
+                            const cplx* __restrict__ gval, const cplx* __restrict__ rdp, V* __restrict__ bu) {
+  GRID_STRIDE(f, Nu) {
+    cplx acc = wide(b[f]);
+    for (int k = 0; k < 2; ++k) {
+      const int c = gcol[2 * f + k];
+      if (c >= 0) acc -= gval[2 * f + k] * (wide(b[Nu + c]) * rdp[c]);
+    }
+    bu[f] = narrow<V>(acc);
+  }
+}
+
+// p(c) = (bp(c) - sum_j Apu(c, j) u(j)) / Dpp(c)
+template <class V>
+__global__ void k_schur_p(int64_t Nu, int64_t Np, const V* __restrict__ b, const int* __restrict__ dcnt,
+                          const int* __restrict__ dcol, const cplx* __restrict__ dval, const cplx* __restrict__ rdp,
+                          V* __restrict__ x) {
+  GRID_STRIDE(c, Np) {
+    cplx acc = wide(b[Nu + c]);
+    const int n = dcnt[c];
+    for (int k = 0; k < n; ++k) acc -= dval[c * kSchurDiv + k] * wide(x[dcol[c * kSchurDiv + k]]);
+    x[Nu + c] = narrow<V>(acc * rdp[c]);
+  }
+}
+
 // complex128 <-> complex64 copies (experiments.hpp:243 convert_field)
 template <class D, class S>
 __global__ void __launch_bounds__(kThreads) k_convert(int64_t n, const S* __restrict__ src, D* __restrict__ dst) {

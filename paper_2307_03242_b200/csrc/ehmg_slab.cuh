@@ -680,12 +680,13 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
       }
       sm->cx_of[r] = open(all[r].h[19]);
     }
-    // Row-partitioned coarsest solve: rank q keeps rows [r0, r1) of A^-1
-    // (1/n of the dense inverse, and of the per-cycle GEMV), then pushes its
-    // rows of the solution into every rank's buffer.
+    // Row-partitioned coarsest solve: rank q keeps rows [r0, r1) of S^-1
+    // (the displacement Schur complement; 1/n of the dense inverse and of the
+    // per-cycle GEMV), pushes its rows of u into every rank's buffer, and
+    // every rank then recovers the pressure locally.
     {
       ehmg_mg_s& R = *sm->rep;
-      const int64_t nco = R.nco, r0 = nco * q / comm->n, r1 = nco * (q + 1) / comm->n;
+      const int64_t ncu = R.ncu, r0 = ncu * q / comm->n, r1 = ncu * (q + 1) / comm->n;
       R.split_coarse(r0, r1, R.s);
       ehmg_slab_mg_s* smp = sm.get();
       R.coarse_gather = [smp, r0, r1](void* x, size_t es) {

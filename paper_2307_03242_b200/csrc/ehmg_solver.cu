@@ -13,6 +13,7 @@
 // sequences launches and makes the Krylov control decisions.
 
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -779,8 +780,16 @@ struct ehmg_mg_s {
   cudaStream_t s = nullptr;
   ehmg_mg_options opt;
   std::vector<std::unique_ptr<Level>> L;
-  DBuf<cplx> ainv;  // row-major inverse of the coarsest operator
-  int64_t nco = 0;
+  // Coarsest solve with the pressure eliminated (ehmg_kernels.cuh k_schur_*):
+  // ainv = row-major S^-1 of the displacement Schur complement (ncu rows),
+  // plus the gradient / divergence entries and 1/Dpp of the assembled matrix.
+  DBuf<cplx> ainv;
+  int64_t nco = 0, ncu = 0;
+  DBuf<int> s_gcol, s_dcnt, s_dcol;
+  DBuf<cplx> s_gval, s_dval, s_rdp, s_bu;
+  DBuf<cplxf> s_buf;
+  cplx* schur_scratch(const cplx*) { return s_bu.p; }
+  cplxf* schur_scratch(const cplxf*) { return s_buf.p; }
   // FGMRES workspace of solves preconditioned by this hierarchy (2m+3
   // level-0 vectors), kept between solves so the basis buffers -- and the
   // CUDA graphs of the cycle, keyed by (r, z) -- are reused; released with
@@ -794,21 +803,21 @@ struct ehmg_mg_s {
   const cplx* coarse_inv(const cplx*) const { return ainv.p; }
   const cplxf* coarse_inv(const cplxf*) const { return ainvf.p; }
   // Row-partitioned coarsest solve (one z-slab per process): this rank keeps
-  // rows [c_r0, c_r1) of A^-1, computes those rows of x and all-gathers x
+  // rows [c_r0, c_r1) of S^-1, computes those rows of u and all-gathers u
   // (coarse_gather pushes the block into every rank's x, then a barrier).
   int64_t c_r0 = 0, c_r1 = -1;
   std::function<void(void* x, size_t esize)> coarse_gather;
   void split_coarse(int64_t r0, int64_t r1, cudaStream_t st) {
     const int64_t rows = r1 - r0;
     if (prec == 0) {
-      DBuf<cplx> blk(rows * nco);
-      CK(cudaMemcpyAsync(blk.p, ainv.p + r0 * nco, sizeof(cplx) * rows * nco, cudaMemcpyDeviceToDevice, st));
+      DBuf<cplx> blk(rows * ncu);
+      CK(cudaMemcpyAsync(blk.p, ainv.p + r0 * ncu, sizeof(cplx) * rows * ncu, cudaMemcpyDeviceToDevice, st));
       CK(cudaStreamSynchronize(st));
       std::swap(ainv.p, blk.p);
       std::swap(ainv.n, blk.n);
     } else {
-      DBuf<cplxf> blk(rows * nco);
-      CK(cudaMemcpyAsync(blk.p, ainvf.p + r0 * nco, sizeof(cplxf) * rows * nco, cudaMemcpyDeviceToDevice, st));
+      DBuf<cplxf> blk(rows * ncu);
+      CK(cudaMemcpyAsync(blk.p, ainvf.p + r0 * ncu, sizeof(cplxf) * rows * ncu, cudaMemcpyDeviceToDevice, st));
       CK(cudaStreamSynchronize(st));
       std::swap(ainvf.p, blk.p);
       std::swap(ainvf.n, blk.n);
@@ -930,16 +939,22 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
   g_level = l;
   if (l + 1 == nl) {
     Prof pf("coarse_solve", s);
+    V* bu = schur_scratch(b);
+    k_schur_rhs<V><<<grid_for(ncu, 148 * 8), kThreads, 0, s>>>(ncu, b, s_gcol.p, s_gval.p, s_rdp.p, bu);
+    CK(cudaGetLastError());
     if (c_r1 < 0) {
-      k_gemv_rows<V><<<grid_for(nco * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x, nco);
+      k_gemv_rows<V><<<grid_for(ncu * 32, 148 * 64), kThreads, 0, s>>>(ncu, coarse_inv(b), bu, x, ncu);
       CK(cudaGetLastError());
     } else {
       const int64_t rows = c_r1 - c_r0;
       if (rows > 0)
-        k_gemv_rows<V><<<grid_for(rows * 32, 148 * 64), kThreads, 0, s>>>(nco, coarse_inv(b), b, x + c_r0, rows);
+        k_gemv_rows<V><<<grid_for(rows * 32, 148 * 64), kThreads, 0, s>>>(ncu, coarse_inv(b), bu, x + c_r0, rows);
       CK(cudaGetLastError());
-      coarse_gather(x, sizeof(V));
+      coarse_gather(x, sizeof(V));  // every rank holds all of u
     }
+    k_schur_p<V><<<grid_for(nco - ncu, 148 * 8), kThreads, 0, s>>>(ncu, nco - ncu, b, s_dcnt.p, s_dcol.p, s_dval.p,
+                                                                 s_rdp.p, x);
+    CK(cudaGetLastError());
     return;
   }
   Level& lev = *L[l];
@@ -1027,17 +1042,18 @@ static void check_device() {
     throw Err(EHMG_ECUDA, "no CUDA device: the B200 path has no CPU fallback");
 }
 
-// Exact coarsest solve: assemble A (row-major == A^T column-major), LU it
-// with cuSOLVER and solve against the identity, leaving A^{-1} row-major.
-static void build_coarse_inverse(const Geo& g, const OpPar& P, const Cell* m, DBuf<cplx>& ainv,
-                                 cudaStream_t s) {
-  const int64_t N = g.ndofs;
-  // The coarsest operator and its inverse are dense in HBM (2 N^2 complex
-  // during the build): allow it while that fits in 80% of free memory
-  // (N ~ 60000 on an idle B200), the reference's SparseLU budget aside.
+// Exact coarsest solve: assemble A row-major (== A^T column-major), take the
+// gradient / divergence entries and 1/Dpp, form S^T = Auu^T - Apu^T Dpp^-1
+// Aup^T in place (cuBLAS ZGEMM on the column-major view), LU it with
+// cuSOLVER and solve against the identity, leaving S^-1 row-major (ncu^2).
+static void build_coarse_inverse(const Geo& g, const OpPar& P, const Cell* m, ehmg_mg_s& mg, cudaStream_t s) {
+  const int64_t N = g.ndofs, Nu = g.off[g.nd], Np = N - Nu;
+  // The coarsest operator is dense in HBM during the build (N^2 + Np Nu +
+  // Nu^2 complex): allow it while that fits in 80% of free memory (N ~ 60000
+  // on an idle B200), the reference's SparseLU budget aside.
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
-  const double need = 2.0 * (double)N * (double)N * sizeof(cplx) + 64.0 * N * sizeof(cplx);
+  const double need = ((double)N * N + (double)Np * Nu + (double)Nu * Nu) * sizeof(cplx) + 64.0 * N * sizeof(cplx);
   if (need > 0.8 * (double)free_b)
     throw Err(EHMG_ERANGE, "assemble_sparse: coarsest grid of " + std::to_string(N) +
                                " DOFs exceeds the dense-LU memory budget");
@@ -1048,18 +1064,53 @@ static void build_coarse_inverse(const Geo& g, const OpPar& P, const Cell* m, DB
   if (g.nd == 3) k_coarse_matrix<3><<<grid_for(total, 148 * 64), kThreads, 0, s>>>(g, P, m, A.p);
   else k_coarse_matrix<2><<<grid_for(total, 148 * 64), kThreads, 0, s>>>(g, P, m, A.p);
   CK(cudaGetLastError());
-  ainv.alloc(N * N);
-  k_identity<<<grid_for(N * N, 148 * 64), kThreads, 0, s>>>(N, ainv.p);
+  mg.nco = N;
+  mg.ncu = Nu;
+  mg.s_gcol.alloc(2 * Nu);
+  mg.s_gval.alloc(2 * Nu);
+  mg.s_dcnt.alloc(Np);
+  mg.s_dcol.alloc(Np * kSchurDiv);
+  mg.s_dval.alloc(Np * kSchurDiv);
+  mg.s_rdp.alloc(Np);
+  DBuf<int> err(1);
+  err.zero(s);
+  k_schur_extract_grad<<<grid_for(Nu * 32, 148 * 32), kThreads, 0, s>>>(N, Nu, A.p, mg.s_gcol.p, mg.s_gval.p, err.p);
+  k_schur_extract_div<<<grid_for(Np * 32, 148 * 32), kThreads, 0, s>>>(N, Nu, A.p, mg.s_dcnt.p, mg.s_dcol.p,
+                                                                      mg.s_dval.p, mg.s_rdp.p, err.p);
+  CK(cudaGetLastError());
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (herr != 0) throw Err(EHMG_ERUNTIME, "multigrid: unexpected coarsest-operator structure (pressure block)");
+  {
+    DBuf<cplx> Y(Np * Nu);
+    k_schur_scale_rows<<<grid_for(Np * Nu, 148 * 64), kThreads, 0, s>>>(N, Nu, A.p, mg.s_rdp.p, Y.p);
+    CK(cudaGetLastError());
+    cublasHandle_t hb;
+    if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) throw Err(EHMG_ECUDA, "cublas: create failed");
+    cublasSetStream(hb, s);
+    const cuDoubleComplex mone = make_cuDoubleComplex(-1.0, 0.0), one = make_cuDoubleComplex(1.0, 0.0);
+    const cublasStatus_t st =
+        cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)Nu, (int)Nu, (int)Np, &mone,
+                    (const cuDoubleComplex*)(A.p + Nu * N), (int)N, (const cuDoubleComplex*)Y.p, (int)Np, &one,
+                    (cuDoubleComplex*)A.p, (int)N);
+    CK(cudaStreamSynchronize(s));
+    cublasDestroy(hb);
+    if (st != CUBLAS_STATUS_SUCCESS) throw Err(EHMG_ECUDA, "cublas: zgemm failed");
+  }
+  DBuf<cplx>& ainv = mg.ainv;
+  ainv.alloc(Nu * Nu);
+  k_identity<<<grid_for(Nu * Nu, 148 * 64), kThreads, 0, s>>>(Nu, ainv.p);
   CK(cudaGetLastError());
   cusolverDnHandle_t h;
   CKS(cusolverDnCreate(&h));
   CKS(cusolverDnSetStream(h, s));
   int lwork = 0;
-  CKS(cusolverDnZgetrf_bufferSize(h, (int)N, (int)N, (cuDoubleComplex*)A.p, (int)N, &lwork));
+  CKS(cusolverDnZgetrf_bufferSize(h, (int)Nu, (int)Nu, (cuDoubleComplex*)A.p, (int)N, &lwork));
   DBuf<cplx> work(lwork > 0 ? lwork : 1);
-  DBuf<int> ipiv(N), info(1);
-  CKS(cusolverDnZgetrf(h, (int)N, (int)N, (cuDoubleComplex*)A.p, (int)N, (cuDoubleComplex*)work.p,
-                       ipiv.p, info.p));
+  DBuf<int> ipiv(Nu), info(1);
+  CKS(cusolverDnZgetrf(h, (int)Nu, (int)Nu, (cuDoubleComplex*)A.p, (int)N, (cuDoubleComplex*)work.p, ipiv.p,
+                       info.p));
   int hinfo = 0;
   CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1067,10 +1118,11 @@ static void build_coarse_inverse(const Geo& g, const OpPar& P, const Cell* m, DB
     cusolverDnDestroy(h);
     throw Err(EHMG_ERUNTIME, "multigrid: coarsest LU factorization failed");
   }
-  CKS(cusolverDnZgetrs(h, CUBLAS_OP_N, (int)N, (int)N, (cuDoubleComplex*)A.p, (int)N, ipiv.p,
-                       (cuDoubleComplex*)ainv.p, (int)N, info.p));
+  CKS(cusolverDnZgetrs(h, CUBLAS_OP_N, (int)Nu, (int)Nu, (cuDoubleComplex*)A.p, (int)N, ipiv.p,
+                       (cuDoubleComplex*)ainv.p, (int)Nu, info.p));
   CK(cudaStreamSynchronize(s));
   cusolverDnDestroy(h);
+  mg.s_bu.alloc(Nu);
 }
 
 // Build a hierarchy of `nlevels` levels below grid g from host media (host)
@@ -1127,10 +1179,10 @@ static std::unique_ptr<ehmg_mg_s> build_mg(const Geo& g, const double* const* ho
       lev->media.soa.release();
     }
   Level& cl = *mg->L.back();
-  mg->nco = cl.g.ndofs;
-  build_coarse_inverse(cl.g, P, cl.media.packed.p, mg->ainv, s);
+  build_coarse_inverse(cl.g, P, cl.media.packed.p, *mg, s);
   if (mixed) {
-    const int64_t nn = mg->nco * mg->nco;
+    mg->s_buf.alloc(mg->ncu);
+    const int64_t nn = mg->ncu * mg->ncu;
     mg->ainvf.alloc(nn);
     k_convert<cplxf, cplx><<<grid_for(nn, 148 * 64), kThreads, 0, s>>>(nn, mg->ainv.p, mg->ainvf.p);
     CK(cudaGetLastError());

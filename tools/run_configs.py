@@ -1,15 +1,13 @@
-"""BASELINE configs[0] and configs[1] (2D) through the public API on the GPU,
-with the reference CPU cycle timed beside configs[0] (a bounded sample).
+"""BASELINE configs[0..3] through the public API on the GPU (the workloads
+pinned in paper_2307_03242_b200/configs.py), one FGMRES(10) + V(2,2) solve
+each, with the reference CPU cycle timed beside configs[0] (a bounded sample).
 
-    python tools/run_configs.py [--which 0,1] [--no-ref]
+    python tools/run_configs.py [--which 0,1,2,3] [--scale 1] [--no-ref]
 
-Synthetic inputs: configs[1]'s layered media with smooth Gaussian
-perturbations is generated here from a seed (numpy); nothing is read from a
-dataset. Prints one JSON object per config.
+Prints one JSON object per config.
 """
 import argparse
 import json
-import math
 import os
 import sys
 import time
@@ -20,55 +18,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import paper_2307_03242_b200 as E  # noqa: E402
+from paper_2307_03242_b200 import configs as K  # noqa: E402
 
 
-def grf(shape, corr, rng):
-    """smooth Gaussian random field (unit max-abs) with correlation length corr cells"""
-    w = rng.standard_normal(shape)
-    k = [np.fft.fftfreq(n) for n in shape]
-    kk = sum(np.meshgrid(*[q ** 2 for q in k], indexing="ij"))
-    f = np.real(np.fft.ifftn(np.fft.fftn(w) * np.exp(-2 * (math.pi * corr) ** 2 * kk)))
-    return f / np.abs(f).max()
-
-
-def layered_grf_media(g, nlayers, seed, gamma):
-    """configs[1]: nlayers horizontal layers, cs in [1, 2.5], cp/cs in [1.7, 2.2],
-    rho in [1, 2.5], each times (1 +- 10% smooth GRF, correlation 20h)."""
-    rng = np.random.default_rng(seed)
-    nz = g.dims[-1]
-    tops = np.sort(rng.choice(np.arange(1, nz), nlayers - 1, replace=False))
-    bounds = np.concatenate([[0], tops, [nz]])
-    cs = rng.uniform(1.0, 2.5, nlayers)
-    ratio = rng.uniform(1.7, 2.2, nlayers)
-    rho = rng.uniform(1.0, 2.5, nlayers)
-    shape = g.dims[::-1]  # (z, ..., x): axis-0-fastest storage
-    L = np.zeros(shape[0], int)
-    for i in range(nlayers):
-        L[bounds[i]:bounds[i + 1]] = i
-    sl = (slice(None),) + (None,) * (g.ndim - 1)
-    pert = [1 + 0.1 * grf(shape, 20, rng) for _ in range(3)]
-    vs = cs[L][sl] * pert[0]
-    vp = (cs * ratio)[L][sl] * pert[1]
-    dens = rho[L][sl] * pert[2]
-    mu = dens * vs ** 2
-    lam = dens * vp ** 2 - 2 * mu
-    n = g.n_cells()
-    return E.MediaModel(lam.ravel(), mu.ravel(), dens.ravel(), np.full(n, gamma))
-
-
-def solve(g, med, sponge, omega, alpha, levels, damping, src_comp, src):
-    med.gamma = E.build_attenuation_profile(g, 0.01, sponge)
-    opt = E.MgOptions(n_levels=levels, cycle="v", nu1=2, nu2=2, damping=damping, vanka_mode="full",
-                      sweep="red_black")
+def solve(w, max_it):
     t0 = time.perf_counter()
-    mg = E.Multigrid(g, med, E.OperatorParams(2 / 3, omega, alpha), opt)
-    D0 = E.make_opdata(g, med, E.OperatorParams(2 / 3, omega, 0.0))
+    mg = E.Multigrid(w.grid, w.media, w.shifted, w.mg)
+    D0 = E.make_opdata(w.grid, w.media, w.unshifted)
     setup = time.perf_counter() - t0
-    b = E.make_point_source(g, src_comp, src)
-    x = np.zeros(g.n_dofs(), np.complex128)
+    b = w.rhs(0)
+    x = np.zeros(w.grid.n_dofs(), np.complex128)
     E.fgmres(D0, mg, b, x.copy(), E.KrylovOptions(restart=10, max_iterations=5))  # warm (graphs)
     t0 = time.perf_counter()
-    res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=2000))
+    res = E.fgmres(D0, mg, b, x, E.KrylovOptions(restart=10, max_iterations=max_it))
     ts = time.perf_counter() - t0
     return {"status": res.status, "iterations": res.iterations, "relres": res.relres,
             "seconds": round(ts, 3), "setup_s": round(setup, 3)}
@@ -77,50 +39,32 @@ def solve(g, med, sponge, omega, alpha, levels, damping, src_comp, src):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="0,1")
+    ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--max-it", type=int, default=4000)
     ap.add_argument("--no-ref", action="store_true")
     a = ap.parse_args()
-    which = [int(w) for w in a.which.split(",")]
-    if 0 in which:
-        n = 256
-        g = E.StaggeredGrid((n, n), 1.0 / n)
-        med = E.MediaModel.homogeneous(g, 2.0, 1.0, 1.0, 0.01)
-        omega = 2 * math.pi / (10 * g.h)
-        out = {"config": "configs[0]: 2D homogeneous 257^2 nodes, 20-cell layer, x-source at centre, "
-                         "FGMRES(10) + V(2,2) to 17^2, damping 0.25; alpha 0.5 (the reference default "
-                         "0.1 stalls at 5 levels, reported as b200_alpha_0.1)",
-               "b200": solve(g, med, E.SpongeConfig(20), omega, 0.5, 5, 0.25, 0, (n // 2, n // 2)),
-               "b200_alpha_0.1": solve(g, E.MediaModel.homogeneous(g, 2.0, 1.0, 1.0, 0.01), E.SpongeConfig(20),
-                                       omega, 0.1, 5, 0.25, 0, (n // 2, n // 2))}
-        if not a.no_ref:
+    for i in [int(v) for v in a.which.split(",")]:
+        w = K.CONFIGS[i](scale=a.scale)
+        g = w.grid
+        out = {"config": w.name, "dims": list(g.dims), "levels": w.mg.n_levels, "omega": w.shifted.omega,
+               "alpha": w.shifted.alpha, "damping": w.mg.damping, "source": w.notes,
+               "b200": solve(w, a.max_it)}
+        if i == 0 and not a.no_ref:
             from oracle import oracle as O
-            m = O.Media(med.lambda_, med.mu, med.rho, med.gamma)
-            b = E.make_point_source(g, 0, (n // 2, n // 2))
+            m = w.media
+            b = w.rhs(0)
             ncyc = 3
-            _, secs = O.ref_mg_cycles((n, n), g.h, m, 2 / 3, omega, 0.5, b, np.zeros_like(b), ncycles=ncyc,
-                                      n_levels=5, cycle="v", nu1=2, nu2=2, damping=0.25, vanka="full",
-                                      sweep="red_black")
+            _, secs = O.ref_mg_cycles(g.dims, g.h, O.Media(m.lambda_, m.mu, m.rho, m.gamma), w.shifted.beta,
+                                      w.shifted.omega, w.shifted.alpha, b, np.zeros_like(b), ncycles=ncyc,
+                                      n_levels=w.mg.n_levels, cycle="v", nu1=2, nu2=2, damping=w.mg.damping,
+                                      vanka="full", sweep="red_black")
             per = secs / ncyc
             it = out["b200"]["iterations"]
             out["reference_cpu"] = {"v_cycle_s": round(per, 4), "cores": 1,
                                     "solve_s_extrapolated": round(per * it, 2),
                                     "sample": f"{ncyc} V(2,2) cycles of oracle/_ref at the same size; "
                                               f"x {it} iterations (cycle cost only, 1 core)"}
-        print(json.dumps(out))
-        sys.stdout.flush()
-    if 1 in which:
-        n = 1024
-        g = E.StaggeredGrid((n, n), 1.0 / n)
-        med = layered_grf_media(g, 8, 2023, 0.01)
-        sp = E.SpongeConfig(32)
-        omega = E.omega_from_gs(g, med, 10.0, sp)
-        # a vertical-displacement source: pressure-row point sources stall
-        # FGMRES with this preconditioner in the reference too (checked with
-        # oracle/_ref at 128^2), so the "point source near the top" is u1
-        out = {"config": "configs[1]: 2D heterogeneous 1025^2 nodes, 8 layers + 10% GRF (seed 2023), "
-                         "32-cell layer, 10 ppw at min cs, vertical-displacement source 4 cells below the "
-                         "top, V(2,2) to 17^2, alpha 0.5, damping 0.25",
-               "b200": solve(g, med, sp, omega, 0.5, 7, 0.25, 1, (n // 2, 4))}
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
