@@ -862,16 +862,23 @@ __global__ void k_schur_rhs(int64_t Nu, const V* __restrict__ b, const int* __re
   }
 }
 
-// p(c) = (bp(c) - sum_j Apu(c, j) u(j)) / Dpp(c)
+// p(c) = (bp(c) - sum_j Apu(c, j) u(j)) / Dpp(c); one warp per p row (the
+// <= 64 entries two per lane, reduced by shuffles in a fixed order)
 template <class V>
 __global__ void k_schur_p(int64_t Nu, int64_t Np, const V* __restrict__ b, const int* __restrict__ dcnt,
                           const int* __restrict__ dcol, const cplx* __restrict__ dval, const cplx* __restrict__ rdp,
                           V* __restrict__ x) {
-  GRID_STRIDE(c, Np) {
-    cplx acc = wide(b[Nu + c]);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; c < Np; c += warps) {
     const int n = dcnt[c];
-    for (int k = 0; k < n; ++k) acc -= dval[c * kSchurDiv + k] * wide(x[dcol[c * kSchurDiv + k]]);
-    x[Nu + c] = narrow<V>(acc * rdp[c]);
+    cplx acc = mk(0, 0);
+    for (int k = lane; k < n; k += 32) acc += dval[c * kSchurDiv + k] * wide(x[dcol[c * kSchurDiv + k]]);
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) x[Nu + c] = narrow<V>((wide(b[Nu + c]) - acc) * rdp[c]);
   }
 }
 

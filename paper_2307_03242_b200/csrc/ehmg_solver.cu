@@ -952,8 +952,8 @@ void ehmg_mg_s::cycle_t(int l, const V* b, V* x, bool xzero) {
       CK(cudaGetLastError());
       coarse_gather(x, sizeof(V));  // every rank holds all of u
     }
-    k_schur_p<V><<<grid_for(nco - ncu, 148 * 8), kThreads, 0, s>>>(ncu, nco - ncu, b, s_dcnt.p, s_dcol.p, s_dval.p,
-                                                                 s_rdp.p, x);
+    k_schur_p<V><<<grid_for((nco - ncu) * 32, 148 * 8), kThreads, 0, s>>>(ncu, nco - ncu, b, s_dcnt.p, s_dcol.p,
+                                                                        s_dval.p, s_rdp.p, x);
     CK(cudaGetLastError());
     return;
   }
