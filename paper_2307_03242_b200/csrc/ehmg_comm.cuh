@@ -35,6 +35,7 @@ struct CommShm {
   std::atomic<int> arrived;
   std::atomic<int> sense;
   std::atomic<int> attached;
+  std::atomic<long long> xseq[kCommMaxRanks];  // halo exchanges whose event record each rank has enqueued
   double red[kCommMaxRanks][kCommRedSlots];
   unsigned char blob[kCommMaxRanks][kCommBlob];
 };
@@ -92,6 +93,7 @@ struct NodeComm {
       shm = map_fd(fd);
       if (!shm) throw std::runtime_error("comm: mmap failed");
       shm->failed.store(0);
+      for (int r = 0; r < kCommMaxRanks; ++r) shm->xseq[r].store(0);
       shm->arrived.store(0);
       shm->sense.store(0);
       shm->attached.store(1);
@@ -175,6 +177,20 @@ struct NodeComm {
         if (shm->failed.load()) throw std::runtime_error("comm: a peer rank failed");
         std::this_thread::yield();
       }
+    }
+  }
+  // Enqueue-order handshake of the halo exchanges: a rank publishes that it
+  // has enqueued the event record of its exchange number `seq`; a neighbour
+  // waits for that (host spin, no GPU drain) before it makes its stream wait
+  // on the event -- the GPU streams then order the exchange among themselves.
+  void publish(long long seq) {
+    if (shm) shm->xseq[rank].store(seq, std::memory_order_release);
+  }
+  void wait_for(int r, long long seq) {
+    if (n == 1) return;
+    while (shm->xseq[r].load(std::memory_order_acquire) < seq) {
+      if (shm->failed.load()) throw std::runtime_error("comm: a peer rank failed");
+      std::this_thread::yield();
     }
   }
   // v[0..k) <- sum over ranks (rank order), identical on every rank

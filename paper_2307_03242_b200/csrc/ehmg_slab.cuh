@@ -27,6 +27,8 @@
 // tests) and the one-slab-per-process mode (NodeComm + CUDA IPC).
 #pragma once
 
+#include <cstdlib>
+
 #include "ehmg_comm.cuh"
 
 struct SlabPlan {
@@ -164,10 +166,26 @@ struct ehmg_slab_mg_s {
   // read ghost planes: pushes/pulls run on sx, the interior rows on s.
   cudaStream_t sx = nullptr;
   cudaEvent_t ev_upd = nullptr, ev_x = nullptr;
+  // One slab per process: halo exchanges ordered GPU-side through CUDA IPC
+  // events (recorded after this rank's pushes, waited on by the neighbours'
+  // copy streams) instead of a stream drain + host barrier per exchange.
+  // kXEv slots in rotation: a rank re-records slot e % kXEv only after its
+  // neighbours published exchange e + kXEv - 1, i.e. after they enqueued
+  // their waits for e. EHMG_HOST_BARRIER=1 keeps the drain + barrier.
+  static constexpr int kXEv = 4;
+  bool ev_exchange = false;
+  cudaEvent_t xev[kXEv] = {}, xev_lo[kXEv] = {}, xev_hi[kXEv] = {};
+  long long xseq = 0;
   std::vector<char> pend;  // per level: the smoothed iterate's ghosts are stale
   std::vector<int> xpar;   // per level: inbox half of the next exchange
 
   ~ehmg_slab_mg_s() {
+    if (sx) cudaStreamSynchronize(sx);
+    for (int i = 0; i < kXEv; ++i) {
+      if (xev[i]) cudaEventDestroy(xev[i]);
+      if (xev_lo[i]) cudaEventDestroy(xev_lo[i]);
+      if (xev_hi[i]) cudaEventDestroy(xev_hi[i]);
+    }
     for (void* p : mapped) cudaIpcCloseMemHandle(p);
     L.clear();
     rep.reset();
@@ -239,7 +257,25 @@ struct ehmg_slab_mg_s {
         for (int k = 0; k < 4; ++k) to_inbox(box, dn.sg, true, (const V*)X[q], me.sg, k, sx);
       }
     }
-    sync_barrier(sx);  // all pushes landed
+    if (ev_exchange) {
+      // GPU-side: the neighbours' pushes into my inboxes are ordered before my
+      // pulls by their events; the host only waits for their enqueue progress
+      const int slot = (int)(xseq % kXEv);
+      CK(cudaEventRecord(xev[slot], sx));
+      ++xseq;
+      comm->publish(xseq);
+      const int q = comm->rank;
+      if (q > 0) {
+        comm->wait_for(q - 1, xseq);
+        CK(cudaStreamWaitEvent(sx, xev_lo[slot], 0));
+      }
+      if (q + 1 < P_()) {
+        comm->wait_for(q + 1, xseq);
+        CK(cudaStreamWaitEvent(sx, xev_hi[slot], 0));
+      }
+    } else {
+      sync_barrier(sx);  // all pushes landed
+    }
     for (int q = q_lo; q < q_hi; ++q) {
       SlabLevel& me = *L[l][q];
       const V* lo = (const V*)SB<V>::in_lo(me) + par * inbox_half(me.sg, false);
@@ -645,6 +681,22 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
       CK(cudaIpcGetMemHandle(&mine.h[18], sm->L[0][q]->in_hi.p));
     }
     comm->exchange_blob(&mine, sizeof(Blob), all);
+    {
+      const char* hb = std::getenv("EHMG_HOST_BARRIER");
+      sm->ev_exchange = !(hb && hb[0] == '1');
+      struct EvBlob {
+        cudaIpcEventHandle_t e[ehmg_slab_mg_s::kXEv];
+      } emine{}, eall[kCommMaxRanks];
+      for (int i = 0; i < ehmg_slab_mg_s::kXEv; ++i) {
+        CK(cudaEventCreateWithFlags(&sm->xev[i], cudaEventDisableTiming | cudaEventInterprocess));
+        CK(cudaIpcGetEventHandle(&emine.e[i], sm->xev[i]));
+      }
+      comm->exchange_blob(&emine, sizeof(EvBlob), eall);
+      for (int i = 0; i < ehmg_slab_mg_s::kXEv; ++i) {
+        if (q > 0) CK(cudaIpcOpenEventHandle(&sm->xev_lo[i], eall[q - 1].e[i]));
+        if (q + 1 < comm->n) CK(cudaIpcOpenEventHandle(&sm->xev_hi[i], eall[q + 1].e[i]));
+      }
+    }
     sm->brep_of.clear();
     sm->brepf_of.clear();
     sm->cx_of.assign(comm->n, nullptr);

@@ -1679,6 +1679,18 @@ struct ehmg_dist_s {
   std::unique_ptr<ehmg_slab_mg_s> mg;
   OpPar P0;  // unshifted operator (alpha = 0) for the Krylov level
   ~ehmg_dist_s() {
+    // every rank drains its streams and meets the others before the IPC
+    // events and inboxes its neighbours' streams may still reference go away
+    if (mg) {
+      if (mg->s) cudaStreamSynchronize(mg->s);
+      if (mg->sx) cudaStreamSynchronize(mg->sx);
+    }
+    if (comm.shm && !comm.shm->failed.load()) {
+      try {
+        comm.barrier();
+      } catch (...) {
+      }
+    }
     mg.reset();
     comm.close();
   }

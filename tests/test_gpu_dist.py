@@ -33,7 +33,10 @@ def _problem():
     return g, med, par, opt, r, b
 
 
-def _rank(rank, ws, job, q, precision="double"):
+def _rank(rank, ws, job, q, precision="double", barrier="event"):
+    # halo exchanges ordered by CUDA IPC events (default) or by a stream drain
+    # + host barrier (EHMG_HOST_BARRIER=1); both must give the same results
+    os.environ["EHMG_HOST_BARRIER"] = "1" if barrier == "host" else "0"
     try:
         g, med, par, opt, r, b = _problem()
         d = E.DistributedSlabSolver(job, rank, ws, 0, g, med, par, opt, agg_n2=8, precision=precision)
@@ -47,8 +50,9 @@ def _rank(rank, ws, job, q, precision="double"):
         q.put((rank, None, None, None, -1, "error", repr(e)))
 
 
-@pytest.mark.parametrize("ws,precision", [(2, "double"), (3, "double"), (2, "mixed")])
-def test_distributed_slabs_match_single_process(ws, precision):
+@pytest.mark.parametrize("ws,precision,barrier", [(2, "double", "event"), (3, "double", "event"),
+                                                   (2, "mixed", "event"), (2, "double", "host")])
+def test_distributed_slabs_match_single_process(ws, precision, barrier):
     g, med, par, opt, r, b = _problem()
     z_ref = E.Multigrid(g, med, par, opt, precision=precision).precondition(r)
     mg = E.Multigrid(g, med, par, opt, precision=precision)
@@ -60,7 +64,7 @@ def test_distributed_slabs_match_single_process(ws, precision):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     job = f"t{os.getpid()}_{uuid.uuid4().hex[:8]}"
-    procs = [ctx.Process(target=_rank, args=(k, ws, job, q, precision)) for k in range(ws)]
+    procs = [ctx.Process(target=_rank, args=(k, ws, job, q, precision, barrier)) for k in range(ws)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(ws)]
