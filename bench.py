@@ -36,8 +36,8 @@ sys.path.insert(0, ROOT)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
 # kernel from one `ncu --set full` capture of the same residual at 256^3
 # (distinct b and x; profiles/round1/ncu_stencil3d_rr_residual.txt).
-NCU_TRAFFIC = {"residual@L0": 2859076000 + 1056127000,
-               "source": "profiles/round1/ncu_stencil3d_rr_residual.txt (ncu --set full, 256^3 residual)"}
+NCU_TRAFFIC = {"residual@L0": 2867563000 + 1056688000,
+               "source": "profiles/round2/ncu_stencil3d_rr_residual_r2.txt (ncu --set full, 256^3 residual)"}
 N_CELLS = 256
 LEVELS = 5  # at 256^3: coarsest level 16^3 cells (17^3 nodes), BASELINE configs[2]
 
@@ -518,9 +518,10 @@ def run_b200(args, ws, rank, local):
                      "traffic": (NCU_TRAFFIC.get(f"{kname}@L{klev}")
                                  if args.workload == "c2" and n == (N_CELLS,) * 3 else None),
                      "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
-                     "limiter": ("shared-memory/shuffle (LSU) pipe: 418 B of LSU traffic per DOF vs 56 B of "
-                                 "HBM, LSU bound = 77% of the HBM roofline; ncu: LSU 72% busy, IPC 1.73, FP64 "
-                                 "pipe 41%, DRAM 42% at 8 warps x 255 registers; see DESIGN.md"),
+                     "limiter": ("latency at 2 warps/scheduler (8 warps x 255 registers): LSU 71% and FP64 41% "
+                                 "of peak, IPC 1.73; stalls 26% short-scoreboard (LDS/SHFL results), 26% FP64 "
+                                 "dependency waits, 7% block barrier; 418 B of shared/shuffle traffic per DOF vs "
+                                 "56 B of HBM (profiles/round2/ncu_stencil3d_rr_residual_r2.txt; DESIGN.md)"),
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "clocks": clocks,
     }

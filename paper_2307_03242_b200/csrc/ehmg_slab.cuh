@@ -28,6 +28,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <cstring>
 
 #include "ehmg_comm.cuh"
 
@@ -171,7 +172,7 @@ struct ehmg_slab_mg_s {
   // copy streams) instead of a stream drain + host barrier per exchange.
   // kXEv slots in rotation: a rank re-records slot e % kXEv only after its
   // neighbours published exchange e + kXEv - 1, i.e. after they enqueued
-  // their waits for e. EHMG_HOST_BARRIER=1 keeps the drain + barrier.
+  // their waits for e.
   static constexpr int kXEv = 4;
   bool ev_exchange = false;
   cudaEvent_t xev[kXEv] = {}, xev_lo[kXEv] = {}, xev_hi[kXEv] = {};
@@ -682,16 +683,31 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
     }
     comm->exchange_blob(&mine, sizeof(Blob), all);
     {
-      const char* hb = std::getenv("EHMG_HOST_BARRIER");
-      sm->ev_exchange = !(hb && hb[0] == '1');
+      // Event-ordered exchanges when the neighbours run on other GPUs; ranks
+      // sharing one GPU keep the drain + host barrier (a stream waiting on
+      // another process's event on the same GPU forces context switches:
+      // 61 vs 13 ms per 128^3 cycle with 2 ranks on one B200,
+      // profiles/round2/dist_overhead_128.json). EHMG_EXCHANGE=event|host
+      // overrides (the tests run both on one GPU).
       struct EvBlob {
         cudaIpcEventHandle_t e[ehmg_slab_mg_s::kXEv];
+        cudaUUID_t dev;
       } emine{}, eall[kCommMaxRanks];
+      {
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, sm->dev));
+        emine.dev = prop.uuid;
+      }
       for (int i = 0; i < ehmg_slab_mg_s::kXEv; ++i) {
         CK(cudaEventCreateWithFlags(&sm->xev[i], cudaEventDisableTiming | cudaEventInterprocess));
         CK(cudaIpcGetEventHandle(&emine.e[i], sm->xev[i]));
       }
       comm->exchange_blob(&emine, sizeof(EvBlob), eall);
+      bool shared = false;
+      for (int r = q - 1; r <= q + 1; r += 2)
+        if (r >= 0 && r < comm->n && std::memcmp(&eall[r].dev, &emine.dev, sizeof(cudaUUID_t)) == 0) shared = true;
+      const char* ex = std::getenv("EHMG_EXCHANGE");
+      sm->ev_exchange = ex && std::strcmp(ex, "event") == 0 ? true : ex && std::strcmp(ex, "host") == 0 ? false : !shared;
       for (int i = 0; i < ehmg_slab_mg_s::kXEv; ++i) {
         if (q > 0) CK(cudaIpcOpenEventHandle(&sm->xev_lo[i], eall[q - 1].e[i]));
         if (q + 1 < comm->n) CK(cudaIpcOpenEventHandle(&sm->xev_hi[i], eall[q + 1].e[i]));

@@ -35,8 +35,8 @@ def _problem():
 
 def _rank(rank, ws, job, q, precision="double", barrier="event"):
     # halo exchanges ordered by CUDA IPC events (default) or by a stream drain
-    # + host barrier (EHMG_HOST_BARRIER=1); both must give the same results
-    os.environ["EHMG_HOST_BARRIER"] = "1" if barrier == "host" else "0"
+    # + host barrier (EHMG_EXCHANGE=host); both must give the same results
+    os.environ["EHMG_EXCHANGE"] = barrier
     try:
         g, med, par, opt, r, b = _problem()
         d = E.DistributedSlabSolver(job, rank, ws, 0, g, med, par, opt, agg_n2=8, precision=precision)

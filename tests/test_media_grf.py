@@ -73,3 +73,14 @@ def test_device_builder_matches_restatement(dims, corr, seed):
     r = O.layered_grf_media(dims, seed, corr_cells=corr, gamma_phys=0.02)
     for got, want in zip((m.lambda_, m.mu, m.rho, m.gamma), r.arrays()):
         assert np.array_equal(got, want)
+
+
+def test_device_builder_validates_before_touching_the_device():
+    import paper_2307_03242_b200 as E
+    g = E.StaggeredGrid((16, 12), 1 / 16)
+    with pytest.raises(ValueError, match="cp/cs must stay above sqrt"):
+        E.layered_grf_media(g, 1, cp_over_cs=(1.2, 2.0))
+    with pytest.raises(ValueError, match="1..64 layers"):
+        E.layered_grf_media(g, 1, n_layers=0)
+    with pytest.raises(ValueError, match="corr in"):
+        E.layered_grf_media(g, 1, corr_cells=0.0)

@@ -2,7 +2,7 @@
 box's GPU (host barriers cannot deadlock; IPC-event waits are stream
 semaphores, not spinning kernels), V(2,2) cycle time with the halo exchanges
 ordered by CUDA IPC events vs by a stream drain + host barrier
-(EHMG_HOST_BARRIER=1). Both ranks share one GPU, so the absolute times are
+(EHMG_EXCHANGE=event|host). Both ranks share one GPU, so the absolute times are
 not a scaling measurement; the difference is the host round trips.
 
     python tools/dist_overhead.py [n_cells]
@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def rank_main(rank, ws, job, n, barrier, q):
-    os.environ["EHMG_HOST_BARRIER"] = "1" if barrier == "host" else "0"
+    os.environ["EHMG_EXCHANGE"] = barrier
     try:
         import paper_2307_03242_b200 as E
         g = E.StaggeredGrid((n, n, n), 1.0 / n)
