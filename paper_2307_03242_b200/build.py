@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libehmg_b200.so")
 SOURCES = ["ehmg_solver.cu"]
-HEADERS = ["ehmg_core.cuh", "ehmg_kernels.cuh", "ehmg_stencil2d.cuh", "ehmg_stencil3d.cuh", "ehmg_stencil3d_rr.cuh", "ehmg_slab.cuh", "ehmg_comm.cuh", "ehmg_solver.cu"]
+HEADERS = ["ehmg_core.cuh", "ehmg_kernels.cuh", "ehmg_stencil2d.cuh", "ehmg_stencil3d.cuh", "ehmg_stencil3d_rr.cuh", "ehmg_stencil3d_sp.cuh", "ehmg_media.cuh", "ehmg_slab.cuh", "ehmg_comm.cuh", "ehmg_solver.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -36,6 +36,7 @@
 #include "ehmg_stencil2d.cuh"
 #include "ehmg_stencil3d.cuh"
 #include "ehmg_stencil3d_rr.cuh"
+#include "ehmg_stencil3d_sp.cuh"
 
 namespace ehmg {
 

@@ -76,8 +76,14 @@ struct S3Params {
   double wn;                      // (1-beta)/6
   double inv_msum[7];             // 1/(beta + k*wn), k valid mass neighbours
   int nchunks, ntiles_x, ntiles_y;
+  int itx, ity;  // k_stencil3d_sp: tile columns 1..itx / rows 1..ity lie strictly inside the box
   int z_lo, z_hi;  // output planes [z_lo, z_hi); z_hi = n2 + 1 includes the top u2 faces
   float inv_wsum_f[16], inv_msum_f[7];  // the same tables accumulated in float (complex64 kernel)
+  double inv_wsum_h[16];                // inv_wsum * inv_h (k_stencil3d_sp)
+  // k_stencil3d_sp, tiles strictly inside the box: the z-dependent constants by
+  // plane class lz | hz0 << 1 | hz1 << 2 | (z >= 0) << 3:
+  // {inv_wsum_h[3|zA], inv_wsum_h[zB|12], inv_wsum_h[3|zC], inv_msum[4+lz+hz0], inv_msum[4+lz+hz1], izp}
+  double zt[16][6];
 };
 
 // Source arrays of the complex64 kernel (loaded with cp.async: complex64
@@ -542,6 +548,7 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z
           wsf += wf * (float)((s1 == 0 ? 2 : 1) * (s2 == 0 ? 2 : 1));
         }
     s.inv_wsum_f[f] = P.beta != 1.0 ? 1.0f / wsf : 1.0f;
+    s.inv_wsum_h[f] = s.inv_wsum[f] * g.inv_h;
   }
   s.wn = (1.0 - P.beta) / 6.0;
   for (int c = 0; c <= 6; ++c) {
@@ -552,8 +559,20 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z
     for (int q = 0; q < c; ++q) wsf += (float)s.wn;
     s.inv_msum_f[c] = P.beta != 1.0 ? 1.0f / wsf : 1.0f;
   }
+  for (int c = 0; c < 16; ++c) {
+    const int lz = c & 1, hz0 = (c >> 1) & 1, hz1 = (c >> 2) & 1, z0 = (c >> 3) & 1;
+    const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
+    s.zt[c][0] = s.inv_wsum_h[3 | zA];
+    s.zt[c][1] = s.inv_wsum_h[zB | 12];
+    s.zt[c][2] = s.inv_wsum_h[3 | zC];
+    s.zt[c][3] = s.inv_msum[4 + lz + hz0];
+    s.zt[c][4] = s.inv_msum[4 + lz + hz1];
+    const int cnt = z0 + hz0;
+    s.zt[c][5] = cnt == 2 ? 0.5 : (cnt == 1 ? 1.0 : 0.0);
+  }
   s.ntiles_x = (g.n[0] + 1 + tx - 1) / tx;
   s.ntiles_y = (g.n[1] + 1 + ty - 1) / ty;
+  s.itx = s.ity = 0;
   // z-chunks: minimise (rounds of persistent CTAs) x (planes per chunk + 2
   // warm-up planes) over chunk counts with >= 4 planes per chunk, so that
   // the tile x chunk items fill whole waves of the 148 SMs.

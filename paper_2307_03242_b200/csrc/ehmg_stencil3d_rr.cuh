@@ -651,8 +651,8 @@ inline bool launch_stencil3d_rr(const Geo& g, const OpPar& P, const typename VT<
   return true;
 }
 
-inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
-                             const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+inline void launch_stencil3d_c128_rr(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x,
+                                     const cplx* b, cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
   if (!launch_stencil3d_rr<cplx>(g, P, media_soa, x, b, y, s, z_lo, z_hi))
     throw std::runtime_error("ehmg: 3D stencil tensor maps could not be encoded");
 }

@@ -1,0 +1,697 @@
+// ehmg_stencil3d_sp.cuh -- split-part register-resident 3D operator / residual
+// (complex128).
+//
+// y = H x  or  r = b - H x  for the staggered mixed elastic-Helmholtz operator
+// (operator.hpp:389-421), all four components in one launch.
+//
+// Every coefficient of the operator is real except the face mass
+// w^2 rho (1 - i(gamma + alpha)) (operator.hpp:131-155), so the real and the
+// imaginary parts of a field are two independent real stencil problems that
+// meet only in the mass product at one point. k_stencil3d_rr gave one lane a
+// whole complex position (29 complex values of z-carried state: 116
+// registers, 8 warps per SM at the 255-register cap, latency-bound). Here a
+// lane PAIR owns a position: even lanes carry the real parts, odd lanes the
+// imaginary parts, so the state per thread halves. That pays for either NY = 2
+// rows per thread (y neighbours of a thread's own rows stay in registers:
+// fewer shared-memory round trips) or twice the warps per SM.
+//  * thread grid = flux window: 16 columns (lane >> 1) x NW*NY rows
+//    (warp * NY + r); outputs are the inner 14 x (NW*NY - 2) positions.
+//  * shared-memory planes stay interleaved complex128 as TMA delivers them:
+//    lane l reads the double at 8*l -- conflict-free, 256 B per warp load.
+//  * x neighbours of computed values by warp shuffles (two lanes away), y
+//    neighbours across threads through shared memory, z by register carries;
+//    the mass product reads both parts of its own value with one 16-byte
+//    load shared by the lane pair.
+//  * everything else as in k_stencil3d_rr: z-march with persistent CTAs over
+//    (tile, z-chunk) items, TMA plane rings one plane ahead with hardware
+//    zero fill for the reference's zero ghosts (operator.hpp:172), in-plane
+//    spreads carried as differences of per-plane spreads, one block barrier
+//    per plane, carries alternating between two register sets.
+// The operation order per value is that of k_stencil3d_rr (component-wise on
+// the parts), so results agree with it to the last bits.
+#pragma once
+
+#include "ehmg_stencil3d_rr.cuh"
+
+namespace ehmg {
+
+template <int NW_, int NY_>
+struct SPCfg {
+  static_assert(NY_ == 1 || NY_ == 2, "rows per thread");
+  static constexpr int NW = NW_, NY = NY_;
+  static constexpr int TX = 14, FX = 16, FY = NW * NY, TY = FY - 2;
+  static constexpr int UX = FX + 2, UY = FY + 2, UN = UX * UY;
+  static constexpr int THREADS = NW * 32;
+  static constexpr int US = (UN + 7) / 8 * 8;     // complex per slot: 128-byte multiples
+  static constexpr int MX = UX, MN = MX * UY, MS = (MN + 15) / 16 * 16;
+  static constexpr int FN = FX * FY;
+  static constexpr int NQ = NY > 1 ? 2 : 1;
+  static constexpr unsigned CBYTES = UN * 16, MBYTES = MN * 8, BBYTES = FN * 16;
+};
+
+// One ring slot holds everything of one plane, so a plane's base address plus
+// compile-time offsets reaches every array (LDS [thread + slot + imm]).
+template <class K>
+struct __align__(128) SPSlot {
+  cplx u[3][K::US];                // x planes by component
+  cplx p[K::US];
+  double mu[K::MS], rho[K::MS], gam[K::MS], ilm[K::MS];
+  cplx bp[4][K::FN];               // residual mode: b rows of the thread grid
+  double q[3][K::NQ][K::THREADS];  // mass products [component][first / last row of a thread]
+};
+template <class K>
+struct __align__(128) SPSmem {
+  SPSlot<K> ring[3];            // [plane % 3]
+  double fy[2][3][K::THREADS];  // [plane & 1]: F11 of a thread's last row, F01 and F21 of its first row
+  unsigned long long bar[2];
+};
+
+__device__ __forceinline__ double sp_up(double v) { return __shfl_up_sync(0xffffffffu, v, 2); }    // x - 1
+__device__ __forceinline__ double sp_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 2); }  // x + 1
+__device__ __forceinline__ double sp_ld(const char* base, int off) {
+  return *reinterpret_cast<const double*>(base + off);
+}
+
+template <class K>
+__device__ __forceinline__ void sp_issue(SPSmem<K>& S, const R3Maps& RM, int i0, int j0, int zu, int nu, int zm,
+                                         int nm, int zp, int np, bool hasb, int zb_, unsigned long long* bar) {
+  const S3Maps& M = RM.m;
+  s3_expect(bar, (unsigned)(nu * 3 * K::CBYTES + nm * 4 * K::MBYTES + np * K::CBYTES + (hasb ? 4 * K::BBYTES : 0)));
+  if (hasb)
+    for (int k = 0; k < 4; ++k) s3_tma(S.ring[s3_mod3(zb_)].bp[k], &RM.b[k], 2 * (i0 - 1), j0 - 1, zb_, bar);
+  const int cx = 2 * (i0 - 2), cy = j0 - 2, mx = i0 - 2;
+  for (int q = 0; q < nu; ++q) {
+    SPSlot<K>& R = S.ring[s3_mod3(zu + q)];
+    for (int k = 0; k < 3; ++k) s3_tma(R.u[k], &M.u[k], cx, cy, zu + q, bar);
+  }
+  for (int q = 0; q < nm; ++q) {
+    SPSlot<K>& R = S.ring[s3_mod3(zm + q)];
+    s3_tma(R.mu, &M.mu, mx, cy, zm + q, bar);
+    s3_tma(R.rho, &M.rho, mx, cy, zm + q, bar);
+    s3_tma(R.gam, &M.gam, mx, cy, zm + q, bar);
+    s3_tma(R.ilm, &M.ilm, mx, cy, zm + q, bar);
+  }
+  for (int q = 0; q < np; ++q) s3_tma(S.ring[s3_mod3(zp + q)].p, &M.p, cx, cy, zp + q, bar);
+}
+
+// elect.sync: one lane of a converged warp (lets the compiler issue the TMA
+// without a per-thread serialisation loop).
+__device__ __forceinline__ bool sp_elect() {
+  unsigned pred;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
+
+// The per-plane load group of step z, spread over the warps: load i of
+// {u0, u1, u2, p, mu, rho, gam, ilm, b0..b3} (the order of the maps in R3Maps)
+// is issued by warp i % NW, so no warp carries the whole issue sequence into
+// the plane's barrier. u and media planes z + 2, p and b planes z + 1. The
+// expect-tx arrival is warp 0's; a completion that lands first only drives
+// the transaction count negative until then.
+template <class K>
+__device__ __forceinline__ void sp_issue_step(SPSmem<K>& S, const R3Maps& RM, int warp, int i0, int j0, int z,
+                                              bool hasb, unsigned long long* bar) {
+  typedef SPSlot<K> SL;
+  const int nl = hasb ? 12 : 8;
+  if (warp >= nl) return;
+  if (!sp_elect()) return;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (warp == 0)
+    s3_expect(bar, (unsigned)(3 * K::CBYTES + 4 * K::MBYTES + K::CBYTES + (hasb ? 4 * K::BBYTES : 0)));
+  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(&RM);
+  const int sl2 = s3_mod3(z + 2), sl1 = s3_mod3(z + 1);
+  for (int i = warp; i < nl; i += K::NW) {
+    int soff, c0, c1, zz, sl;
+    if (i < 3) {
+      soff = (int)offsetof(SL, u) + i * K::US * 16, c0 = 2 * (i0 - 2), c1 = j0 - 2, zz = z + 2, sl = sl2;
+    } else if (i == 3) {
+      soff = (int)offsetof(SL, p), c0 = 2 * (i0 - 2), c1 = j0 - 2, zz = z + 1, sl = sl1;
+    } else if (i < 8) {
+      soff = (int)offsetof(SL, mu) + (i - 4) * K::MS * 8, c0 = i0 - 2, c1 = j0 - 2, zz = z + 2, sl = sl2;
+    } else {
+      soff = (int)offsetof(SL, bp) + (i - 8) * K::FN * 16, c0 = 2 * (i0 - 1), c1 = j0 - 1, zz = z + 1, sl = sl1;
+    }
+    s3_tma(reinterpret_cast<char*>(&S.ring[sl]) + soff, maps + i, c0, c1, zz, bar);
+  }
+}
+
+// Quantities one row of a thread carries from plane to plane (one part of
+// each complex value). Two instances per row alternate roles (cur = newest
+// values, nxt = the older ones, overwritten by this plane's results); the z
+// loop is unrolled by two with the roles swapped, so nothing is copied.
+struct SPCarry {
+  double r00, r11, r01, r10, r20, r21;  // z-family row sums
+  double t0, t1, t2;                    // in-plane spreads of u0, u1, u2 at plane z
+  double f02, f12, f22;                 // in-plane family fluxes of the previous step
+  double q0, q1, q2;                    // mass products
+  double p;                             // p of the previous plane
+  double u0, u1, u2;                    // own u at plane z
+  double mu02, mu12;                    // edge averages of planes (z-1, z)
+};
+
+// Per-item constants of a thread: x flags shared by its rows, y flags per row.
+//   xb: 1 lx, 2 hx0, 4 hx1, 8 x in [0, n0], 16 x in [0, n0), 32 output column
+//   yb: 1 ly, 2 hy0, 4 hy1, 8 y in [0, n1), 16 y in [0, n1], 32 output row
+// uo / mo / bo / qo: byte offsets of the thread's first row inside a ring slot.
+template <class K>
+struct SPPos {
+  int t, warp, part, i0, j0, zb, xb;
+  int uo, xo, mo, bo, qo;
+  int yb[K::NY];
+  double ix;
+  double* yp[4];  // output pointers of the first row (this part) at the current plane
+};
+
+template <class K>
+__device__ __forceinline__ SPPos<K> sp_pos(const Geo& g, int t, int i0, int j0, int zb, int z0, cplx* y) {
+  SPPos<K> Q;
+  const int lane = t & 31, warp = t >> 5, px = lane >> 1, part = lane & 1;
+  const int n0 = g.n[0], n1 = g.n[1];
+  Q.t = t;
+  Q.warp = __shfl_sync(0xffffffffu, warp, 0);  // warp-uniform for the compiler
+  Q.part = part;
+  Q.i0 = i0;
+  Q.j0 = j0;
+  Q.zb = zb;
+  const int fy0 = warp * K::NY;
+  Q.uo = (int)offsetof(SPSlot<K>, u) + (2 * ((px + 1) + K::UX * (fy0 + 1)) + part) * 8;
+  Q.xo = part ? -8 : 8;  // the other part of the same value
+  Q.mo = (int)offsetof(SPSlot<K>, mu) + ((px + 1) + K::MX * (fy0 + 1)) * 8;
+  Q.bo = (int)offsetof(SPSlot<K>, bp) + (fy0 * 32 + lane) * 8;
+  Q.qo = (int)offsetof(SPSlot<K>, q) + t * 8;
+  const int xg = i0 - 1 + px;
+  const int lx = xg >= 1, hx0 = xg + 1 < n0, hx1 = xg < n0;
+  Q.xb = lx | (hx0 << 1) | (hx1 << 2) | ((xg >= 0 && xg <= n0) << 3) | ((xg >= 0 && xg < n0) << 4) |
+         ((px >= 1 && px <= K::TX) << 5);
+  Q.ix = s3_inv<double>(lx + hx1);
+  const int yg0 = j0 - 1 + fy0;
+#pragma unroll
+  for (int r = 0; r < K::NY; ++r) {
+    const int fy = fy0 + r, yg = yg0 + r;
+    const int ly = yg >= 1, hy0 = yg + 1 < n1, hy1 = yg < n1;
+    Q.yb[r] = ly | (hy0 << 1) | (hy1 << 2) | ((yg >= 0 && yg < n1) << 3) | ((yg >= 0 && yg <= n1) << 4) |
+              ((fy >= 1 && fy <= K::TY) << 5);
+  }
+  double* yd = reinterpret_cast<double*>(y) + part;
+  Q.yp[0] = yd + 2 * (g.off[0] + xg + (int64_t)(n0 + 1) * (yg0 + (int64_t)n1 * z0));
+  Q.yp[1] = yd + 2 * (g.off[1] + xg + (int64_t)n0 * (yg0 + (int64_t)(n1 + 1) * z0));
+  Q.yp[2] = yd + 2 * (g.off[2] + xg + (int64_t)n0 * (yg0 + (int64_t)n1 * z0));
+  Q.yp[3] = yd + 2 * (g.off[3] + xg + (int64_t)n0 * (yg0 + (int64_t)n1 * z0));
+  return Q;
+}
+
+// IN: the tile's whole window lies strictly inside the box in x and y, so
+// every x / y boundary flag is a compile-time constant.
+template <class K, bool IN>
+__device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const S3Params& P, SPPos<K>& Q,
+                                        const bool hasb, int z, int& su0, unsigned& seq, SPCarry (&cur)[K::NY],
+                                        SPCarry (&nxt)[K::NY]) {
+  typedef SPSlot<K> SL;
+  constexpr int NY = K::NY, NT = K::THREADS, NQ = K::NQ;
+  constexpr int ROW = K::UX * 16;    // bytes between rows of a complex window
+  constexpr int MROW = K::MX * 8;    // ... of a media window
+  constexpr int CU = K::US * 16;     // bytes between components in SL::u
+  constexpr int OP = (int)offsetof(SL, p) - (int)offsetof(SL, u);
+  constexpr int ORH = (int)offsetof(SL, rho) - (int)offsetof(SL, mu);
+  constexpr int OGA = (int)offsetof(SL, gam) - (int)offsetof(SL, mu);
+  constexpr int OIL = (int)offsetof(SL, ilm) - (int)offsetof(SL, mu);
+  constexpr int CB = K::FN * 16;     // bytes between components in SL::bp
+  constexpr int QC = NQ * NT * 8, QJ = NT * 8;
+  const Geo& g = P.g;
+  const int t = Q.t, part = Q.part;
+  const double beta = P.beta, w = P.w, ih = g.inv_h, wn = P.wn;
+  auto IWH = [&](int i) -> double { return P.inv_wsum_h[i]; };  // inv_wsum * inv_h
+  auto IM = [&](int i) -> double { return P.inv_msum[i]; };
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int n2g = g.gn2;
+
+  s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+  ++seq;
+  sp_issue_step<K>(S, maps, Q.warp, Q.i0, Q.j0, z, hasb, &S.bar[seq & 1]);
+  const int s0 = su0, s1 = su0 == 2 ? 0 : su0 + 1;
+  su0 = s1;
+  const char* R0 = reinterpret_cast<const char*>(&S.ring[s0]);
+  const char* R1 = reinterpret_cast<const char*>(&S.ring[s1]);
+  const char* U = R0 + Q.uo;   // plane z, my part, first row
+  const char* V = R1 + Q.uo;   // plane z + 1
+  const char* VX = V + Q.xo;   // plane z + 1, the other part
+  const char* M0 = R0 + Q.mo;
+  const char* M1 = R1 + Q.mo;
+  const int zg = z + g.zoff;
+  const int lz = zg >= 1, hz0 = zg + 1 < n2g, hz1 = zg + 1 < n2g + 1;
+  const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
+  // tiles inside the box: the plane's constants from one table row (uniform loads)
+  const double* ZT = P.zt[lz | (hz0 << 1) | (hz1 << 2) | ((zg >= 0) << 3)];
+  const double izp = IN ? ZT[5] : s3_inv<double>((zg + 1 >= 1) + (zg + 1 < n2g));
+  auto WA = [&](int yb) -> double { return IN ? ZT[0] : IWH((yb & 3) | zA); };
+  auto WB = [&](int f) -> double { return IN ? ZT[1] : IWH(zB | f); };
+  auto WC = [&](int f) -> double { return IN ? ZT[2] : IWH(f | zC); };
+  auto WI = [&](int i) -> double { return IN ? P.inv_wsum_h[15] : IWH(i); };
+  const double al = P.alpha, w2 = P.omega2, w2s = part ? -w2 : w2;
+  const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
+  const bool zin2 = zg + 1 >= 0 && zg + 1 <= n2g;
+  // mass product md * v, my part: md = (w2 rho_f, -w2 gam_f rho_f)
+  auto mdq = [&](double sr, double sg, double ic, double mine, double other) {
+    const double rho_f = sr * ic, gam_f = sg * ic + al;
+    const double mdx = w2 * rho_f, sm = w2s * gam_f * rho_f;  // sm = +-Im(md): -w2 gam_f rho_f for the imaginary part
+    return mdx * mine + sm * other;
+  };
+  char* QN = reinterpret_cast<char*>(&S.ring[s1]) + Q.qo;
+  double(*FYs)[NT] = S.fy[z & 1];
+  const int xb = IN ? (Q.xb | 31) : Q.xb;
+  const int xl = xb & 3;                                // lx | hx0 << 1
+  const int fl01x = ((xb & 1) << 2) | ((xb & 4) << 1);  // lx << 2 | hx1 << 3
+  const double ix = IN ? 0.5 : Q.ix;
+
+  double m0[NY], m1[NY], m2[NY], o0v[NY], o1v[NY], o2v[NY], o3v[NY], pt0[NY], pt2[NY], pc[NY];
+  double f1[NY], f2[NY], f5[NY];
+  {
+    // media columns: index r + 1 = own row r, r = the row below it
+    double mcC[NY + 1], mcL[NY + 1], mpC[NY + 1], mpL[NY + 1], rpC[NY + 1], gpC[NY + 1];
+#pragma unroll
+    for (int r = 0; r <= NY; ++r) {
+      const int o = (r - 1) * MROW;
+      mcC[r] = sp_ld(M0, o);
+      mcL[r] = sp_ld(M0, o - 8);
+      mpC[r] = sp_ld(M1, o);
+      rpC[r] = sp_ld(M1, ORH + o);
+      gpC[r] = sp_ld(M1, OGA + o);
+    }
+#pragma unroll
+    for (int r = 1; r <= NY; ++r) mpL[r] = sp_ld(M1, (r - 1) * MROW - 8);
+    double mu01[NY], mu02p[NY], mu12p[NY], iy[NY];
+    int ybs[NY];
+#pragma unroll
+    for (int r = 0; r < NY; ++r) {
+      const int yb = IN ? (Q.yb[r] | 31) : Q.yb[r];
+      ybs[r] = yb;
+      iy[r] = s3_inv<double>((yb & 1) + ((yb >> 2) & 1));
+      mu01[r] = (mcL[r] + mcL[r + 1] + mcC[r] + mcC[r + 1]) * (ix * iy[r]);
+      mu02p[r] = (mcL[r + 1] + mpL[r + 1] + mcC[r + 1] + mpC[r + 1]) * (ix * izp);
+      mu12p[r] = (mcC[r] + mpC[r] + mcC[r + 1] + mpC[r + 1]) * (iy[r] * izp);
+    }
+    // mass: beta*q + the x neighbours (the lane pairs two lanes away stored
+    // them for their y neighbours last step: read instead of shuffled) + the
+    // z-1 neighbour; y neighbours and z+1 follow after the barrier
+    const char* SQ0 = R0 + Q.qo;
+    auto mass_head = [&](double qc, double qm, int off) {
+      double m = beta * qc;
+      m += wn * sp_ld(SQ0, off - 16);
+      m += wn * sp_ld(SQ0, off + 16);
+      m += wn * qm;
+      return m;
+    };
+    // ---- component 0: F00 (cell, +x pair), F01 (edge01, -y pair), F02 (edge02, +z pair)
+    {
+      double vc[NY + 2], vo[NY];
+#pragma unroll
+      for (int r = 0; r < NY + 2; ++r) vc[r] = sp_ld(V, (r - 1) * ROW);
+#pragma unroll
+      for (int r = 0; r < NY; ++r) vo[r] = sp_ld(VX, r * ROW);
+      const double ub = sp_ld(U, -ROW);
+#pragma unroll
+      for (int r = 0; r < NY; ++r) {
+        const int yb = ybs[r];
+        const double v00 = vc[r + 1];
+        const double u00 = cur[r].u0, u0p = sp_ld(U, r * ROW + 16), um0 = r == 0 ? ub : cur[r == 0 ? 0 : r - 1].u0;
+        const double sy = vc[r] + vc[r + 2] + 2.0 * v00, syl = sp_up(sy), syr = sp_dn(sy);
+        const double dy = v00 - vc[r];
+        const double rn0 = syr - sy;
+        const double sz0 = (nxt[r].r00 + 2.0 * cur[r].r00) + rn0;
+        nxt[r].r00 = rn0;
+        const double d00 = (beta * (u0p - u00) + w * sz0) * WA(yb);
+        o3v[r] = d00;
+        const double f0 = mcC[r + 1] * d00;
+        o0v[r] = (sp_up(f0) - f0) * ih;
+        const double rn1 = sp_up(dy) + sp_dn(dy) + 2.0 * dy;
+        const double sz1 = (nxt[r].r01 + 2.0 * cur[r].r01) + rn1;
+        nxt[r].r01 = rn1;
+        f2[r] = mu01[r] * ((beta * (u00 - um0) + w * sz1) * WB(fl01x));
+        const double tn = syl + syr + 2.0 * sy;
+        nxt[r].f02 = mu02p[r] * ((beta * (v00 - u00) + w * (tn - cur[r].t0)) * WI((yb & 3) | fl01x));
+        nxt[r].t0 = tn;
+        m0[r] = mass_head(cur[r].q0, nxt[r].q0, (r == 0 ? 0 : QJ));
+        const bool ok = IN || (zin && (xb & 8) && (yb & 8));  // outside: zero-filled u and media give 0
+        const double qn =
+            ok ? mdq(sp_ld(M1, ORH + r * MROW - 8) + rpC[r + 1], sp_ld(M1, OGA + r * MROW - 8) + gpC[r + 1], ix, v00, vo[r])
+               : 0.0;
+        nxt[r].q0 = qn;
+        nxt[r].u0 = v00;
+        if (r == 0) *reinterpret_cast<double*>(QN) = qn;
+        if (r == NY - 1 && NY > 1) *reinterpret_cast<double*>(QN + QJ) = qn;
+      }
+      FYs[1][t] = f2[0];
+    }
+    // ---- component 1: F11 (cell, +y pair), F10 (edge01, -x pair), F12 (edge12, +z pair)
+    {
+      double vc[NY + 2], vo[NY];
+#pragma unroll
+      for (int r = 0; r < NY + 2; ++r) vc[r] = sp_ld(V, CU + (r - 1) * ROW);
+#pragma unroll
+      for (int r = 0; r < NY; ++r) vo[r] = sp_ld(VX, CU + r * ROW);
+      const double ut = sp_ld(U, CU + NY * ROW);
+#pragma unroll
+      for (int r = 0; r < NY; ++r) {
+        const int yb = ybs[r];
+        const int fl10 = ((yb & 1) << 2) | ((yb & 4) << 1);
+        const double v00 = vc[r + 1];
+        const double u00 = cur[r].u1, up0 = r == NY - 1 ? ut : cur[r == NY - 1 ? r : r + 1].u1,
+                     u0m = sp_ld(U, CU + r * ROW - 16);
+        const double sy = vc[r] + vc[r + 2] + 2.0 * v00, syl = sp_up(sy), syr = sp_dn(sy);
+        const double dy = vc[r + 2] - v00;
+        const double rn0 = sp_up(dy) + sp_dn(dy) + 2.0 * dy;
+        const double sz0 = (nxt[r].r11 + 2.0 * cur[r].r11) + rn0;
+        nxt[r].r11 = rn0;
+        const double d11 = (beta * (up0 - u00) + w * sz0) * WB(xl << 2);
+        o3v[r] += d11;
+        f1[r] = mcC[r + 1] * d11;
+        const double rn1 = sy - syl;
+        const double sz1 = (nxt[r].r10 + 2.0 * cur[r].r10) + rn1;
+        nxt[r].r10 = rn1;
+        const double f3 = mu01[r] * ((beta * (u00 - u0m) + w * sz1) * WB(fl10));
+        o1v[r] = (f3 - sp_dn(f3)) * ih;
+        const double tn = syl + syr + 2.0 * sy;
+        nxt[r].f12 = mu12p[r] * ((beta * (v00 - u00) + w * (tn - cur[r].t1)) * WI(xl | fl10));
+        nxt[r].t1 = tn;
+        m1[r] = mass_head(cur[r].q1, nxt[r].q1, QC + (r == 0 ? 0 : QJ));
+        const bool ok = IN || (zin && (xb & 16) && (yb & 16));
+        const double qn = ok ? mdq(rpC[r] + rpC[r + 1], gpC[r] + gpC[r + 1], iy[r], v00, vo[r]) : 0.0;
+        nxt[r].q1 = qn;
+        nxt[r].u1 = v00;
+        if (r == 0) *reinterpret_cast<double*>(QN + QC) = qn;
+        if (r == NY - 1 && NY > 1) *reinterpret_cast<double*>(QN + QC + QJ) = qn;
+      }
+      FYs[0][t] = f1[NY - 1];
+    }
+    // ---- component 2: F20 (edge02, -x pair), F21 (edge12, -y pair), F22 (cell, +z pair)
+    {
+      double vc[NY + 2], vo[NY];
+#pragma unroll
+      for (int r = 0; r < NY + 2; ++r) vc[r] = sp_ld(V, 2 * CU + (r - 1) * ROW);
+#pragma unroll
+      for (int r = 0; r < NY; ++r) vo[r] = sp_ld(VX, 2 * CU + r * ROW);
+      const double ub = sp_ld(U, 2 * CU - ROW);
+#pragma unroll
+      for (int r = 0; r < NY; ++r) {
+        const int yb = ybs[r];
+        const double v00 = vc[r + 1];
+        const double u00 = cur[r].u2, u0m = sp_ld(U, 2 * CU + r * ROW - 16),
+                     um0 = r == 0 ? ub : cur[r == 0 ? 0 : r - 1].u2;
+        const double sy = vc[r] + vc[r + 2] + 2.0 * v00, syl = sp_up(sy), syr = sp_dn(sy);
+        const double dy = v00 - vc[r];
+        const double rn0 = sy - syl;
+        const double sz0 = (nxt[r].r20 + 2.0 * cur[r].r20) + rn0;
+        nxt[r].r20 = rn0;
+        const double f4 = cur[r].mu02 * ((beta * (u00 - u0m) + w * sz0) * WC(yb & 3));
+        o2v[r] = (f4 - sp_dn(f4)) * ih;
+        const double rn1 = sp_up(dy) + sp_dn(dy) + 2.0 * dy;
+        const double sz1 = (nxt[r].r21 + 2.0 * cur[r].r21) + rn1;
+        nxt[r].r21 = rn1;
+        f5[r] = cur[r].mu12 * ((beta * (u00 - um0) + w * sz1) * WC(xl));
+        const double tn = syl + syr + 2.0 * sy;
+        const double d22 = (beta * (v00 - u00) + w * (tn - cur[r].t2)) * WI(xl | ((yb & 3) << 2));
+        o3v[r] += d22;
+        nxt[r].f22 = mcC[r + 1] * d22;  // zero-filled mu masks cells outside the box
+        nxt[r].t2 = tn;
+        m2[r] = mass_head(cur[r].q2, nxt[r].q2, 2 * QC + (r == 0 ? 0 : QJ));
+        const bool ok = IN || (zin2 && (xb & 16) && (yb & 8));
+        const double qn = ok ? mdq(sp_ld(M0, ORH + r * MROW) + rpC[r + 1], sp_ld(M0, OGA + r * MROW) + gpC[r + 1], izp,
+                                   v00, vo[r])
+                             : 0.0;
+        nxt[r].q2 = qn;
+        nxt[r].u2 = v00;
+        if (r == 0) *reinterpret_cast<double*>(QN + 2 * QC) = qn;
+        if (r == NY - 1 && NY > 1) *reinterpret_cast<double*>(QN + 2 * QC + QJ) = qn;
+      }
+      FYs[2][t] = f5[0];
+    }
+#pragma unroll
+    for (int r = 0; r < NY; ++r) {
+      nxt[r].mu02 = mu02p[r];
+      nxt[r].mu12 = mu12p[r];
+      const double pv = sp_ld(U, OP + r * ROW);
+      pc[r] = pv;
+      o3v[r] += sp_ld(M0, OIL + r * MROW) * pv;
+      pt0[r] = (pv - sp_ld(U, OP + r * ROW - 16)) * ih;
+      pt2[r] = pv - cur[r].p;
+      nxt[r].p = pv;
+    }
+  }
+  __syncthreads();
+
+  if ((xb & 32) && z >= Q.zb) {
+    const char* SQ = R0 + Q.qo;
+    const char* BP = R0 + Q.bo;
+    const int czz = lz + hz0;
+    const int cx0 = (xb & 1) + ((xb >> 1) & 1), cx1 = (xb & 1) + ((xb >> 2) & 1);
+#pragma unroll
+    for (int r = 0; r < NY; ++r) {
+      const int yb = IN ? (Q.yb[r] | 31) : Q.yb[r];
+      if (!(yb & 32)) continue;  // halo row (warp-uniform)
+      const int cy0 = (yb & 1) + ((yb >> 1) & 1), cy1 = (yb & 1) + ((yb >> 2) & 1);
+      double a0 = o0v[r], a1 = o1v[r], a2 = o2v[r], a3 = o3v[r];
+      const double f2n = r < NY - 1 ? f2[r < NY - 1 ? r + 1 : r] : FYs[1][t + 32];
+      a0 += (f2[r] - f2n) * ih;
+      a0 += (cur[r].f02 - nxt[r].f02) * ih;
+      double mm = m0[r];
+      mm += wn * (r > 0 ? cur[r > 0 ? r - 1 : 0].q0 : sp_ld(SQ, (NQ - 1) * QJ - 256));
+      mm += wn * (r < NY - 1 ? cur[r < NY - 1 ? r + 1 : r].q0 : sp_ld(SQ, 256));
+      mm += wn * nxt[r].q0;
+      a0 -= mm * (IN ? ZT[3] : IM(cx1 + cy0 + czz));
+      a0 += pt0[r];
+      const double f1p = r > 0 ? f1[r > 0 ? r - 1 : 0] : FYs[0][t - 32];
+      a1 += (f1p - f1[r]) * ih;
+      a1 += (cur[r].f12 - nxt[r].f12) * ih;
+      mm = m1[r];
+      mm += wn * (r > 0 ? cur[r > 0 ? r - 1 : 0].q1 : sp_ld(SQ, QC + (NQ - 1) * QJ - 256));
+      mm += wn * (r < NY - 1 ? cur[r < NY - 1 ? r + 1 : r].q1 : sp_ld(SQ, QC + 256));
+      mm += wn * nxt[r].q1;
+      a1 -= mm * (IN ? ZT[3] : IM(cx0 + cy1 + czz));
+      a1 += (pc[r] - (r > 0 ? pc[r > 0 ? r - 1 : 0] : sp_ld(U, OP - ROW))) * ih;
+      const double f5n = r < NY - 1 ? f5[r < NY - 1 ? r + 1 : r] : FYs[2][t + 32];
+      a2 += (f5[r] - f5n) * ih;
+      a2 += (cur[r].f22 - nxt[r].f22) * ih;
+      mm = m2[r];
+      mm += wn * (r > 0 ? cur[r > 0 ? r - 1 : 0].q2 : sp_ld(SQ, 2 * QC + (NQ - 1) * QJ - 256));
+      mm += wn * (r < NY - 1 ? cur[r < NY - 1 ? r + 1 : r].q2 : sp_ld(SQ, 2 * QC + 256));
+      mm += wn * nxt[r].q2;
+      a2 -= mm * (IN ? ZT[4] : IM(cx0 + cy0 + lz + hz1));
+      a2 += pt2[r] * ih;
+      if (hasb) {
+        a0 = sp_ld(BP, r * 256) - a0;
+        a1 = sp_ld(BP, CB + r * 256) - a1;
+        a2 = sp_ld(BP, 2 * CB + r * 256) - a2;
+        a3 = sp_ld(BP, 3 * CB + r * 256) - a3;
+      }
+      const bool v0 = IN || ((xb & 8) && (yb & 8)), v1 = IN || ((xb & 16) && (yb & 16)),
+                 v2 = IN || ((xb & 16) && (yb & 8));
+      if (v0 && z < n2) Q.yp[0][(int64_t)r * (2 * (n0 + 1))] = a0;
+      if (v1 && z < n2) Q.yp[1][(int64_t)r * (2 * n0)] = a1;
+      if (v2) Q.yp[2][(int64_t)r * (2 * n0)] = a2;
+      if (v2 && z < n2) Q.yp[3][(int64_t)r * (2 * n0)] = a3;
+    }
+  }
+  // next plane
+  Q.yp[0] += 2 * (int64_t)(n0 + 1) * n1;
+  Q.yp[1] += 2 * (int64_t)n0 * (n1 + 1);
+  Q.yp[2] += 2 * (int64_t)n0 * n1;
+  Q.yp[3] += 2 * (int64_t)n0 * n1;
+}
+
+template <class K, bool IN>
+__device__ __forceinline__ void sp_march(SPSmem<K>& S, const R3Maps& maps, const S3Params& P, SPPos<K>& Q,
+                                         const bool hasb, int zs, int zend, unsigned& seq) {
+  SPCarry A[K::NY], B[K::NY];
+#pragma unroll
+  for (int r = 0; r < K::NY; ++r) {
+    SPCarry c;
+    c.r00 = c.r11 = c.r01 = c.r10 = c.r20 = c.r21 = 0.0;
+    c.t0 = c.t1 = c.t2 = c.f02 = c.f12 = c.f22 = c.q0 = c.q1 = c.q2 = c.p = 0.0;
+    c.u0 = c.u1 = c.u2 = 0.0;
+    c.mu02 = c.mu12 = 0.0;
+    A[r] = c;
+    B[r] = c;
+  }
+  int su0 = s3_mod3(zs);
+  for (int z = zs; z < zend; z += 2) {
+    sp_step<K, IN>(S, maps, P, Q, hasb, z, su0, seq, A, B);
+    sp_step<K, IN>(S, maps, P, Q, hasb, z + 1, su0, seq, B, A);
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::THREADS, 1)
+    k_stencil3d_sp(const __grid_constant__ R3Maps maps, const __grid_constant__ S3Params P,
+                   const cplx* __restrict__ b, cplx* __restrict__ y) {
+  extern __shared__ __align__(1024) unsigned char sp_raw[];
+  SPSmem<K>& S = *reinterpret_cast<SPSmem<K>*>(sp_raw);
+  const Geo& g = P.g;
+  const int t = threadIdx.x;
+
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s3_saddr(&S.bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned seq = 0;
+  const bool hasb = b != nullptr;
+
+  const int items = P.ntiles_x * P.ntiles_y * P.nchunks;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    // items: every (inside tile, chunk) first, then the tiles that touch the
+    // box boundary (they run the general path, slower per plane: kept apart
+    // so neighbouring tiles march in step and share their halos in L2)
+    int tx, ty, chunk;
+    {
+      const int ntx = P.ntiles_x, nint = P.itx * P.ity;
+      if (item < nint * P.nchunks) {
+        const int q = item % nint;
+        chunk = item / nint;
+        tx = 1 + q % P.itx;
+        ty = 1 + q / P.itx;
+      } else {
+        const int nb = ntx * P.ntiles_y - nint, e = item - nint * P.nchunks;
+        int q = e % nb;
+        chunk = e / nb;
+        const int rowb = ntx - P.itx, mid = P.ity * rowb;
+        if (q < ntx) {
+          tx = q, ty = 0;
+        } else if (q - ntx < mid) {
+          q -= ntx;
+          const int k = q % rowb;
+          ty = 1 + q / rowb;
+          tx = k == 0 ? 0 : P.itx + k;
+        } else {
+          q -= ntx + mid;
+          ty = P.ity + 1 + q / ntx;
+          tx = q % ntx;
+        }
+      }
+    }
+    const int zspan = P.z_hi - P.z_lo;
+    const int zb = P.z_lo + (int)(((int64_t)chunk * zspan) / P.nchunks);
+    const int zend = P.z_lo + (int)(((int64_t)(chunk + 1) * zspan) / P.nchunks);
+    const int i0 = tx * K::TX, j0 = ty * K::TY;
+    const int zs = zb - 2 - ((zend - zb) & 1);
+    SPPos<K> Q = sp_pos<K>(g, t, i0, j0, zb, zs, y);
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      sp_issue<K>(S, maps, i0, j0, zs, 2, zs, 2, zs, 1, false, 0, &S.bar[seq & 1]);
+    }
+    // window columns i0-1 .. i0+14 and rows j0-1 .. j0+FY-2 strictly inside the box
+    const bool inside = i0 >= 2 && i0 + K::FX < g.n[0] && j0 >= 2 && j0 + K::FY < g.n[1];
+    if (inside)
+      sp_march<K, true>(S, maps, P, Q, hasb, zs, zend, seq);
+    else
+      sp_march<K, false>(S, maps, P, Q, hasb, zs, zend, seq);
+    s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
+    ++seq;
+    __syncthreads();
+  }
+}
+
+template <class K>
+inline int sp_device_init() {
+  static std::mutex mu;
+  static int nsm_of[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!nsm_of[dev]) {
+    cudaFuncSetAttribute(k_stencil3d_sp<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SPSmem<K>));
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    nsm_of[dev] = nsm > 0 ? nsm : 148;
+  }
+  return nsm_of[dev];
+}
+
+template <class K>
+inline bool launch_stencil3d_sp(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x, const cplx* b,
+                                cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+  const int nsm = sp_device_init<K>();
+  struct Entry {
+    const void* x;
+    const void* m;
+    const void* b;
+    int n[3];
+    R3Maps M;
+  };
+  static std::vector<Entry> cache;
+  static size_t next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const R3Maps* Mp = nullptr;
+  for (const Entry& e : cache)
+    if (e.x == x && e.m == media_soa && e.b == b && e.n[0] == n0 && e.n[1] == n1 && e.n[2] == n2) {
+      Mp = &e.M;
+      break;
+    }
+  if (!Mp) {
+    Entry e;
+    e.x = x;
+    e.m = media_soa;
+    e.b = b;
+    e.n[0] = n0, e.n[1] = n1, e.n[2] = n2;
+    bool ok = true;
+    for (int k = 0; k < 3; ++k)
+      ok &= r3_encode(&e.M.m.u[k], x + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * K::UX, K::UY);
+    ok &= r3_encode(&e.M.m.p, x + g.off[3], 2 * n0, n1, n2, 2 * K::UX, K::UY);
+    const int64_t nc = g.ncells;
+    ok &= r3_encode(&e.M.m.mu, media_soa + 0 * nc, n0, n1, n2, K::MX, K::UY);
+    ok &= r3_encode(&e.M.m.rho, media_soa + 1 * nc, n0, n1, n2, K::MX, K::UY);
+    ok &= r3_encode(&e.M.m.gam, media_soa + 2 * nc, n0, n1, n2, K::MX, K::UY);
+    ok &= r3_encode(&e.M.m.ilm, media_soa + 3 * nc, n0, n1, n2, K::MX, K::UY);
+    if (b) {
+      for (int k = 0; k < 3; ++k)
+        ok &= r3_encode(&e.M.b[k], b + g.off[k], 2 * (n0 + (k == 0)), n1 + (k == 1), n2 + (k == 2), 2 * K::FX, K::FY);
+      ok &= r3_encode(&e.M.b[3], b + g.off[3], 2 * n0, n1, n2, 2 * K::FX, K::FY);
+    }
+    if (!ok) {
+      fprintf(stderr, "ehmg: tensor map encode failed (sp, n=%d,%d,%d x=%p b=%p)\n", n0, n1, n2, (const void*)x,
+              (const void*)b);
+      return false;
+    }
+    if (cache.size() < 256) {
+      cache.push_back(e);
+      Mp = &cache.back().M;
+    } else {
+      cache[next] = e;
+      Mp = &cache[next].M;
+      next = (next + 1) % cache.size();
+    }
+  }
+  const R3Maps M = *Mp;
+  S3Params sp = make_s3params(g, P, nsm, z_lo, z_hi, K::TY, K::TX);
+  if (sp.z_hi <= sp.z_lo) return true;
+  // tiles tx >= 1 with TX tx + FX < n0 (the kernel's `inside` test), likewise in y
+  sp.itx = n0 > K::FX + K::TX ? (n0 - K::FX - 1) / K::TX : 0;
+  sp.ity = n1 > K::FY + K::TY ? (n1 - K::FY - 1) / K::TY : 0;
+  if (sp.itx == 0 || sp.ity == 0) sp.itx = sp.ity = 0;
+  const int items = sp.ntiles_x * sp.ntiles_y * sp.nchunks;
+  const int grid = items < nsm ? items : nsm;
+  k_stencil3d_sp<K><<<grid, K::THREADS, sizeof(SPSmem<K>), s>>>(M, sp, b, y);
+  return true;
+}
+
+// complex128 production dispatch. EHMG_SP_NW = 0 selects k_stencil3d_rr.
+#ifndef EHMG_SP_NW
+#define EHMG_SP_NW 8
+#endif
+#ifndef EHMG_SP_NY
+#define EHMG_SP_NY 2
+#endif
+inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x, const cplx* b,
+                             cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
+#if EHMG_SP_NW > 0
+  if (!launch_stencil3d_sp<SPCfg<EHMG_SP_NW, EHMG_SP_NY>>(g, P, media_soa, x, b, y, s, z_lo, z_hi))
+    throw std::runtime_error("ehmg: 3D stencil tensor maps could not be encoded");
+#else
+  launch_stencil3d_c128_rr(g, P, media_soa, x, b, y, s, z_lo, z_hi);
+#endif
+}
+
+}  // namespace ehmg
