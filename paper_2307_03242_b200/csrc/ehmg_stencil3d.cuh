@@ -81,9 +81,10 @@ struct S3Params {
   float inv_wsum_f[16], inv_msum_f[7];  // the same tables accumulated in float (complex64 kernel)
   double inv_wsum_h[16];                // inv_wsum * inv_h (k_stencil3d_sp)
   // k_stencil3d_sp, tiles strictly inside the box: the z-dependent constants by
-  // plane class lz | hz0 << 1 | hz1 << 2 | (z >= 0) << 3:
-  // {inv_wsum_h[3|zA], inv_wsum_h[zB|12], inv_wsum_h[3|zC], inv_msum[4+lz+hz0], inv_msum[4+lz+hz1], izp}
-  double zt[16][6];
+  // plane class lz | hz0 << 1 | hz1 << 2 | (z >= 0) << 3, with c = inv_wsum_h[.]:
+  // {beta c, w c} for c at [3|zA], [zB|12], [3|zC]; inv_msum[4+lz+hz0], inv_msum[4+lz+hz1], izp, izp*omega2
+  double zt[16][10];
+  double bw_in[2];  // {beta c, w c} for c = inv_wsum_h[15] (in-plane families inside the box)
 };
 
 // Source arrays of the complex64 kernel (loaded with cp.async: complex64
@@ -562,14 +563,17 @@ inline S3Params make_s3params(const Geo& g, const OpPar& P, int nsm = 148, int z
   for (int c = 0; c < 16; ++c) {
     const int lz = c & 1, hz0 = (c >> 1) & 1, hz1 = (c >> 2) & 1, z0 = (c >> 3) & 1;
     const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
-    s.zt[c][0] = s.inv_wsum_h[3 | zA];
-    s.zt[c][1] = s.inv_wsum_h[zB | 12];
-    s.zt[c][2] = s.inv_wsum_h[3 | zC];
-    s.zt[c][3] = s.inv_msum[4 + lz + hz0];
-    s.zt[c][4] = s.inv_msum[4 + lz + hz1];
+    const double cA = s.inv_wsum_h[3 | zA], cB = s.inv_wsum_h[zB | 12], cC = s.inv_wsum_h[3 | zC];
+    s.zt[c][0] = P.beta * cA, s.zt[c][1] = w * cA;
+    s.zt[c][2] = P.beta * cB, s.zt[c][3] = w * cB;
+    s.zt[c][4] = P.beta * cC, s.zt[c][5] = w * cC;
+    s.zt[c][6] = s.inv_msum[4 + lz + hz0];
+    s.zt[c][7] = s.inv_msum[4 + lz + hz1];
     const int cnt = z0 + hz0;
-    s.zt[c][5] = cnt == 2 ? 0.5 : (cnt == 1 ? 1.0 : 0.0);
+    s.zt[c][8] = cnt == 2 ? 0.5 : (cnt == 1 ? 1.0 : 0.0);
+    s.zt[c][9] = s.zt[c][8] * P.omega2;
   }
+  s.bw_in[0] = P.beta * s.inv_wsum_h[15], s.bw_in[1] = w * s.inv_wsum_h[15];
   s.ntiles_x = (g.n[0] + 1 + tx - 1) / tx;
   s.ntiles_y = (g.n[1] + 1 + ty - 1) / ty;
   s.itx = s.ity = 0;

@@ -242,19 +242,27 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
   const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
   // tiles inside the box: the plane's constants from one table row (uniform loads)
   const double* ZT = P.zt[lz | (hz0 << 1) | (hz1 << 2) | ((zg >= 0) << 3)];
-  const double izp = IN ? ZT[5] : s3_inv<double>((zg + 1 >= 1) + (zg + 1 < n2g));
-  auto WA = [&](int yb) -> double { return IN ? ZT[0] : IWH((yb & 3) | zA); };
-  auto WB = [&](int f) -> double { return IN ? ZT[1] : IWH(zB | f); };
-  auto WC = [&](int f) -> double { return IN ? ZT[2] : IWH(f | zC); };
-  auto WI = [&](int i) -> double { return IN ? P.inv_wsum_h[15] : IWH(i); };
-  const double al = P.alpha, w2 = P.omega2, w2s = part ? -w2 : w2;
+  const double izp = IN ? ZT[8] : s3_inv<double>((zg + 1 >= 1) + (zg + 1 < n2g));
+  // derivative sample (beta d + w sz) c, c = inv_wsum_h[flags] (operator.hpp:274-300); inside the box
+  // beta c and w c come premultiplied. kind 0: [yb|zA], 1: [zB|f], 2: [f|zC], 3: in-plane [f]
+  auto DS = [&](int kind, int f, double d, double sz) -> double {
+    if (IN) {
+      const double bc = kind == 3 ? P.bw_in[0] : ZT[2 * kind], wc = kind == 3 ? P.bw_in[1] : ZT[2 * kind + 1];
+      return d * bc + sz * wc;
+    }
+    const double c = IWH(kind == 0 ? (f | zA) : kind == 1 ? (zB | f) : kind == 2 ? (f | zC) : f);
+    return (beta * d + w * sz) * c;
+  };
+  const double al = P.alpha, w2 = P.omega2;
   const bool zin = zg + 1 >= 0 && zg + 1 < n2g;
   const bool zin2 = zg + 1 >= 0 && zg + 1 <= n2g;
-  // mass product md * v, my part: md = (w2 rho_f, -w2 gam_f rho_f)
-  auto mdq = [&](double sr, double sg, double ic, double mine, double other) {
-    const double rho_f = sr * ic, gam_f = sg * ic + al;
-    const double mdx = w2 * rho_f, sm = w2s * gam_f * rho_f;  // sm = +-Im(md): -w2 gam_f rho_f for the imaginary part
-    return mdx * mine + sm * other;
+  // mass product md * v, my part: md = w2 rho_f (1, -gam_f) (operator.hpp:152-154), so
+  // Re = mdx (v.re + gam_f v.im), Im = mdx (v.im - gam_f v.re): mdx (mine + sgn gam_f other).
+  // icw = ic * w2 (ic: the face-average divisor 1/1 or 1/2)
+  const double sgn = part ? -1.0 : 1.0, als = sgn * al;
+  auto mdq = [&](double sr, double sg, double ic, double icw, double mine, double other) {
+    const double mdx = sr * icw, gs = sg * (sgn * ic) + als;
+    return mdx * (gs * other + mine);
   };
   char* QN = reinterpret_cast<char*>(&S.ring[s1]) + Q.qo;
   double(*FYs)[NT] = S.fy[z & 1];
@@ -319,21 +327,21 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
         const double rn0 = syr - sy;
         const double sz0 = (nxt[r].r00 + 2.0 * cur[r].r00) + rn0;
         nxt[r].r00 = rn0;
-        const double d00 = (beta * (u0p - u00) + w * sz0) * WA(yb);
+        const double d00 = DS(0, yb & 3, u0p - u00, sz0);
         o3v[r] = d00;
         const double f0 = mcC[r + 1] * d00;
         o0v[r] = (sp_up(f0) - f0) * ih;
         const double rn1 = sp_up(dy) + sp_dn(dy) + 2.0 * dy;
         const double sz1 = (nxt[r].r01 + 2.0 * cur[r].r01) + rn1;
         nxt[r].r01 = rn1;
-        f2[r] = mu01[r] * ((beta * (u00 - um0) + w * sz1) * WB(fl01x));
+        f2[r] = mu01[r] * DS(1, fl01x, u00 - um0, sz1);
         const double tn = syl + syr + 2.0 * sy;
-        nxt[r].f02 = mu02p[r] * ((beta * (v00 - u00) + w * (tn - cur[r].t0)) * WI((yb & 3) | fl01x));
+        nxt[r].f02 = mu02p[r] * DS(3, (yb & 3) | fl01x, v00 - u00, tn - cur[r].t0);
         nxt[r].t0 = tn;
         m0[r] = mass_head(cur[r].q0, nxt[r].q0, (r == 0 ? 0 : QJ));
         const bool ok = IN || (zin && (xb & 8) && (yb & 8));  // outside: zero-filled u and media give 0
         const double qn =
-            ok ? mdq(sp_ld(M1, ORH + r * MROW - 8) + rpC[r + 1], sp_ld(M1, OGA + r * MROW - 8) + gpC[r + 1], ix, v00, vo[r])
+            ok ? mdq(sp_ld(M1, ORH + r * MROW - 8) + rpC[r + 1], sp_ld(M1, OGA + r * MROW - 8) + gpC[r + 1], ix, ix * w2, v00, vo[r])
                : 0.0;
         nxt[r].q0 = qn;
         nxt[r].u0 = v00;
@@ -362,20 +370,20 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
         const double rn0 = sp_up(dy) + sp_dn(dy) + 2.0 * dy;
         const double sz0 = (nxt[r].r11 + 2.0 * cur[r].r11) + rn0;
         nxt[r].r11 = rn0;
-        const double d11 = (beta * (up0 - u00) + w * sz0) * WB(xl << 2);
+        const double d11 = DS(1, xl << 2, up0 - u00, sz0);
         o3v[r] += d11;
         f1[r] = mcC[r + 1] * d11;
         const double rn1 = sy - syl;
         const double sz1 = (nxt[r].r10 + 2.0 * cur[r].r10) + rn1;
         nxt[r].r10 = rn1;
-        const double f3 = mu01[r] * ((beta * (u00 - u0m) + w * sz1) * WB(fl10));
+        const double f3 = mu01[r] * DS(1, fl10, u00 - u0m, sz1);
         o1v[r] = (f3 - sp_dn(f3)) * ih;
         const double tn = syl + syr + 2.0 * sy;
-        nxt[r].f12 = mu12p[r] * ((beta * (v00 - u00) + w * (tn - cur[r].t1)) * WI(xl | fl10));
+        nxt[r].f12 = mu12p[r] * DS(3, xl | fl10, v00 - u00, tn - cur[r].t1);
         nxt[r].t1 = tn;
         m1[r] = mass_head(cur[r].q1, nxt[r].q1, QC + (r == 0 ? 0 : QJ));
         const bool ok = IN || (zin && (xb & 16) && (yb & 16));
-        const double qn = ok ? mdq(rpC[r] + rpC[r + 1], gpC[r] + gpC[r + 1], iy[r], v00, vo[r]) : 0.0;
+        const double qn = ok ? mdq(rpC[r] + rpC[r + 1], gpC[r] + gpC[r + 1], iy[r], iy[r] * w2, v00, vo[r]) : 0.0;
         nxt[r].q1 = qn;
         nxt[r].u1 = v00;
         if (r == 0) *reinterpret_cast<double*>(QN + QC) = qn;
@@ -402,21 +410,21 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
         const double rn0 = sy - syl;
         const double sz0 = (nxt[r].r20 + 2.0 * cur[r].r20) + rn0;
         nxt[r].r20 = rn0;
-        const double f4 = cur[r].mu02 * ((beta * (u00 - u0m) + w * sz0) * WC(yb & 3));
+        const double f4 = cur[r].mu02 * DS(2, yb & 3, u00 - u0m, sz0);
         o2v[r] = (f4 - sp_dn(f4)) * ih;
         const double rn1 = sp_up(dy) + sp_dn(dy) + 2.0 * dy;
         const double sz1 = (nxt[r].r21 + 2.0 * cur[r].r21) + rn1;
         nxt[r].r21 = rn1;
-        f5[r] = cur[r].mu12 * ((beta * (u00 - um0) + w * sz1) * WC(xl));
+        f5[r] = cur[r].mu12 * DS(2, xl, u00 - um0, sz1);
         const double tn = syl + syr + 2.0 * sy;
-        const double d22 = (beta * (v00 - u00) + w * (tn - cur[r].t2)) * WI(xl | ((yb & 3) << 2));
+        const double d22 = DS(3, xl | ((yb & 3) << 2), v00 - u00, tn - cur[r].t2);
         o3v[r] += d22;
         nxt[r].f22 = mcC[r + 1] * d22;  // zero-filled mu masks cells outside the box
         nxt[r].t2 = tn;
         m2[r] = mass_head(cur[r].q2, nxt[r].q2, 2 * QC + (r == 0 ? 0 : QJ));
         const bool ok = IN || (zin2 && (xb & 16) && (yb & 8));
         const double qn = ok ? mdq(sp_ld(M0, ORH + r * MROW) + rpC[r + 1], sp_ld(M0, OGA + r * MROW) + gpC[r + 1], izp,
-                                   v00, vo[r])
+                                   IN ? ZT[9] : izp * w2, v00, vo[r])
                              : 0.0;
         nxt[r].q2 = qn;
         nxt[r].u2 = v00;
@@ -457,7 +465,7 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
       mm += wn * (r > 0 ? cur[r > 0 ? r - 1 : 0].q0 : sp_ld(SQ, (NQ - 1) * QJ - 256));
       mm += wn * (r < NY - 1 ? cur[r < NY - 1 ? r + 1 : r].q0 : sp_ld(SQ, 256));
       mm += wn * nxt[r].q0;
-      a0 -= mm * (IN ? ZT[3] : IM(cx1 + cy0 + czz));
+      a0 -= mm * (IN ? ZT[6] : IM(cx1 + cy0 + czz));
       a0 += pt0[r];
       const double f1p = r > 0 ? f1[r > 0 ? r - 1 : 0] : FYs[0][t - 32];
       a1 += (f1p - f1[r]) * ih;
@@ -466,7 +474,7 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
       mm += wn * (r > 0 ? cur[r > 0 ? r - 1 : 0].q1 : sp_ld(SQ, QC + (NQ - 1) * QJ - 256));
       mm += wn * (r < NY - 1 ? cur[r < NY - 1 ? r + 1 : r].q1 : sp_ld(SQ, QC + 256));
       mm += wn * nxt[r].q1;
-      a1 -= mm * (IN ? ZT[3] : IM(cx0 + cy1 + czz));
+      a1 -= mm * (IN ? ZT[6] : IM(cx0 + cy1 + czz));
       a1 += (pc[r] - (r > 0 ? pc[r > 0 ? r - 1 : 0] : sp_ld(U, OP - ROW))) * ih;
       const double f5n = r < NY - 1 ? f5[r < NY - 1 ? r + 1 : r] : FYs[2][t + 32];
       a2 += (f5[r] - f5n) * ih;
@@ -475,7 +483,7 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
       mm += wn * (r > 0 ? cur[r > 0 ? r - 1 : 0].q2 : sp_ld(SQ, 2 * QC + (NQ - 1) * QJ - 256));
       mm += wn * (r < NY - 1 ? cur[r < NY - 1 ? r + 1 : r].q2 : sp_ld(SQ, 2 * QC + 256));
       mm += wn * nxt[r].q2;
-      a2 -= mm * (IN ? ZT[4] : IM(cx0 + cy0 + lz + hz1));
+      a2 -= mm * (IN ? ZT[7] : IM(cx0 + cy0 + lz + hz1));
       a2 += pt2[r] * ih;
       if (hasb) {
         a0 = sp_ld(BP, r * 256) - a0;
@@ -677,21 +685,30 @@ inline bool launch_stencil3d_sp(const Geo& g, const OpPar& P, const double* medi
   return true;
 }
 
-// complex128 production dispatch. EHMG_SP_NW = 0 selects k_stencil3d_rr.
+// complex128 production dispatch. k_stencil3d_sp (8 warps x 2 rows) on levels
+// wide enough to fill its 14 x 14 tiles (256^3: 1.08 vs 1.13 ms per residual);
+// k_stencil3d_rr below that, where its 30 x 6 tiles quantise better (128^3:
+// 0.184 vs 0.216 ms). EHMG_SP_NW = 0 selects k_stencil3d_rr everywhere;
+// EHMG_SP_MIN_N overrides the width threshold (A/B builds).
 #ifndef EHMG_SP_NW
 #define EHMG_SP_NW 8
 #endif
 #ifndef EHMG_SP_NY
 #define EHMG_SP_NY 2
 #endif
+#ifndef EHMG_SP_MIN_N
+#define EHMG_SP_MIN_N 192
+#endif
 inline void launch_stencil3d(const Geo& g, const OpPar& P, const double* media_soa, const cplx* x, const cplx* b,
                              cplx* y, cudaStream_t s, int z_lo = 0, int z_hi = -1) {
 #if EHMG_SP_NW > 0
-  if (!launch_stencil3d_sp<SPCfg<EHMG_SP_NW, EHMG_SP_NY>>(g, P, media_soa, x, b, y, s, z_lo, z_hi))
-    throw std::runtime_error("ehmg: 3D stencil tensor maps could not be encoded");
-#else
-  launch_stencil3d_c128_rr(g, P, media_soa, x, b, y, s, z_lo, z_hi);
+  if (g.n[0] >= EHMG_SP_MIN_N && g.n[1] >= EHMG_SP_MIN_N) {
+    if (!launch_stencil3d_sp<SPCfg<EHMG_SP_NW, EHMG_SP_NY>>(g, P, media_soa, x, b, y, s, z_lo, z_hi))
+      throw std::runtime_error("ehmg: 3D stencil tensor maps could not be encoded");
+    return;
+  }
 #endif
+  launch_stencil3d_c128_rr(g, P, media_soa, x, b, y, s, z_lo, z_hi);
 }
 
 }  // namespace ehmg
