@@ -35,9 +35,11 @@ sys.path.insert(0, ROOT)
 # workload: BASELINE.json configs[2]
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
 # kernel from one `ncu --set full` capture of the same residual at 256^3
-# (distinct b and x; profiles/round1/ncu_stencil3d_rr_residual.txt).
-NCU_TRAFFIC = {"residual@L0": 2867563000 + 1056688000,
-               "source": "profiles/round2/ncu_stencil3d_rr_residual_r2.txt (ncu --set full, 256^3 residual)"}
+# (distinct b and x; k_stencil3d_sp<8, 2>, profiles/round2/ncu_stencil3d_sp82_residual.txt:
+# 11% above the algorithmic bytes: the 18 x 18 windows of the 14 x 14 tiles re-read their halo
+# rows where the neighbouring tile's copy has left L2).
+NCU_TRAFFIC = {"residual@L0": 3113847000 + 1063663000,
+               "source": "profiles/round2/ncu_stencil3d_sp82_residual.txt (ncu --set full, 256^3 residual)"}
 N_CELLS = 256
 LEVELS = 5  # at 256^3: coarsest level 16^3 cells (17^3 nodes), BASELINE configs[2]
 
@@ -199,8 +201,10 @@ def alg_bytes(kernel, n, level):
         return 16 * 3 * N + 32 * C
     if kernel == "apply":
         return 16 * 2 * N + 32 * C
-    if kernel == "vanka_update":   # colour-half of the factor cache, r and x at the owned DOFs
-        return 16 * 13 * (C // 2) + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
+    if kernel == "vanka_update":
+        # colour-half of the stiffness cache (12 reals of K + 1/s per cell), rho and gamma of every
+        # cell once (the mass part of the local blocks is rebuilt from them), r and x at the owned DOFs
+        return 8 * 14 * (C // 2) + 16 * C + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
     if kernel == "restrict":
         return 16 * N + 16 * ndofs(level_dims(n, level + 1))
     if kernel == "prolong_add":
@@ -529,10 +533,12 @@ def run_b200(args, ws, rank, local):
                      "traffic": (NCU_TRAFFIC.get(f"{kname}@L{klev}")
                                  if args.workload == "c2" and n == (N_CELLS,) * 3 else None),
                      "traffic_source": NCU_TRAFFIC["source"], "alg_bytes_per_launch": nbytes,
-                     "limiter": ("latency at 2 warps/scheduler (8 warps x 255 registers): LSU 71% and FP64 41% "
-                                 "of peak, IPC 1.73; stalls 26% short-scoreboard (LDS/SHFL results), 26% FP64 "
-                                 "dependency waits, 7% block barrier; 418 B of shared/shuffle traffic per DOF vs "
-                                 "56 B of HBM (profiles/round2/ncu_stencil3d_rr_residual_r2.txt; DESIGN.md)"),
+                     "limiter": ("instruction issue at 2 warps/scheduler (8 warps x 255 registers, 2 rows per "
+                                 "thread): 564 M warp instructions per launch (43% FP64, 20% LDS/SHFL) at IPC 1.91; "
+                                 "each pipe alone would allow 0.44 ms (FP64, 2 issue cycles per warp DFMA), 0.65 ms "
+                                 "(184 M shared-memory wavefronts) and 0.58 ms (HBM) -- the launch needs all three "
+                                 "overlapped; stalls: 29% fixed-latency FP64 waits, 17% LDS/SHFL results, 6% block "
+                                 "barrier (profiles/round2/ncu_stencil3d_sp82_residual.txt; DESIGN.md)"),
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "smoother_colour_pass_L0": smoother_pass, "clocks": clocks,
     }

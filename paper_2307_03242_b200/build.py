@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
-LIB = os.path.join(LIBDIR, "libehmg_b200.so")
+LIB = os.environ.get("EHMG_B200_LIB") or os.path.join(LIBDIR, "libehmg_b200.so")  # override: A/B builds
 SOURCES = ["ehmg_solver.cu"]
 HEADERS = ["ehmg_core.cuh", "ehmg_kernels.cuh", "ehmg_stencil2d.cuh", "ehmg_stencil3d.cuh", "ehmg_stencil3d_rr.cuh", "ehmg_stencil3d_sp.cuh", "ehmg_media.cuh", "ehmg_slab.cuh", "ehmg_comm.cuh", "ehmg_solver.cu"]
 

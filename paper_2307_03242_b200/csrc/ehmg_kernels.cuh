@@ -177,6 +177,10 @@ EH_HD int64_t colour_index(const Geo& g, const int* c) {
 struct VkPar {
   double beta, w, ih;
   double inv_wsum[16];  // by transverse validity bits of dspread_cell
+  // face mass of the local blocks (operator.hpp:131-155, :358-383), for the
+  // stiffness-cache update (k_vanka_update_k)
+  double wn, omega2, alpha;
+  double inv_msum[7];  // 1/(beta + k*wn), k valid mass neighbours
 };
 
 inline VkPar make_vkpar(const Geo& g, const OpPar& P) {
@@ -203,6 +207,14 @@ inline VkPar make_vkpar(const Geo& g, const OpPar& P) {
       }
     }
     v.inv_wsum[f] = P.beta != 1.0 ? 1.0 / wsum : 1.0;
+  }
+  v.wn = (1.0 - P.beta) / (2.0 * g.nd);
+  v.omega2 = P.omega2;
+  v.alpha = P.alpha;
+  for (int c = 0; c <= 6; ++c) {
+    double wsum = P.beta;
+    for (int q = 0; q < c; ++q) wsum += v.wn;
+    v.inv_msum[c] = P.beta != 1.0 ? 1.0 / wsum : 1.0;
   }
   return v;
 }
@@ -376,6 +388,186 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k
     if constexpr (XZERO) {
       // the x-partner (other colour): its p, and its faces on the domain
       // boundary (interior faces belong to a cell of this colour)
+      int pc[3] = {c[0] ^ 1, c[1], c[2]};
+      x[g.off[ND] + g.clin(pc)] = zero;
+#pragma unroll
+      for (int k = 0; k < ND; ++k) {
+        if (pc[k] == 0) x[g.off[k] + g.flin(k, pc)] = zero;
+        if (pc[k] == g.n[k] - 1) {
+          int f1[3];
+          sh(pc, k, 1, f1);
+          x[g.off[k] + g.flin(k, f1)] = zero;
+        }
+      }
+    }
+  }
+}
+
+// ---- stiffness cache (3D, full Vanka, complex128 levels and z-windows)
+// The 2x2 local block of component k is U = K - M: K collects the flux terms,
+// whose coefficients are all real (operator.hpp:263-355), M the face mass
+// spread, M_ij = (i == j ? beta : wn) md(f_j) / wsum(f_i) with md = w^2 rho_f
+// (1 - i(gamma_f + alpha)) (operator.hpp:131-155, :358-383). Instead of the 12
+// complex entries of Uinv the cache keeps the 12 reals of K (and 1/s); the
+// update rebuilds M from the cell's and its six neighbours' rho / gamma,
+// forms U = K - M and inverts it as vanka.hpp:107-113 does. 112 instead of
+// 208 cache bytes per cell against ~32 bytes of media: the HBM-bound colour
+// update moves ~12% fewer bytes. Results agree with the Uinv cache to
+// rounding (K is recovered from Uinv at set-up: U = Uinv^-1, K = Re(U + M)).
+constexpr int kVkK = 14;  // doubles per cell: K[3][4], Re 1/s, Im 1/s
+
+__device__ __forceinline__ cplx vk_inv2(const cplx* U, cplx* Ui) {  // vanka.hpp:107-113
+  const cplx det = U[0] * U[3] - U[1] * U[2];
+  const double rd = 1.0 / (det.x * det.x + det.y * det.y);  // one division: 1/det = conj(det) / |det|^2
+  const cplx idet = mk(det.x * rd, -det.y * rd);
+  Ui[0] = U[3] * idet;
+  Ui[1] = -U[1] * idet;
+  Ui[2] = -U[2] * idet;
+  Ui[3] = U[0] * idet;
+  return det;
+}
+
+// Mass part M[k][4] of the three local blocks of cell c from the SoA media
+// (rho, gam: cell arrays of the level, or of its z-window: boundary rules
+// follow the global planes (g.zoff / g.gn2); a z neighbour the window does not
+// hold reads as zero, which only touches the outermost ghost planes, and
+// set-up and update see the same M, so U = K - M is reproduced either way).
+__device__ __forceinline__ void vk_mass_blocks(const Geo& g, const VkPar& V, const double* __restrict__ rho,
+                                               const double* __restrict__ gam, const int* c, cplx (*M)[4]) {
+  const int64_t ci = g.clin(c);
+  const double r0 = rho[ci], g0 = gam[ci];
+  const int64_t st[3] = {1, g.n[0], (int64_t)g.n[0] * g.n[1]};
+  const int cg[3] = {c[0], c[1], c[2] + g.zoff};
+  const int L[3] = {g.n[0], g.n[1], g.gn2};
+  // valid mass neighbours of a face across the axes other than k: both faces of
+  // the cell share them (the face box equals the cell box on those axes)
+  int tr[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) tr[a] = (cg[a] >= 1) + (cg[a] + 1 < L[a]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const bool lo = cg[k] >= 1, hi = cg[k] + 1 < L[k];
+    const bool llo = lo && c[k] >= 1, lhi = hi && c[k] + 1 < g.n[k];  // present in this array
+    // face f0 = c: cells c - e_k (if inside) and c; face f1 = c + e_k: cells c and c + e_k (if inside)
+    const double rl = llo ? rho[ci - st[k]] : 0.0, gl = llo ? gam[ci - st[k]] : 0.0;
+    const double rh = lhi ? rho[ci + st[k]] : 0.0, gh = lhi ? gam[ci + st[k]] : 0.0;
+    const double i0 = lo ? 0.5 : 1.0, i1 = hi ? 0.5 : 1.0;
+    const double rf0 = (rl + r0) * i0, gf0 = (gl + g0) * i0 + V.alpha;
+    const double rf1 = (r0 + rh) * i1, gf1 = (g0 + gh) * i1 + V.alpha;
+    const cplx md0 = mk(V.omega2 * rf0, -V.omega2 * gf0 * rf0), md1 = mk(V.omega2 * rf1, -V.omega2 * gf1 * rf1);
+    // along k: face index c[k] has neighbours c[k]-1 (if >= 0) and c[k]+1 (<= n_k: always); face c[k]+1
+    // has c[k] (always) and c[k]+2 (if <= n_k)
+    const int other = tr[(k + 1) % 3] + tr[(k + 2) % 3];
+    const double im0 = V.inv_msum[other + (lo ? 2 : 1)], im1 = V.inv_msum[other + (hi ? 2 : 1)];
+    M[k][0] = (V.beta * im0) * md0;
+    M[k][1] = (V.wn * im0) * md1;
+    M[k][2] = (V.wn * im1) * md0;
+    M[k][3] = (V.beta * im1) * md1;
+  }
+}
+
+// Set-up: K and 1/s of every cell from the compact Uinv cache.
+__global__ void k_vanka_kcache(Geo g, VkPar V, const double* __restrict__ rho, const double* __restrict__ gam,
+                               const cplx* __restrict__ soa, double* __restrict__ ksoa) {
+  const int64_t nt = colour_threads(g);
+  GRID_STRIDE(u, 2 * nt) {
+    const int col = (int)(u / nt);
+    const int64_t t = u % nt;
+    int c[3];
+    if (!colour_cell(g, t, col, c)) continue;
+    cplx M[3][4];
+    vk_mass_blocks(g, V, rho, gam, c, M);
+    const cplx* q = soa + (int64_t)col * 13 * nt + t;
+    double* o = ksoa + (int64_t)col * kVkK * nt + t;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      cplx Ui[4], U[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Ui[e] = q[(int64_t)(4 * k + e) * nt];
+      vk_inv2(Ui, U);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[(int64_t)(4 * k + e) * nt] = U[e].x + M[k][e].x;
+    }
+    const cplx sinv = q[(int64_t)12 * nt];
+    o[(int64_t)12 * nt] = sinv.x;
+    o[(int64_t)13 * nt] = sinv.y;
+  }
+}
+
+// Red-black colour update from the stiffness cache (see above); otherwise as
+// k_vanka_update<3, cplx, XZERO> (full mode).
+// 12 warps per SM at 168 registers: the block inversions lengthen each cell's
+// arithmetic, and the extra warps keep the HBM pipe fed meanwhile (256^3 colour
+// update: 0.75 ms at 8 warps, 0.70 at 12, 0.89 at 14 with spills)
+#ifndef EHMG_VKK_THREADS
+#define EHMG_VKK_THREADS 384
+#endif
+constexpr int kVkkThreads = EHMG_VKK_THREADS;
+template <bool XZERO>
+__global__ void __launch_bounds__(kVkkThreads, 1)
+    k_vanka_update_k(Geo g, VkPar V, const double* __restrict__ ksoa, const double* __restrict__ rho,
+                     const double* __restrict__ gam, const cplx* __restrict__ r, int color, double w,
+                     cplx* __restrict__ x) {
+  constexpr int ND = 3;
+  const cplx zero = mk(0, 0);
+  const int64_t nt = colour_threads(g);
+  GRID_STRIDE(t, nt) {
+    int c[3];
+    if (!colour_cell(g, t, color, c)) continue;
+    const double* q = ksoa + (int64_t)color * kVkK * nt + t;
+    const int64_t pi = g.off[ND] + g.clin(c);
+    int64_t fi[ND][2];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      int f1[3];
+      sh(c, k, 1, f1);
+      fi[k][0] = g.off[k] + g.flin(k, c);
+      fi[k][1] = g.off[k] + g.flin(k, f1);
+    }
+    // every load of the cell is issued before any arithmetic
+    double K[ND][4];
+    cplx rr[ND][2], xx[ND][2];
+    const cplx rp = r[pi], xp = XZERO ? zero : x[pi];
+    const cplx sinv = mk(q[(int64_t)12 * nt], q[(int64_t)13 * nt]);
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      rr[k][0] = r[fi[k][0]];
+      rr[k][1] = r[fi[k][1]];
+      xx[k][0] = XZERO ? zero : x[fi[k][0]];
+      xx[k][1] = XZERO ? zero : x[fi[k][1]];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) K[k][e] = q[(int64_t)(4 * k + e) * nt];
+    }
+    cplx M[ND][4];
+    vk_mass_blocks(g, V, rho, gam, c, M);
+    cplx U[ND][4];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      cplx A[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) A[e] = mk(K[k][e] - M[k][e].x, -M[k][e].y);
+      vk_inv2(A, U[k]);
+    }
+    cplx dpa = rp;
+    const cplx b0 = mk(V.ih, 0), b1 = mk(-V.ih, 0);
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const double c0 = vk_c0<ND>(V, g, k, c);
+      const cplx k0 = mk(c0, 0), k1 = mk(-c0, 0);
+      const cplx h0 = k0 * U[k][0] + k1 * U[k][2], h1 = k0 * U[k][1] + k1 * U[k][3];
+      dpa -= h0 * rr[k][0] + h1 * rr[k][1];
+    }
+    const cplx dp = sinv * dpa;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const cplx g0 = U[k][0] * b0 + U[k][1] * b1, g1 = U[k][2] * b0 + U[k][3] * b1;
+      const cplx du0 = U[k][0] * rr[k][0] + U[k][1] * rr[k][1] - g0 * dp;
+      const cplx du1 = U[k][2] * rr[k][0] + U[k][3] * rr[k][1] - g1 * dp;
+      x[fi[k][0]] = xx[k][0] + w * du0;
+      x[fi[k][1]] = xx[k][1] + w * du1;
+    }
+    x[pi] = xp + w * dp;
+    if constexpr (XZERO) {
       int pc[3] = {c[0] ^ 1, c[1], c[2]};
       x[g.off[ND] + g.clin(pc)] = zero;
 #pragma unroll

@@ -595,7 +595,7 @@ static std::unique_ptr<ehmg_slab_mg_s> build_slab_mg(const Geo& g0, const double
       sl->local = sm->local(q);
       if (sl->local) {
         sl->media.window_of(*gm[l], sm->G[l], w0, w1, s);
-        sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1);
+        sl->sm.build(sm->G[l], P, gm[l]->packed.p, opt.vanka_mode == 0 ? 1 : 0, s, w0, w1, sl->media.soa.p);
         const int64_t nd = sl->sg.g.ndofs;
         // two halves per inbox (exchanges alternate between them)
         const int64_t ilo = 2 * ehmg_slab_mg_s::inbox_half(sl->sg, false);

@@ -308,6 +308,11 @@ struct Smoother {
   VkPar vk;
   DBuf<cplx> soa, res;
   DBuf<cplxf> soaf, resf;  // complex64 cache / residual (single-precision hierarchy)
+  // stiffness cache (k_vanka_update_k): 3D full Vanka on complex128 levels / z-windows
+  DBuf<double> ksoa;
+  const double* mrho = nullptr;
+  const double* mgam = nullptr;
+  bool kpath = false;
   // switch this smoother to complex64 storage (the double cache is released)
   void make_float(const Geo& g, cudaStream_t s) {
     soaf.alloc(soa.n);
@@ -316,6 +321,8 @@ struct Smoother {
     CK(cudaStreamSynchronize(s));
     soa.release();
     res.release();
+    ksoa.release();
+    kpath = false;
     resf.alloc(g.ndofs);
   }
   const cplx* cache(const cplx*) const { return soa.p; }
@@ -325,7 +332,7 @@ struct Smoother {
   // Cache for the cells of `gg` (global grid, global packed media m), or of
   // its z-window [z0, z1) when z1 >= 0; sweeps then run on the window geometry.
   void build(const Geo& gg, const OpPar& P, const Cell* m, int full_, cudaStream_t s, int z0 = 0,
-             int z1 = -1) {
+             int z1 = -1, const double* media_soa = nullptr) {
     full = full_;
     stride = gg.nd * ((full ? 4 : 2) + 4) + 1;
     const Geo g = z1 < 0 ? gg : make_window(gg, z0, z1);
@@ -359,6 +366,17 @@ struct Smoother {
       CK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (hb) throw Err(EHMG_ERUNTIME, "vanka: singular local cell system");
+      // stiffness cache for the colour updates (EHMG_VANKA_KCACHE=0 keeps the Uinv cache)
+      const char* ev = getenv("EHMG_VANKA_KCACHE");
+      kpath = false;
+      if (g.nd == 3 && full && media_soa && g.n[0] % 2 == 0 && !(ev && ev[0] == '0')) {
+        ksoa.alloc(2 * nt * kVkK);
+        mrho = media_soa + g.ncells;
+        mgam = media_soa + 2 * g.ncells;
+        k_vanka_kcache<<<grid_for(2 * nt, 148 * 64), kThreads, 0, s>>>(g, vk, mrho, mgam, soa.p, ksoa.p);
+        CK(cudaGetLastError());
+        kpath = true;
+      }
     }
     res.alloc(g.ndofs);
   }
@@ -406,6 +424,14 @@ struct Smoother {
     const int lc = color ^ (g.zoff & 1);
     const V* cq = cache(r);
     Prof pf("vanka_update", s);
+    if constexpr (sizeof(V) == sizeof(cplx)) {
+      if (kpath && g.nd == 3) {
+        (xzero ? k_vanka_update_k<true> : k_vanka_update_k<false>)<<<(int)std::min<int64_t>((nt + kVkkThreads - 1) / kVkkThreads, 148 * 64), kVkkThreads, 0, s>>>(
+            g, vk, ksoa.p, mrho, mgam, r, lc, w, x);
+        CK(cudaGetLastError());
+        return;
+      }
+    }
     if (g.nd == 3)
       (xzero ? k_vanka_update<3, V, true> : k_vanka_update<3, V, false>)<<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(
           g, vk, full, cq, r, lc, w, x);
@@ -1154,7 +1180,7 @@ static std::unique_ptr<ehmg_mg_s> build_mg(const Geo& g, const double* const* ho
     }
     const bool coarsest = (l + 1 == nlevels);
     if (!coarsest) {
-      lev->sm.build(lev->g, P, lev->media.packed.p, opt.vanka_mode == 0 ? 1 : 0, s);
+      lev->sm.build(lev->g, P, lev->media.packed.p, opt.vanka_mode == 0 ? 1 : 0, s, 0, -1, lev->media.soa.p);
       if (mixed) {
         lev->sm.make_float(lev->g, s);
         lev->rf.alloc(lev->g.ndofs);
@@ -1346,7 +1372,7 @@ int ehmg_vanka_create(ehmg_op op, int mode, ehmg_vanka* out) {
   return guard([&] {
     auto v = std::make_unique<ehmg_vanka_s>();
     v->op = op;
-    v->sm.build(op->g, op->P, op->media.packed.p, mode == 0 ? 1 : 0, op->s);
+    v->sm.build(op->g, op->P, op->media.packed.p, mode == 0 ? 1 : 0, op->s, 0, -1, op->media.soa.p);
     *out = v.release();
   });
 }

@@ -102,36 +102,55 @@ __device__ __forceinline__ bool sp_elect() {
   return pred != 0;
 }
 
-// The per-plane load group of step z, spread over the warps: load i of
-// {u0, u1, u2, p, mu, rho, gam, ilm, b0..b3} (the order of the maps in R3Maps)
-// is issued by warp i % NW, so no warp carries the whole issue sequence into
-// the plane's barrier. u and media planes z + 2, p and b planes z + 1. The
-// expect-tx arrival is warp 0's; a completion that lands first only drives
-// the transaction count negative until then.
+// The per-plane load group of step z, spread over warps 0..7 (one or two
+// loads each, straight-line code with compile-time offsets), so no warp
+// carries the whole issue sequence into the plane's barrier: u and media
+// planes z + 2 go to ring slot sl2, p and b planes z + 1 to sl1. The expect-tx
+// arrival is warp 0's; a completion that lands first only drives the
+// transaction count negative until then. Map order in R3Maps: u0 u1 u2 p mu
+// rho gam ilm b0..b3.
 template <class K>
 __device__ __forceinline__ void sp_issue_step(SPSmem<K>& S, const R3Maps& RM, int warp, int i0, int j0, int z,
-                                              bool hasb, unsigned long long* bar) {
+                                              int sl1, int sl2, bool hasb, unsigned long long* bar) {
   typedef SPSlot<K> SL;
-  const int nl = hasb ? 12 : 8;
-  if (warp >= nl) return;
+  static_assert(K::NW >= 8, "eight issuing warps");
+  if (warp >= 8) return;
   if (!sp_elect()) return;
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  if (warp == 0)
-    s3_expect(bar, (unsigned)(3 * K::CBYTES + 4 * K::MBYTES + K::CBYTES + (hasb ? 4 * K::BBYTES : 0)));
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(&RM);
-  const int sl2 = s3_mod3(z + 2), sl1 = s3_mod3(z + 1);
-  for (int i = warp; i < nl; i += K::NW) {
-    int soff, c0, c1, zz, sl;
-    if (i < 3) {
-      soff = (int)offsetof(SL, u) + i * K::US * 16, c0 = 2 * (i0 - 2), c1 = j0 - 2, zz = z + 2, sl = sl2;
-    } else if (i == 3) {
-      soff = (int)offsetof(SL, p), c0 = 2 * (i0 - 2), c1 = j0 - 2, zz = z + 1, sl = sl1;
-    } else if (i < 8) {
-      soff = (int)offsetof(SL, mu) + (i - 4) * K::MS * 8, c0 = i0 - 2, c1 = j0 - 2, zz = z + 2, sl = sl2;
-    } else {
-      soff = (int)offsetof(SL, bp) + (i - 8) * K::FN * 16, c0 = 2 * (i0 - 1), c1 = j0 - 1, zz = z + 1, sl = sl1;
-    }
-    s3_tma(reinterpret_cast<char*>(&S.ring[sl]) + soff, maps + i, c0, c1, zz, bar);
+  char* D2 = reinterpret_cast<char*>(&S.ring[sl2]);
+  char* D1 = reinterpret_cast<char*>(&S.ring[sl1]);
+  const int cx = 2 * (i0 - 2), cy = j0 - 2, mx = i0 - 2, bx = 2 * (i0 - 1), by = j0 - 1;
+  constexpr int OU = (int)offsetof(SL, u), OPP = (int)offsetof(SL, p), OM = (int)offsetof(SL, mu),
+                OB = (int)offsetof(SL, bp), CU = K::US * 16, CM = K::MS * 8, CB = K::FN * 16;
+  switch (warp) {
+    case 0:
+      s3_expect(bar, (unsigned)(3 * K::CBYTES + 4 * K::MBYTES + K::CBYTES + (hasb ? 4 * K::BBYTES : 0)));
+      s3_tma(D2 + OU, maps + 0, cx, cy, z + 2, bar);
+      break;
+    case 1: s3_tma(D2 + OU + CU, maps + 1, cx, cy, z + 2, bar); break;
+    case 2: s3_tma(D2 + OU + 2 * CU, maps + 2, cx, cy, z + 2, bar); break;
+    case 3: s3_tma(D1 + OPP, maps + 3, cx, cy, z + 1, bar); break;
+    case 4:
+      s3_tma(D2 + OM, maps + 4, mx, cy, z + 2, bar);
+      s3_tma(D2 + OM + CM, maps + 5, mx, cy, z + 2, bar);
+      break;
+    case 5:
+      s3_tma(D2 + OM + 2 * CM, maps + 6, mx, cy, z + 2, bar);
+      s3_tma(D2 + OM + 3 * CM, maps + 7, mx, cy, z + 2, bar);
+      break;
+    case 6:
+      if (hasb) {
+        s3_tma(D1 + OB, maps + 8, bx, by, z + 1, bar);
+        s3_tma(D1 + OB + CB, maps + 9, bx, by, z + 1, bar);
+      }
+      break;
+    default:
+      if (hasb) {
+        s3_tma(D1 + OB + 2 * CB, maps + 10, bx, by, z + 1, bar);
+        s3_tma(D1 + OB + 3 * CB, maps + 11, bx, by, z + 1, bar);
+      }
+      break;
   }
 }
 
@@ -227,9 +246,9 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
 
   s3_wait(&S.bar[seq & 1], (seq >> 1) & 1);
   ++seq;
-  sp_issue_step<K>(S, maps, Q.warp, Q.i0, Q.j0, z, hasb, &S.bar[seq & 1]);
   const int s0 = su0, s1 = su0 == 2 ? 0 : su0 + 1;
   su0 = s1;
+  sp_issue_step<K>(S, maps, Q.warp, Q.i0, Q.j0, z, s1, 3 - s0 - s1, hasb, &S.bar[seq & 1]);
   const char* R0 = reinterpret_cast<const char*>(&S.ring[s0]);
   const char* R1 = reinterpret_cast<const char*>(&S.ring[s1]);
   const char* U = R0 + Q.uo;   // plane z, my part, first row
@@ -237,6 +256,11 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
   const char* VX = V + Q.xo;   // plane z + 1, the other part
   const char* M0 = R0 + Q.mo;
   const char* M1 = R1 + Q.mo;
+#ifdef EHMG_SP_RELOAD_U
+  auto CU_ = [&](int k, int r) -> double { return sp_ld(U, k * CU + r * ROW); };  // own u at plane z, reloaded
+#else
+  auto CU_ = [&](int k, int r) -> double { return k == 0 ? cur[r].u0 : k == 1 ? cur[r].u1 : cur[r].u2; };
+#endif
   const int zg = z + g.zoff;
   const int lz = zg >= 1, hz0 = zg + 1 < n2g, hz1 = zg + 1 < n2g + 1;
   const int zA = (lz << 2) | (hz0 << 3), zB = lz | (hz0 << 1), zC = (lz << 2) | (hz1 << 3);
@@ -321,7 +345,7 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
       for (int r = 0; r < NY; ++r) {
         const int yb = ybs[r];
         const double v00 = vc[r + 1];
-        const double u00 = cur[r].u0, u0p = sp_ld(U, r * ROW + 16), um0 = r == 0 ? ub : cur[r == 0 ? 0 : r - 1].u0;
+        const double u00 = CU_(0, r), u0p = sp_ld(U, r * ROW + 16), um0 = r == 0 ? ub : CU_(0, r == 0 ? 0 : r - 1);
         const double sy = vc[r] + vc[r + 2] + 2.0 * v00, syl = sp_up(sy), syr = sp_dn(sy);
         const double dy = v00 - vc[r];
         const double rn0 = syr - sy;
@@ -344,7 +368,9 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
             ok ? mdq(sp_ld(M1, ORH + r * MROW - 8) + rpC[r + 1], sp_ld(M1, OGA + r * MROW - 8) + gpC[r + 1], ix, ix * w2, v00, vo[r])
                : 0.0;
         nxt[r].q0 = qn;
+#ifndef EHMG_SP_RELOAD_U
         nxt[r].u0 = v00;
+#endif
         if (r == 0) *reinterpret_cast<double*>(QN) = qn;
         if (r == NY - 1 && NY > 1) *reinterpret_cast<double*>(QN + QJ) = qn;
       }
@@ -363,7 +389,7 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
         const int yb = ybs[r];
         const int fl10 = ((yb & 1) << 2) | ((yb & 4) << 1);
         const double v00 = vc[r + 1];
-        const double u00 = cur[r].u1, up0 = r == NY - 1 ? ut : cur[r == NY - 1 ? r : r + 1].u1,
+        const double u00 = CU_(1, r), up0 = r == NY - 1 ? ut : CU_(1, r == NY - 1 ? r : r + 1),
                      u0m = sp_ld(U, CU + r * ROW - 16);
         const double sy = vc[r] + vc[r + 2] + 2.0 * v00, syl = sp_up(sy), syr = sp_dn(sy);
         const double dy = vc[r + 2] - v00;
@@ -385,7 +411,9 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
         const bool ok = IN || (zin && (xb & 16) && (yb & 16));
         const double qn = ok ? mdq(rpC[r] + rpC[r + 1], gpC[r] + gpC[r + 1], iy[r], iy[r] * w2, v00, vo[r]) : 0.0;
         nxt[r].q1 = qn;
+#ifndef EHMG_SP_RELOAD_U
         nxt[r].u1 = v00;
+#endif
         if (r == 0) *reinterpret_cast<double*>(QN + QC) = qn;
         if (r == NY - 1 && NY > 1) *reinterpret_cast<double*>(QN + QC + QJ) = qn;
       }
@@ -403,8 +431,8 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
       for (int r = 0; r < NY; ++r) {
         const int yb = ybs[r];
         const double v00 = vc[r + 1];
-        const double u00 = cur[r].u2, u0m = sp_ld(U, 2 * CU + r * ROW - 16),
-                     um0 = r == 0 ? ub : cur[r == 0 ? 0 : r - 1].u2;
+        const double u00 = CU_(2, r), u0m = sp_ld(U, 2 * CU + r * ROW - 16),
+                     um0 = r == 0 ? ub : CU_(2, r == 0 ? 0 : r - 1);
         const double sy = vc[r] + vc[r + 2] + 2.0 * v00, syl = sp_up(sy), syr = sp_dn(sy);
         const double dy = v00 - vc[r];
         const double rn0 = sy - syl;
@@ -427,7 +455,9 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
                                    IN ? ZT[9] : izp * w2, v00, vo[r])
                              : 0.0;
         nxt[r].q2 = qn;
+#ifndef EHMG_SP_RELOAD_U
         nxt[r].u2 = v00;
+#endif
         if (r == 0) *reinterpret_cast<double*>(QN + 2 * QC) = qn;
         if (r == NY - 1 && NY > 1) *reinterpret_cast<double*>(QN + 2 * QC + QJ) = qn;
       }
@@ -521,6 +551,11 @@ __device__ __forceinline__ void sp_march(SPSmem<K>& S, const R3Maps& maps, const
     B[r] = c;
   }
   int su0 = s3_mod3(zs);
+#ifndef EHMG_SP_UNROLL
+#define EHMG_SP_UNROLL 1
+#endif
+  constexpr int kUnroll = EHMG_SP_UNROLL;
+#pragma unroll kUnroll
   for (int z = zs; z < zend; z += 2) {
     sp_step<K, IN>(S, maps, P, Q, hasb, z, su0, seq, A, B);
     sp_step<K, IN>(S, maps, P, Q, hasb, z + 1, su0, seq, B, A);
