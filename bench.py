@@ -202,9 +202,12 @@ def alg_bytes(kernel, n, level):
     if kernel == "apply":
         return 16 * 2 * N + 32 * C
     if kernel == "vanka_update":
-        # colour-half of the stiffness cache (12 reals of K + 1/s per cell), rho and gamma of every
-        # cell once (the mass part of the local blocks is rebuilt from them), r and x at the owned DOFs
-        return 8 * 14 * (C // 2) + 16 * C + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
+        if os.environ.get("EHMG_VANKA_KCACHE", "0")[:1] == "1":
+            # colour-half of the stiffness cache (12 reals of K + 1/s per cell), rho and gamma of every
+            # cell once (the mass part of the local blocks is rebuilt from them), r and x at the owned DOFs
+            return 8 * 14 * (C // 2) + 16 * C + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
+        # colour-half of the factor cache (13 complex per cell), r and x at the owned DOFs
+        return 16 * 13 * (C // 2) + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
     if kernel == "restrict":
         return 16 * N + 16 * ndofs(level_dims(n, level + 1))
     if kernel == "prolong_add":
