@@ -26,6 +26,7 @@ def _problem(dims, seed):
     ((24, 16, 64), 4, 4, 8, "w"),
     ((32, 32, 128), 4, 4, 16, "v"),
     ((16, 24, 48), 3, 2, 64, "v"),   # only the finest level sharded
+    ((192, 192, 32), 5, 2, 8, "v"),  # finest level on k_stencil3d_sp (>= 192 wide): windows, plane ranges
 ])
 def test_slab_cycle_equals_single_domain(dims, nl, ns, agg, cyc):
     g, m, b = _problem(dims, 3)
