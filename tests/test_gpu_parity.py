@@ -85,7 +85,7 @@ def test_golden_through_cuda(golden):
 # the last three run the split-part kernel k_stencil3d_sp (levels >= 192 wide): tiles inside the
 # box and on every boundary, one and several z-chunks
 @pytest.mark.parametrize("dims", [(64, 48), (128, 128), (24, 20, 16), (32, 32, 32), (40, 24, 36), (24, 20, 80), (66, 10, 12),
-                                  (200, 196, 6), (224, 193, 5), (192, 192, 40)])
+                                  (200, 196, 6), (224, 193, 5), (192, 192, 40), (192, 194, 2)])
 @pytest.mark.parametrize("beta", [1.0, 2 / 3])
 def test_apply_vs_oracle(dims, beta):
     rng = np.random.default_rng(hash((dims, beta)) % 2**32)
