@@ -316,8 +316,17 @@ __global__ void k_vanka_expand(Geo g, VkPar V, int full, const cplx* __restrict_
 // it owns. Cells of one colour share no DOFs, so the in-place writes commute.
 // T = cplx or cplxf: storage and arithmetic type (the single-precision
 // hierarchy updates in float, as the reference's VankaSmoother<float>).
-template <int ND, class T = cplx, bool XZERO = false>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == sizeof(cplx) ? 1 : 2) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
+// complex128 colour update: 12 warps per SM at 168 registers (one block per SM). All 27 complex
+// loads of a cell are still issued before any arithmetic; against 8 warps x 248 registers the
+// extra warps keep more HBM requests in flight: 256^3 update 0.727 -> 0.708 ms, 128^3 0.105 ->
+// 0.096 ms (0.739 at 11 warps, 0.90 at 13-14 warps, where 128 registers spill).
+#ifndef EHMG_VK_THREADS
+#define EHMG_VK_THREADS 384
+#endif
+constexpr int kVkThreads = EHMG_VK_THREADS;
+template <class T> constexpr int vk_threads() { return sizeof(T) == sizeof(cplx) ? kVkThreads : kThreads; }
+template <int ND, class T, bool XZERO>
+__global__ void __launch_bounds__(vk_threads<T>(), sizeof(T) == sizeof(cplx) ? 1 : 2) k_vanka_update(Geo g, VkPar V, int full, const T* __restrict__ soa,
                                                            const T* __restrict__ r, int color, double w,
                                                            T* __restrict__ x) {
   constexpr bool xzero = XZERO;  // compile-time: the regular update keeps its load schedule

@@ -433,12 +433,14 @@ struct Smoother {
         return;
       }
     }
+    constexpr int nth = vk_threads<V>();
+    const int nblk = (int)std::min<int64_t>((nt + nth - 1) / nth, 148 * 64);
     if (g.nd == 3)
-      (xzero ? k_vanka_update<3, V, true> : k_vanka_update<3, V, false>)<<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(
-          g, vk, full, cq, r, lc, w, x);
+      (xzero ? k_vanka_update<3, V, true> : k_vanka_update<3, V, false>)<<<nblk, nth, 0, s>>>(g, vk, full, cq, r, lc, w,
+                                                                                            x);
     else
-      (xzero ? k_vanka_update<2, V, true> : k_vanka_update<2, V, false>)<<<grid_for(nt, 148 * 64), kThreads, 0, s>>>(
-          g, vk, full, cq, r, lc, w, x);
+      (xzero ? k_vanka_update<2, V, true> : k_vanka_update<2, V, false>)<<<nblk, nth, 0, s>>>(g, vk, full, cq, r, lc, w,
+                                                                                            x);
     CK(cudaGetLastError());
   }
 };
