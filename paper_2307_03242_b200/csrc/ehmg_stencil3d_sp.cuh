@@ -477,12 +477,8 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
   }
   __syncthreads();
 
-#ifdef EHMG_SP_COLBRANCH
+  // (running the halo columns through the rows under a uniform branch, stores masked, measured no faster)
   if ((xb & 32) && z >= Q.zb) {
-#else
-  // (halo columns run the rows too -- a uniform branch -- and only their stores are masked)
-  if (z >= Q.zb) {
-#endif
     const char* SQ = R0 + Q.qo;
     const char* BP = R0 + Q.bo;
     const int czz = lz + hz0;
@@ -526,9 +522,8 @@ __device__ __forceinline__ void sp_step(SPSmem<K>& S, const R3Maps& maps, const 
         a2 = sp_ld(BP, 2 * CB + r * 256) - a2;
         a3 = sp_ld(BP, 3 * CB + r * 256) - a3;
       }
-      const bool oc = (xb & 32) != 0;  // output column
-      const bool v0 = oc && (IN || ((xb & 8) && (yb & 8))), v1 = oc && (IN || ((xb & 16) && (yb & 16))),
-                 v2 = oc && (IN || ((xb & 16) && (yb & 8)));
+      const bool v0 = IN || ((xb & 8) && (yb & 8)), v1 = IN || ((xb & 16) && (yb & 16)),
+                 v2 = IN || ((xb & 16) && (yb & 8));
       if (v0 && z < n2) Q.yp[0][(int64_t)r * (2 * (n0 + 1))] = a0;
       if (v1 && z < n2) Q.yp[1][(int64_t)r * (2 * n0)] = a1;
       if (v2) Q.yp[2][(int64_t)r * (2 * n0)] = a2;
