@@ -190,6 +190,9 @@ def ndofs(d):
     return c + sum(c // d[a] * (d[a] + 1) for a in range(3))
 
 
+FACTOR_SETS = {}  # level -> distinct factor entry sets when the factor dictionary is active (0: per-cell cache)
+
+
 def alg_bytes(kernel, n, level):
     """Algorithmic HBM bytes of one launch at a level (DESIGN.md §8(d));
     n = cube edge or the level-0 cell dims."""
@@ -202,6 +205,10 @@ def alg_bytes(kernel, n, level):
     if kernel == "apply":
         return 16 * 2 * N + 32 * C
     if kernel == "vanka_update":
+        if FACTOR_SETS.get(level, 0) > 0:
+            # factor dictionary: a 4-byte id per colour cell (the table of distinct entry sets stays
+            # on chip: FACTOR_SETS[level] x 208 bytes), r and x at the owned DOFs
+            return 4 * (C // 2) + 16 * (Nu + C // 2) + 2 * 16 * (Nu + C // 2)
         if os.environ.get("EHMG_VANKA_KCACHE", "0")[:1] == "1":
             # colour-half of the stiffness cache (12 reals of K + 1/s per cell), rho and gamma of every
             # cell once (the mass part of the local blocks is rebuilt from them), r and x at the owned DOFs
@@ -387,6 +394,8 @@ def run_b200(args, ws, rank, local):
     ms_max = max_over_ranks(ws, ms)
     value = ws * args.steps / (ms_max / 1e3)
 
+    for lv in range(mg.n_levels()):
+        FACTOR_SETS[lv] = mg.factor_sets(lv)
     # profile pass (same steps, per-launch events) -> dominant kernel
     E.profile_enable(True)
     for _ in range(args.steps):
@@ -544,6 +553,7 @@ def run_b200(args, ws, rank, local):
                                  "barrier (profiles/round2/ncu_stencil3d_sp82_residual.txt; DESIGN.md)"),
                      "avg_launch_ms": round(avg_ms, 4), "peak_source": peak_src},
         "kernels": kernels, "smoother_colour_pass_L0": smoother_pass, "clocks": clocks,
+        "vanka_factor_sets": {f"L{lv}": c for lv, c in sorted(FACTOR_SETS.items())},
     }
     if rank == 0 and ws == 1 and not args.no_cpu and args.workload == "c2":
         rate, kind, per, wall, lv = run_cpu_sample(1, 1, args.ref_cells)

@@ -146,6 +146,12 @@ int ehmg_multigrid_create(int ndim, const int* dims, double h, const double* lam
                           double omega, double alpha, const ehmg_mg_options* opt, ehmg_mg* out);
 int ehmg_multigrid_destroy(ehmg_mg mg);
 int ehmg_multigrid_n_levels(ehmg_mg mg);
+/* Number of distinct Vanka factor entry sets of a level when its colour
+ * updates read them through the factor dictionary (exact deduplication of
+ * vanka.hpp:72's per-cell cache: homogeneous regions, sponge depth classes);
+ * 0 when the level keeps the per-cell cache; -1 for a bad handle / level.
+ * No reference counterpart (measurement: the bytes one update moves). */
+int ehmg_multigrid_factor_sets(ehmg_mg mg, int level);
 int ehmg_multigrid_cycle(ehmg_mg mg, const double* b, double* x, int where);
 int ehmg_multigrid_precondition(ehmg_mg mg, const double* r, double* z, int where);
 /* multigrid.hpp:136 Multigrid::precondition applied to `count` right-hand

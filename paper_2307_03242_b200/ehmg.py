@@ -110,6 +110,7 @@ def lib():
                                             C.POINTER(vp)]
         L.ehmg_multigrid_destroy.argtypes = [vp]
         L.ehmg_multigrid_n_levels.argtypes = [vp]
+        L.ehmg_multigrid_factor_sets.argtypes = [vp, C.c_int]
         L.ehmg_multigrid_cycle.argtypes = [vp, vp, vp, C.c_int]
         L.ehmg_multigrid_precondition.argtypes = [vp, vp, vp, C.c_int]
         L.ehmg_multigrid_precondition_many.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
@@ -611,6 +612,11 @@ class Multigrid:
 
     def n_levels(self) -> int:
         return lib().ehmg_multigrid_n_levels(self._h)
+
+    def factor_sets(self, level: int = 0) -> int:
+        """Distinct Vanka factor entry sets of a level when its colour updates use the factor
+        dictionary (0: per-cell cache). No reference counterpart (measurement)."""
+        return lib().ehmg_multigrid_factor_sets(self._h, int(level))
 
     def coarse_kind(self) -> str:
         return "lu"

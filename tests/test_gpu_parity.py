@@ -259,3 +259,31 @@ def test_vanka_stiffness_cache_matches_uinv_cache(monkeypatch):
     zr = O.MG(dims, h, O.Media(lam, mu, rho, gam), 2 / 3, omega, 0.3, n_levels=3, cycle="v", nu1=2, nu2=2,
               damping=0.35).precondition(b)
     assert rel(z1, zr) < CYCLE_TOL
+
+
+def test_vanka_factor_dictionary_is_exact(monkeypatch):
+    """The factor dictionary (distinct factor entry sets of a level kept once, 4-byte id per cell:
+    homogeneous regions and sponge depth classes) is an exact deduplication: sweeps and cycles
+    are bit-identical to the per-cell cache, on media where it engages (homogeneous + sponge)
+    and on random media where every cell differs (it must then stay off)."""
+    dims = (32, 32, 32)
+    g = E.StaggeredGrid(dims, 1.0 / 32)
+    omega = 2 * np.pi * 32 / 10
+    par = E.OperatorParams(2 / 3, omega, 0.5)
+    opt = E.MgOptions(n_levels=3, cycle="v", nu1=2, nu2=2, damping=0.25, vanka_mode="full", sweep="red_black")
+    rng = np.random.default_rng(21)
+    b = rfield(rng, O.n_dofs(dims))
+    x0 = rfield(rng, O.n_dofs(dims))
+    hom = E.MediaModel.homogeneous(g, 2.0, 1.0, 1.0, 0.01)
+    hom.gamma = E.build_attenuation_profile(g, 0.01, E.SpongeConfig(6))
+    het = E.MediaModel(*rand_media(rng, dims))
+    for med in (hom, het):
+        out = []
+        for flag in ("0", "1"):
+            monkeypatch.setenv("EHMG_VANKA_DICT", flag)
+            D = E.make_opdata(g, med, par)
+            x = x0.copy()
+            E.VankaSmoother("full").sweep(D, b, x, 0.6, "red_black", nsweeps=2)
+            out.append((x, E.Multigrid(g, med, par, opt).precondition(b)))
+        assert np.array_equal(out[0][0], out[1][0])
+        assert np.array_equal(out[0][1], out[1][1])
