@@ -316,6 +316,9 @@ struct Smoother {
   // factor dictionary (complex128): id per colour cell + table of the distinct entry sets
   DBuf<unsigned> didx;
   DBuf<cplx> dtab;
+  DBuf<cplxf> dtabf;  // complex64 hierarchy
+  const cplx* dict_table(const cplx*) const { return dtab.p; }
+  const cplxf* dict_table(const cplxf*) const { return dtabf.p; }
   bool dict = false;
   int dict_sets = 0;
   // Deduplicate the compact cache when the level has few distinct entry sets
@@ -370,9 +373,13 @@ struct Smoother {
     res.release();
     ksoa.release();
     kpath = false;
-    didx.release();
+    if (dict) {  // the dictionary follows: the table rounded like the per-cell entries, same ids
+      dtabf.alloc(dtab.n);
+      k_convert<cplxf, cplx><<<grid_for(dtab.n, 148 * 64), kThreads, 0, s>>>(dtab.n, dtab.p, dtabf.p);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));
+    }
     dtab.release();
-    dict = false;
     resf.alloc(g.ndofs);
   }
   const cplx* cache(const cplx*) const { return soa.p; }
@@ -486,22 +493,23 @@ struct Smoother {
     }
     constexpr int nth = vk_threads<V>();
     const int nblk = (int)std::min<int64_t>((nt + nth - 1) / nth, 148 * 64);
-    if constexpr (sizeof(V) == sizeof(cplx)) {
-      if (dict) {
+    if (dict) {
 #ifndef EHMG_VKD_BLOCKS_PER_SM
 #define EHMG_VKD_BLOCKS_PER_SM 2
 #endif
-        const int nblk = (int)std::min<int64_t>((nt + nth - 1) / nth, 148 * EHMG_VKD_BLOCKS_PER_SM);
-        // (an L2 access-policy window pinning the table was measured: 0.81 vs 0.56 ms, so not used)
-        if (g.nd == 3)
-          (xzero ? k_vanka_update<3, V, true, true> : k_vanka_update<3, V, false, true>)<<<nblk, nth, 0, s>>>(
-              g, vk, full, cq, r, lc, w, x, didx.p, dtab.p);
-        else
-          (xzero ? k_vanka_update<2, V, true, true> : k_vanka_update<2, V, false, true>)<<<nblk, nth, 0, s>>>(
-              g, vk, full, cq, r, lc, w, x, didx.p, dtab.p);
-        CK(cudaGetLastError());
-        return;
-      }
+      // blocks resident per SM x EHMG_VKD_BLOCKS_PER_SM (complex128: one 384-thread block per SM)
+      const int nblk = (int)std::min<int64_t>((nt + nth - 1) / nth,
+                                              148 * EHMG_VKD_BLOCKS_PER_SM * (sizeof(V) == sizeof(cplx) ? 1 : 2));
+      const V* tab = dict_table(r);
+      // (an L2 access-policy window pinning the table was measured: 0.81 vs 0.56 ms, so not used)
+      if (g.nd == 3)
+        (xzero ? k_vanka_update<3, V, true, true> : k_vanka_update<3, V, false, true>)<<<nblk, nth, 0, s>>>(
+            g, vk, full, cq, r, lc, w, x, didx.p, tab);
+      else
+        (xzero ? k_vanka_update<2, V, true, true> : k_vanka_update<2, V, false, true>)<<<nblk, nth, 0, s>>>(
+            g, vk, full, cq, r, lc, w, x, didx.p, tab);
+      CK(cudaGetLastError());
+      return;
     }
     if (g.nd == 3)
       (xzero ? k_vanka_update<3, V, true> : k_vanka_update<3, V, false>)<<<nblk, nth, 0, s>>>(

@@ -264,8 +264,9 @@ def test_vanka_stiffness_cache_matches_uinv_cache(monkeypatch):
 def test_vanka_factor_dictionary_is_exact(monkeypatch):
     """The factor dictionary (distinct factor entry sets of a level kept once, 4-byte id per cell:
     homogeneous regions and sponge depth classes) is an exact deduplication: sweeps and cycles
-    are bit-identical to the per-cell cache, on media where it engages (homogeneous + sponge)
-    and on random media where every cell differs (it must then stay off)."""
+    are bit-identical to the per-cell cache -- complex128 and the complex64 hierarchy -- on media
+    where it engages (homogeneous + sponge) and on random media where every cell differs (it must
+    then stay off)."""
     dims = (32, 32, 32)
     g = E.StaggeredGrid(dims, 1.0 / 32)
     omega = 2 * np.pi * 32 / 10
@@ -284,6 +285,7 @@ def test_vanka_factor_dictionary_is_exact(monkeypatch):
             D = E.make_opdata(g, med, par)
             x = x0.copy()
             E.VankaSmoother("full").sweep(D, b, x, 0.6, "red_black", nsweeps=2)
-            out.append((x, E.Multigrid(g, med, par, opt).precondition(b)))
-        assert np.array_equal(out[0][0], out[1][0])
-        assert np.array_equal(out[0][1], out[1][1])
+            out.append((x, E.Multigrid(g, med, par, opt).precondition(b),
+                        E.Multigrid(g, med, par, opt, precision="mixed").precondition(b)))
+        for a, c in zip(out[0], out[1]):
+            assert np.array_equal(a, c)
