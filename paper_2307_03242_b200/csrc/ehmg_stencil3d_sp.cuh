@@ -18,17 +18,30 @@
 //    (warp * NY + r); outputs are the inner 14 x (NW*NY - 2) positions.
 //  * shared-memory planes stay interleaved complex128 as TMA delivers them:
 //    lane l reads the double at 8*l -- conflict-free, 256 B per warp load.
-//  * x neighbours of computed values by warp shuffles (two lanes away), y
-//    neighbours across threads through shared memory, z by register carries;
-//    the mass product reads both parts of its own value with one 16-byte
-//    load shared by the lane pair.
+//  * x neighbours of computed values by warp shuffles (two lanes away) -- those
+//    of the mass products and of p are read from shared memory, where the
+//    neighbour lanes stored them for their y neighbours anyway; y neighbours
+//    across threads through shared memory, z by register carries; the mass
+//    product reads the other part of its own value with one more load.
+//  * one ring slot holds everything of a plane (u, p, media, b, mass products):
+//    every load is LDS [thread offset + slot base + immediate].
+//  * tiles strictly inside the box run an instantiation of the step in which
+//    every x / y boundary flag is a compile-time constant and the z-dependent
+//    constants come from one table row per plane class (S3Params::zt) by
+//    uniform loads, premultiplied (beta c, w c); they are scheduled first so
+//    that neighbouring tiles march in step and share their halos in L2.
+//  * the per-plane TMA group is issued by warps 0..7 (one or two loads each,
+//    elect.sync) so no warp carries the whole issue sequence into the plane's
+//    barrier.
 //  * everything else as in k_stencil3d_rr: z-march with persistent CTAs over
 //    (tile, z-chunk) items, TMA plane rings one plane ahead with hardware
 //    zero fill for the reference's zero ghosts (operator.hpp:172), in-plane
 //    spreads carried as differences of per-plane spreads, one block barrier
 //    per plane, carries alternating between two register sets.
 // The operation order per value is that of k_stencil3d_rr (component-wise on
-// the parts), so results agree with it to the last bits.
+// the parts) except the premultiplied constants and the six-operation mass
+// product: results agree with it to 2.5e-16 relative. Measurements, the
+// instruction / pipe accounting and what was tried: DESIGN.md.
 #pragma once
 
 #include "ehmg_stencil3d_rr.cuh"
