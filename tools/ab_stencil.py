@@ -20,6 +20,7 @@ def main():
     ap.add_argument("libs", nargs="+")
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--homogeneous", action="store_true", help="constant media (uniform-media tile path)")
     ap.add_argument("--one", action="store_true", help="(internal) time one library in this process")
     ap.add_argument("--cmp", action="store_true", help="(internal) compare with the first library's output")
     a = ap.parse_args()
@@ -28,7 +29,7 @@ def main():
         import subprocess
         for i, path in enumerate(a.libs):
             subprocess.run([sys.executable, __file__, path, "--n", str(a.n), "--reps", str(a.reps), "--one"]
-                           + (["--cmp"] if i else []), check=False)
+                           + (["--cmp"] if i else []) + (["--homogeneous"] if a.homogeneous else []), check=False)
         return
     n = a.n
     nc = n ** 3
@@ -37,6 +38,8 @@ def main():
     mu = rng.uniform(0.8, 1.2, nc)
     rho = rng.uniform(0.8, 1.2, nc)
     gam = 0.01 * rng.uniform(0.5, 1.5, nc)
+    if a.homogeneous:
+        lam, mu, rho, gam = np.full(nc, 2.0), np.ones(nc), np.ones(nc), np.full(nc, 0.01)
     y_ref = None
     dims = (C.c_int * 3)(n, n, n)
     dp = lambda v: v.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
