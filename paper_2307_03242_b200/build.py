@@ -34,6 +34,8 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    if os.environ.get("EHMG_B200_LIB"):
+        return LIB  # an A/B build chosen by the caller: never rebuilt here
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
